@@ -1,0 +1,403 @@
+#!/usr/bin/env python
+"""bench.py -- packets/s of one detection window (scan + estimate + restore + filter).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+Workload (BASELINE.json configs[1]): default DDH parameters (r=5, g=1024, k=14,
+alpha=6), theta 1024, a 100M-packet window per GPU: 150k uniform-address
+background hosts with Zipf(1.5) cardinalities capped at 256 plus 50 injected
+scanners with 2048..8192 destinations (~3.8M distinct flows), every packet a
+uniform draw from the flow table (so ~26 packets per flow, shuffled).  A "step"
+is one whole window: reset the sketch, scan every packet, (N > 1: OR-merge the
+per-GPU sketches), estimate, restore and threshold-filter the super points.
+
+One JSON line on rank 0 (see the keys below).  `value` is device-resident
+throughput; `e2e` pushes the same window from pinned HOST arrays through the
+public API (`Dhla.update_batch(numpy)` -> C ABI), host<->device copies inside
+the timed region.  `--impl reference` times the reference's own compiled CPU
+loops (oracle/_ref, or the oracle port when that is absent) on the host cores.
+"""
+from __future__ import annotations
+
+import argparse
+import concurrent.futures
+import hashlib
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+THETA = 1024
+WORKLOAD = ("config2: 100M-packet window per GPU, default DDH (r5 g1024 k14 a6), 150k uniform background hosts "
+            "(Zipf1.5 cardinality<=256) + 50 scanners (2048-8192), ~3.8M distinct flows, theta 1024")
+
+
+# ------------------------------------------------------------------ workload --
+
+def make_flows(seed: int, background_hosts: int = 150_000, scanners: int = 50):
+    """Distinct (src, dst) flows of the window: the reference generator's population shape
+    (/root/reference/pkg/src/dhsa/ingest.py:109-131) at config-2 scale."""
+    rng = np.random.default_rng(seed)
+    n_hosts = background_hosts + scanners
+    hosts = np.unique(rng.integers(0, 2 ** 32, size=n_hosts + n_hosts // 32 + 64, dtype=np.uint64))
+    rng.shuffle(hosts)
+    hosts = hosts[:n_hosts]
+    cards = np.empty(n_hosts, dtype=np.int64)
+    cards[:background_hosts] = np.minimum(rng.zipf(1.5, size=background_hosts), 256)
+    cards[background_hosts:] = rng.integers(2048, 8193, size=scanners)
+    src = np.repeat(hosts, cards)
+    bases = rng.integers(0, 2 ** 32, size=n_hosts, dtype=np.uint64)
+    starts = np.repeat(np.cumsum(cards) - cards, cards).astype(np.uint64)
+    dst = (np.repeat(bases, cards) + np.arange(len(src), dtype=np.uint64) - starts) & np.uint64(0xFFFFFFFF)
+    return src.astype(np.uint32), dst.astype(np.uint32), hosts[background_hosts:].astype(np.uint32)
+
+
+def sha(a) -> str:
+    return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()
+
+
+# -------------------------------------------------------------------- clocks --
+
+class ClockSampler:
+    """Samples SM clock and throttle reasons while the timed region runs."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index, self.rows, self.proc = index, [], None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._pump, daemon=True)
+            self.thread.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _pump(self):
+        for line in self.proc.stdout:
+            self.rows.append([c.strip() for c in line.split(",")])
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            time.sleep(0.15)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self) -> dict:
+        sm, mx, reasons = [], [], set()
+        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+        for row in self.rows:
+            try:
+                sm.append(float(row[0]))
+                mx.append(float(row[1]))
+            except (ValueError, IndexError):
+                continue
+            for name, cell in zip(names, row[3:7]):
+                if cell.lower().startswith("active"):
+                    reasons.add(name)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": float(max(mx)),
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ---------------------------------------------------------------- CPU baseline --
+
+def cpu_reference_window(cand: np.ndarray, opp: np.ndarray, threads: int):
+    """One window on the host cores with the reference's own compiled loops when
+    oracle/_ref holds them (kind "reference"), else the oracle's C port ("port").
+    Mirrors `dhsa bench` (/root/reference/pkg/src/dhsa/cli.py:371-382): batches of
+    65536 pairs handed to a thread pool sharing one sketch, seal, then restore."""
+    from oracle import oracle as O
+
+    core = O.load_ref_core()
+    ora = O.OracleSketch()
+    t0 = time.perf_counter()
+    if core is not None:
+        kind = "reference"
+        mu = 65536  # engine.py:22 DEFAULT_BATCH_PAIRS
+        with concurrent.futures.ThreadPoolExecutor(max_workers=threads) as pool:
+            futs = [pool.submit(core.update_batch, ora.bits, ora.state_dh0, ora.state_h1, ora.k, ora.alpha,
+                                cand[s:s + mu], opp[s:s + mu]) for s in range(0, len(cand), mu)]
+            for f in futs:
+                f.result()
+    else:
+        kind = "port"
+        ora.update_batch(cand, opp, threads=threads)
+    t_scan = time.perf_counter() - t0
+    reports = ora.restore_superpoints(THETA)  # the reference's restore is pure Python: timed via the C port
+    t_all = time.perf_counter() - t0
+    return kind, t_scan, t_all, reports
+
+
+def run_reference(args, rank: int) -> None:
+    if rank != 0:
+        return
+    src, dst, _ = make_flows(args.seed)
+    threads = os.cpu_count() or 1
+    n = min(args.packets, args.cpu_sample)
+    rng = np.random.default_rng(args.seed + 1)
+    pick = rng.integers(0, len(src), size=n)
+    cand, opp = src[pick], dst[pick]
+    times = []
+    kind = "port"
+    for it in range(args.warmup + args.steps):
+        kind, _, t_all, _ = cpu_reference_window(cand, opp, threads)
+        if it >= args.warmup:
+            times.append(t_all)
+    total = sum(times)
+    mpps = n * len(times) / total / 1e6
+    sample = f"{n} packets drawn from the same flow table ({len(src)} flows), {threads} threads, batches of 65536"
+    print(json.dumps({
+        "impl": "reference", "metric": "packets/sec per detection window (scan+estimate+restore)",
+        "value": mpps, "unit": "Mpps", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * total / len(times), "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "u32/u64 integer hashing + f64 estimates", "data": "synthetic",
+        "config": {"workload": WORKLOAD, "sample_packets": n, "theta": THETA},
+        "cpu_baseline": {"value": mpps, "unit": "Mpps", "cores": threads, "kind": kind, "sample": sample},
+        "e2e": {"value": mpps, "unit": "Mpps", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }), flush=True)
+
+
+# ------------------------------------------------------------------- GPU arm --
+
+def run_ours(args, rank: int, local_rank: int, world: int) -> None:
+    import torch
+    import torch.distributed as dist
+
+    import paper_1803_11449_b200 as P
+    from paper_1803_11449_b200 import _cabi
+    from paper_1803_11449_b200.multi import ShardedWindow
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    n = args.packets
+    src, dst, scanners = make_flows(args.seed)
+    flows = len(src)
+    gen = torch.Generator(device=dev)
+    gen.manual_seed(args.seed * 1000 + rank)
+    src_d = torch.from_numpy(src.view(np.int32)).to(dev)
+    dst_d = torch.from_numpy(dst.view(np.int32)).to(dev)
+    pick = torch.randint(0, flows, (n,), device=dev, generator=gen)
+    if rank == 0 and n >= flows:
+        pick[:flows] = torch.arange(flows, device=dev)  # the window contains every flow at least once
+        pick = pick[torch.randperm(n, device=dev, generator=gen)]
+    cand_d, opp_d = src_d[pick].contiguous(), dst_d[pick].contiguous()
+    del pick
+    torch.cuda.synchronize()
+
+    win = ShardedWindow(P.DhgParams(), theta=THETA, device=local_rank, merge=args.merge)
+    sk = win.sketch
+    sk.set_scan_mode(args.scan_mode)
+    stream = torch.cuda.current_stream(dev)
+    sk.use_stream(stream.cuda_stream)
+
+    # -- roofline inputs measured here: random-address L2 rates (rank 0, N = 1 only)
+    l2 = None
+    if rank == 0 and world == 1 and not args.no_probe:
+        import ctypes as C
+        rates = {}
+        for kind, name in ((0, "red"), (1, "ld")):
+            out = C.c_double()
+            _cabi.check(_cabi.lib().dhsa_probe_l2(local_rank, kind, 16 << 20, 1 << 28, C.byref(out)))
+            rates[name] = out.value / 1e9
+        l2 = {"buffer_mib": 16, "red_gops": rates["red"], "ld_gops": rates["ld"]}
+
+    def step_device(events=None):
+        if events:
+            events[0].record(stream)
+        win.reset()
+        win.scan(cand_d, opp_d)
+        if events:
+            events[1].record(stream)
+        win.merge()
+        reports = win.restore()
+        if events:
+            events[2].record(stream)
+        return reports
+
+    # -- warm-up, then parity of what the timed steps compute (not timed)
+    for _ in range(args.warmup):
+        reports = step_device()
+    parity = None
+    if rank == 0 and not args.no_parity:
+        from oracle import oracle as O
+        ora = O.OracleSketch()
+        ora.update_batch(src, dst, threads=os.cpu_count() or 1)
+        want = ora.restore_superpoints(THETA)
+        bits_ok = (n * world >= flows) and sha(sk.bits) == sha(ora.bits)
+        sp_ok = [(r.host, r.saturated) for r in reports] == [(r.host, r.saturated) for r in want] and \
+            all(abs(a.estimate - b.estimate) <= 1e-6 * abs(b.estimate) for a, b in zip(reports, want))
+        parity = {"bits_equal_oracle": bool(bits_ok), "superpoints_equal_oracle": bool(sp_ok),
+                  "n_superpoints": len(reports),
+                  "scanners_found": int(len(set(scanners.tolist()) & {r.host for r in reports}))}
+
+    # -- timed: device-resident window
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(args.steps)]
+    t_begin, t_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    launches0 = sk.launch_count
+    with ClockSampler(local_rank) as clocks:
+        barrier()
+        t_begin.record(stream)
+        for k in range(args.steps):
+            reports = step_device(evs[k])
+        t_end.record(stream)
+        barrier()
+    launches = sk.launch_count - launches0
+    ms_total = t_begin.elapsed_time(t_end)
+    scan_ms = float(np.mean([e[0].elapsed_time(e[1]) for e in evs]))
+    readout_ms = float(np.mean([e[1].elapsed_time(e[2]) for e in evs]))
+
+    # -- timed: end to end from pinned host arrays through the public API
+    e2e = None
+    if not args.no_e2e:
+        cand_h = torch.empty(n, dtype=torch.int32, pin_memory=True)
+        opp_h = torch.empty(n, dtype=torch.int32, pin_memory=True)
+        cand_h.copy_(cand_d)
+        opp_h.copy_(opp_d)
+        torch.cuda.synchronize()
+        cand_np, opp_np = cand_h.numpy().view(np.uint32), opp_h.numpy().view(np.uint32)
+
+        def step_host():
+            win.reset()
+            win.scan(cand_np, opp_np)   # Dhla.update_batch(numpy): chunked H2D overlapped with the scan
+            win.merge()
+            return win.restore()        # reports come back to host memory
+
+        for _ in range(max(1, min(args.warmup, 2))):
+            step_host()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        barrier()
+        e0.record(stream)
+        for _ in range(args.steps):
+            reports_h = step_host()
+        e1.record(stream)
+        barrier()
+        e2e_ms = e0.elapsed_time(e1)
+        e2e = (e2e_ms, len(reports_h))
+        del cand_h, opp_h
+
+    # -- max over ranks
+    stats = torch.tensor([ms_total, scan_ms, readout_ms, e2e[0] if e2e else 0.0], device=dev, dtype=torch.float64)
+    if world > 1:
+        dist.all_reduce(stats, op=dist.ReduceOp.MAX)
+    ms_total, scan_ms, readout_ms, e2e_ms = (float(v) for v in stats.tolist())
+
+    if rank == 0:
+        peaks_path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+        if os.path.exists(peaks_path):
+            peak, peak_src = float(json.load(open(peaks_path))["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+        else:
+            peak, peak_src = 6650.0, "fallback (B200_PROFILING.md)"
+        achieved = 8.0 * n / (scan_ms * 1e-3) / 1e9
+        roofline = {
+            "bound": "hbm", "kernel": f"k_scan_vec4<5,{P.dhla.SCAN_MODES.get(args.scan_mode, args.scan_mode)}>",
+            "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+            "peak_source": peak_src, "algorithmic_bytes_per_packet": 8,
+            "launch_ms": scan_ms, "packets_per_launch": n, "scan_gpps": n / (scan_ms * 1e-3) / 1e9,
+            "traffic": args.traffic_bytes,
+        }
+        if l2:
+            # the second ceiling of the north star: sketch traffic at the measured random-address L2 rates
+            roofline["l2_probe"] = l2
+            roofline["l2_red_ceiling_gpps"] = l2["red_gops"] / 5.0
+            roofline["l2_ld_ceiling_gpps"] = l2["ld_gops"] / 5.0
+            binding = min(peak / 8.0, l2["ld_gops"] / 5.0)
+            roofline["binding_ceiling_gpps"] = binding
+            roofline["frac_of_binding_ceiling"] = roofline["scan_gpps"] / binding
+        value = world * n * args.steps / (ms_total * 1e-3) / 1e6
+        line = {
+            "metric": "packets/sec per detection window (scan+estimate+restore)",
+            "value": value, "unit": "Mpps", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": ms_total / args.steps, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "u32/u64 integer hashing + f64 estimates", "data": "synthetic",
+            "config": {"workload": WORKLOAD, "packets_per_gpu": n, "distinct_flows": flows, "theta": THETA,
+                       "scan_mode": args.scan_mode, "merge": win.merged_with,
+                       "l2": "inputs (800 MB per GPU) larger than L2; sketch (10 MiB) L2-resident by design"},
+            "phase_ms": {"scan": scan_ms, "merge+estimate+restore+filter": readout_ms},
+            "roofline": roofline,
+            "gpu_launches": int(launches),
+            "clocks": clocks.summary(),
+        }
+        if parity:
+            line["parity"] = parity
+        if e2e:
+            reports_bytes = 24 * e2e[1] + 1584  # dhsa_report_t rows + the control block read back per window
+            line["e2e"] = {"value": world * n * args.steps / (e2e_ms * 1e-3) / 1e6, "unit": "Mpps",
+                           "h2d_bytes_per_step": 8 * n, "d2h_bytes_per_step": reports_bytes,
+                           "ms_per_step": e2e_ms / args.steps}
+        if world == 1 and not args.no_cpu_baseline:
+            m = min(n, args.cpu_sample)
+            cand_s = cand_d[:m].cpu().numpy().view(np.uint32)
+            opp_s = opp_d[:m].cpu().numpy().view(np.uint32)
+            threads = os.cpu_count() or 1
+            kind, t_scan, t_all, _ = cpu_reference_window(cand_s, opp_s, threads)
+            line["cpu_baseline"] = {
+                "value": m / t_all / 1e6, "unit": "Mpps", "cores": threads, "kind": kind,
+                "scan_only_mpps": m / t_scan / 1e6,
+                "sample": f"first {m} packets of the same window, {threads} threads sharing one sketch, "
+                          f"batches of 65536 (restore timed via the oracle's C port)"}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def main() -> None:
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--packets", type=int, default=100_000_000, help="packets per GPU per window")
+    ap.add_argument("--seed", type=int, default=100)
+    ap.add_argument("--scan-mode", default="test_agg", choices=["red", "test", "test_agg"])
+    ap.add_argument("--merge", default="auto", choices=["auto", "p2p", "allgather"])
+    ap.add_argument("--cpu-sample", type=int, default=50_000_000)
+    ap.add_argument("--traffic-bytes", type=float, default=None,
+                    help="dram bytes per scan launch from the committed ncu capture (profiles/)")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-parity", action="store_true")
+    ap.add_argument("--no-probe", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if args.impl == "reference":
+        run_reference(args, rank)
+        return
+    if world != args.gpus and world == 1 and args.gpus > 1:
+        print(json.dumps({"error": f"--gpus {args.gpus} needs torchrun with {args.gpus} ranks"}), flush=True)
+        sys.exit(2)
+    run_ours(args, rank, local_rank, world)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,186 @@
+/*
+ * dhsa_b200.h -- C ABI of the B200-native super point detector hot path.
+ *
+ * One shared library (paper_1803_11449_b200/csrc -> libdhsa_b200.so, sm_100a)
+ * exports exactly the entry points below.  They are what the reference's FFI for
+ * this path would bind: each one names the reference interface it replaces
+ * (paths relative to /root/reference).  Plain pointers and sizes only -- no
+ * torch, numpy or C++ types cross this boundary.  The reference-side binding
+ * (a ctypes stub that plugs a GPU sketch into dhsa.engine.WindowSession) is shown
+ * in INTEGRATION.md.
+ *
+ * Conventions
+ *   - Every function returns int: 0 ok; 2 config error; 3 data error; 4 capacity
+ *     error -- the reference CLI's exit-code classes (pkg/src/dhsa/errors.py:1-5,
+ *     pkg/src/dhsa/cli.py:26,33-46); negative = -(1000 + cudaError_t).  Nothing
+ *     throws.  dhsa_last_error() returns a thread-local message for the last
+ *     non-zero return on the calling thread.
+ *   - "_host" pointers are ordinary host memory owned by the caller; pinned
+ *     (page-locked) memory is detected and DMA'd directly.  "_dev" pointers are
+ *     device memory on the sketch's device.  The caller may free its inputs as
+ *     soon as a call returns (pkg/src/dhsa/engine.py:78-86 hands in views).
+ *   - A sketch is thread-safe: concurrent calls on one handle are serialised and
+ *     stream-ordered (the reference updates one sketch from a thread pool,
+ *     pkg/src/dhsa/engine.py:81-86).  Read-out calls see every update issued
+ *     before them; dhsa_seal() is the barrier (pkg/src/dhsa/engine.py:89-94).
+ *   - Bit layout of the sketch is the reference's snapshot layout: arrays in
+ *     order, cells in index order, g/8 bytes per cell, bit b of a cell at bit b%8
+ *     of byte b/8 (pkg/src/dhsa/estimator.py:3-5, pkg/src/dhsa/dhla.py:64-67).
+ */
+#ifndef DHSA_B200_H
+#define DHSA_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define DHSA_ABI_VERSION 1
+
+#define DHSA_OK 0
+#define DHSA_ECONFIG 2   /* ConfigError    pkg/src/dhsa/errors.py:12 */
+#define DHSA_EDATA 3     /* DataError      pkg/src/dhsa/errors.py:16 */
+#define DHSA_ECAPACITY 4 /* CapacityError  pkg/src/dhsa/errors.py:20 */
+
+/* Scan kernel variants (dhsa_set_scan_mode). */
+#define DHSA_SCAN_RED_ONLY 0      /* one atomic OR per (packet, array), unconditionally        */
+#define DHSA_SCAN_TEST_RED 1      /* load the word, atomic only if the bit is still clear      */
+#define DHSA_SCAN_TEST_AGG_RED 2  /* as 1, and lanes of a warp hitting one word merge first    */
+
+typedef struct dhsa_sketch dhsa_sketch_t; /* opaque; replaces dhsa.dhla.Dhla, pkg/src/dhsa/dhla.py:57-68 */
+
+/* The validated parameter record, replaces DhgParams (pkg/src/dhsa/dhg.py:59-118).
+ * state_* are the post-tag states: state_dh0 = mix64(seed_dh0 ^ 0x9E3779B97F4A7C15),
+ * state_h1 = mix64(seed_h1 ^ 0xD1B54A32D192ED03) (dhg.py:29-30,112-118). */
+typedef struct {
+    int32_t r;
+    int32_t g;
+    int32_t k;
+    int32_t alpha;
+    int32_t key_width;
+    int32_t reserved;
+    uint64_t state_dh0;
+    uint64_t state_h1;
+} dhsa_params_t;
+
+/* One reported super point, replaces SuperPointReport (pkg/src/dhsa/dhla.py:50-54). */
+typedef struct {
+    uint64_t host;
+    double estimate;
+    int32_t saturated;
+    int32_t shared_zero_count; /* SZ before the saturation clamp (dhla.py:183) */
+} dhsa_report_t;
+
+/* Everything else one read-out produced. */
+typedef struct {
+    uint64_t n_candidates;     /* verified, distinct keys (dhla.py:213-217)                 */
+    uint64_t n_reports;        /* keys with estimate >= theta (dhla.py:190-194)             */
+    int32_t fail_stage;        /* 0, or the stage number of the CapacityError text          */
+    int32_t flow_saturated;    /* estimator.py:31                                           */
+    uint64_t fail_count;       /* survivor count of the failing stage (dhla.py:270-273)     */
+    double flow_count;         /* dhla.py:121-128                                           */
+    double psi;                /* dhla.py:130-134                                           */
+    double denom;              /* g (1 - psi^r), dhla.py:184                                */
+    uint64_t hot_counts[64];   /* |HE(i)|, dhla.py:111-119                                  */
+    uint64_t stage_counts[64]; /* survivors after stage 1, 2, ... (r - 2 entries)           */
+    int64_t zero_totals[64];   /* ZR(i), dhla.py:126                                        */
+} dhsa_restore_info_t;
+
+int dhsa_abi_version(void);
+const char *dhsa_last_error(void);
+
+/* ---- lifetime ---------------------------------------------------------------- */
+
+/* Dhla(params) -- allocate and zero r * 2^k * g/8 bytes on `device`
+ * (pkg/src/dhsa/dhla.py:60-68).  Re-validates the DhgParams rules
+ * (pkg/src/dhsa/dhg.py:78-105) -> DHSA_ECONFIG. */
+int dhsa_create(const dhsa_params_t *params, int device, dhsa_sketch_t **out);
+int dhsa_destroy(dhsa_sketch_t *s);
+/* Dhla.reset (pkg/src/dhsa/dhla.py:97-99). */
+int dhsa_reset(dhsa_sketch_t *s);
+/* Dhla.memory_bytes (pkg/src/dhsa/dhla.py:74-76). */
+int dhsa_sketch_bytes(const dhsa_sketch_t *s, uint64_t *nbytes);
+/* Device address of the bit array (for peers, snapshots, torch views). */
+int dhsa_bits_device_ptr(dhsa_sketch_t *s, void **bits_dev);
+/* Launch stream: NULL selects the sketch's own stream (the default). */
+int dhsa_set_stream(dhsa_sketch_t *s, void *cuda_stream);
+int dhsa_get_stream(dhsa_sketch_t *s, void **cuda_stream);
+int dhsa_set_scan_mode(dhsa_sketch_t *s, int mode);
+/* Kernel launches issued through this handle so far (bench.py's gpu_launches). */
+int dhsa_launch_count(const dhsa_sketch_t *s, uint64_t *n);
+
+/* ---- scan: Backend.update_batch / Dhla.update_batch ------------------------------
+ * (pkg/src/dhsa/_core.pyx:52-86, pkg/src/dhsa/_pykernels.py:29-55,
+ *  pkg/src/dhsa/dhla.py:87-95).  For every t < n set bit h1(opp[t]) in cell
+ *  (i, idx_i(cand[t])) of every array i. */
+int dhsa_update_device(dhsa_sketch_t *s, const uint32_t *cand_dev, const uint32_t *opp_dev,
+                       uint64_t n);
+int dhsa_update_host(dhsa_sketch_t *s, const uint32_t *cand_host, const uint32_t *opp_host,
+                     uint64_t n);
+/* WindowSession.seal's barrier (pkg/src/dhsa/engine.py:89-94): drain the stream. */
+int dhsa_seal(dhsa_sketch_t *s);
+
+/* ---- the `bits` attribute (pkg/src/dhsa/dhla.py:64-67; written directly by
+ *      pkg/src/dhsa/dhla.py:372 and pkg/tests/test_dhla.py:88-90) ----------------- */
+int dhsa_download_bits(dhsa_sketch_t *s, uint8_t *bits_host, uint64_t nbytes);
+int dhsa_upload_bits(dhsa_sketch_t *s, const uint8_t *bits_host, uint64_t nbytes);
+
+/* ---- read-out ---------------------------------------------------------------- */
+
+/* Backend.zero_counts / Dhla.zero_counts (pkg/src/dhsa/_core.pyx:89-118,
+ * pkg/src/dhsa/dhla.py:103-105): zc_host = int64 (r, 2^k); zr_host (optional) =
+ * per-array totals ZR(i) (pkg/src/dhsa/dhla.py:126). */
+int dhsa_zero_counts(dhsa_sketch_t *s, int64_t *zc_host, int64_t *zr_host);
+/* Dhla.hot_sets (pkg/src/dhsa/dhla.py:111-119, hot_threshold :45-47): row i of
+ * lists_host (r x 2^k u64) holds counts_host[i] ascending indices. */
+int dhsa_hot_sets(dhsa_sketch_t *s, double theta, uint64_t *lists_host, uint64_t *counts_host);
+/* Dhla.estimate_flow_count + bit_set_probability (pkg/src/dhsa/dhla.py:121-134) with the
+ * hot-set sizes for `theta`: fills zero_totals, hot_counts, flow_count, flow_saturated,
+ * psi and denom of *info. */
+int dhsa_estimate(dhsa_sketch_t *s, double theta, dhsa_restore_info_t *info);
+/* Dhla._candidate_hosts (pkg/src/dhsa/dhla.py:198-217 with _stage_first :252-274 and
+ * _stage_next :277-299): ascending distinct verified keys.  DHSA_ECAPACITY with
+ * info->fail_stage / fail_count when a stage exceeds max_candidates. */
+int dhsa_candidate_hosts(dhsa_sketch_t *s, double theta, uint64_t max_candidates,
+                         uint64_t *hosts_host, uint64_t hosts_cap, dhsa_restore_info_t *info);
+/* Dhla.shared_zero_counts (pkg/src/dhsa/dhla.py:136-143). */
+int dhsa_shared_zero_counts(dhsa_sketch_t *s, const uint64_t *hosts_host, uint64_t n,
+                            int64_t *sz_host);
+/* Dhla.restore_superpoints (pkg/src/dhsa/dhla.py:164-196): reports sorted by
+ * (-estimate, host).  reports_host holds reports_cap entries; info->n_reports is
+ * the true count (DHSA_EDATA if it exceeds reports_cap). */
+int dhsa_restore(dhsa_sketch_t *s, double theta, uint64_t max_candidates,
+                 dhsa_report_t *reports_host, uint64_t reports_cap, dhsa_restore_info_t *info);
+
+/* ---- merge: dhsa.dhla.merge (pkg/src/dhsa/dhla.py:305-318) ------------------------ */
+
+/* dst |= src; both handles in this process (same or peer device).  Parameter
+ * mismatch -> DHSA_ECONFIG (pkg/src/dhsa/dhla.py:312-315). */
+int dhsa_or_merge(dhsa_sketch_t *dst, dhsa_sketch_t *src);
+/* dst[byte_lo:byte_hi) |= each peer_bits_dev[p][byte_lo:byte_hi) -- the
+ * reduce-scatter-with-OR step of the multi-GPU merge, reading peers over
+ * NVLink (peer or IPC-mapped pointers).  byte_lo / byte_hi are multiples of 16. */
+int dhsa_or_merge_peers(dhsa_sketch_t *dst, const void *const *peer_bits_dev, int n_peers,
+                        uint64_t byte_lo, uint64_t byte_hi);
+/* dst[byte_lo:byte_hi) = peer_bits_dev[byte_lo:byte_hi) -- the all-gather step. */
+int dhsa_copy_slice_from_peer(dhsa_sketch_t *dst, const void *peer_bits_dev, uint64_t byte_lo,
+                              uint64_t byte_hi);
+/* dst |= bits_dev (a whole sketch image already on this device, e.g. one slot of an
+ * NCCL all-gather buffer). */
+int dhsa_or_merge_buffer(dhsa_sketch_t *dst, const void *bits_dev, uint64_t nbytes);
+/* CUDA IPC plumbing so one-process-per-GPU ranks can map each other's bit arrays. */
+int dhsa_ipc_export(dhsa_sketch_t *s, uint8_t handle_out[64]);
+int dhsa_ipc_open(int device, const uint8_t handle[64], void **bits_dev);
+int dhsa_ipc_close(int device, void *bits_dev);
+
+/* ---- measurement -------------------------------------------------------------
+ * Random-address L2 probe used for the scan roofline: `ops` 32-bit operations at
+ * hashed word addresses inside a `buffer_bytes` buffer.  kind 0 = atomic OR
+ * (RED), 1 = load.  Returns the rate in operations per second. */
+int dhsa_probe_l2(int device, int kind, uint64_t buffer_bytes, uint64_t ops, double *ops_per_sec);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* DHSA_B200_H */

@@ -1,0 +1,801 @@
+// dhsa_device.cuh -- sm_100a kernels of the super point detector hot path.
+//
+// Written from the algorithm's definition for B200; the reference citations
+// (paths relative to /root/reference) say which reference behaviour each kernel
+// reproduces bit for bit, not where code came from -- the reference has no GPU
+// code at all.
+//
+// Data layout in HBM
+//   bits    r * 2^k cells of g bits, the reference's snapshot layout
+//           (pkg/src/dhsa/dhla.py:64-67, estimator.py:3-5).  Kernels view it as
+//           little-endian 32-bit words: global bit B = cell * g + b lives at bit
+//           B & 31 of word B >> 5, which is bit b % 8 of byte b / 8 of the cell.
+//   cand/opp  SoA uint32 packet stream, 8 B per packet, read once.
+//
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace dhsa {
+
+struct DevParams {
+    int r, k, alpha, log2g, key_width;
+    uint32_t kmask;  // 2^k - 1
+    uint32_t gmask;  // g - 1
+    uint64_t state_dh0, state_h1;
+    uint64_t ncell;   // r * 2^k
+    uint64_t nwords;  // 32-bit words backing the bit array (allocation is padded to 16 B)
+};
+
+// Device-resident control block of one read-out: every stage kernel reads its
+// trip counts from here, so the whole chain is stream-ordered with no host sync.
+struct Control {
+    unsigned long long hot_counts[64];
+    unsigned long long stage_counts[64];  // survivors after stage 1, 2, ...
+    long long zero_totals[64];            // ZR(i)
+    unsigned long long n_candidates;
+    unsigned long long n_reports;
+    unsigned long long fail_count;
+    int fail_stage;
+    int flow_saturated;
+    int any_empty;  // some hot set is empty -> no candidates (dhla.py:208-209)
+    int sorted;     // reports/candidates were sorted on the device by the single-CTA sorter
+    double flow_count, psi, denom;
+};
+
+// ------------------------------------------------------------------ hashing --
+
+// splitmix64 finaliser: pkg/src/dhsa/dhg.py:36-44, pkg/src/dhsa/_core.pyx:35-40.
+__device__ __forceinline__ uint64_t mix64(uint64_t z)
+{
+    z ^= z >> 30;
+    z *= 0xBF58476D1CE4E5B9ULL;
+    z ^= z >> 27;
+    z *= 0x94D049BB133111EBULL;
+    z ^= z >> 31;
+    return z;
+}
+
+// dh0: pkg/src/dhsa/dhg.py:126-128
+__device__ __forceinline__ uint32_t dh0_of(const DevParams &p, uint64_t a)
+{
+    return (uint32_t)mix64(p.state_dh0 ^ a) & p.kmask;
+}
+
+// index of key `a` in array i given d0 = dh0(a): pkg/src/dhsa/dhg.py:131-139,152-158
+__device__ __forceinline__ uint32_t index_of(const DevParams &p, uint64_t a, uint32_t d0, int i)
+{
+    return i == 0 ? d0 : (((uint32_t)(a >> ((i - 1) * p.alpha)) & p.kmask) ^ d0);
+}
+
+// ---------------------------------------------------------- memory helpers --
+
+// Packet stream: read once, 16 B per lane, kept out of L1 and first in line for
+// L2 eviction so it never displaces the sketch.  (On sm_100a the direct
+// .L2::evict_first qualifier exists only for 32-byte loads, so the priority is
+// passed as a cache-policy operand.)
+__device__ __forceinline__ uint64_t policy_evict_first()
+{
+    uint64_t pol;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+    return pol;
+}
+
+__device__ __forceinline__ uint64_t policy_evict_last()
+{
+    uint64_t pol;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+    return pol;
+}
+
+__device__ __forceinline__ uint4 ld_stream_v4(const uint4 *ptr, uint64_t pol)
+{
+    uint4 v;
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.u32 {%0,%1,%2,%3}, [%4], %5;"
+                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+                 : "l"(ptr), "l"(pol));
+    return v;
+}
+
+__device__ __forceinline__ uint32_t ld_stream_u32(const uint32_t *ptr, uint64_t pol)
+{
+    uint32_t v;
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.u32 %0, [%1], %2;"
+                 : "=r"(v)
+                 : "l"(ptr), "l"(pol));
+    return v;
+}
+
+// Sketch word test-load.  L1 may serve it: bits only ever go 0 -> 1 inside a
+// window and L1 is invalidated at every launch, so a stale line can only show a
+// set bit as clear, which costs one redundant (idempotent) atomic, never a miss.
+__device__ __forceinline__ uint32_t ld_sketch(const uint32_t *ptr)
+{
+    uint32_t v;
+    asm volatile("ld.global.ca.u32 %0, [%1];" : "=r"(v) : "l"(ptr) : "memory");
+    return v;
+}
+
+// Fire-and-forget atomic OR (SASS: RED.E.OR), resolved in the L2 slice that owns the word.
+__device__ __forceinline__ void red_or(uint32_t *ptr, uint32_t m)
+{
+    asm volatile("red.relaxed.gpu.global.or.b32 [%0], %1;" ::"l"(ptr), "r"(m) : "memory");
+}
+
+// --------------------------------------------------------------- K1: scan --
+//
+// Backend.update_batch (pkg/src/dhsa/_core.pyx:75-86): for each packet, bit
+// h1(opp) of cell (i, idx_i(cand)) for every array i.
+//
+// Fast path: 4 packets per lane per trip (two 16-byte loads), R arrays
+// unrolled, 32-bit word addressing (g >= 32, sketch < 16 GiB).  All 4*R test
+// loads of a lane are issued before the first is consumed, so each lane keeps
+// up to 20 L2 requests in flight.
+//
+//   MODE 0  one RED per (packet, array), unconditionally
+//   MODE 1  test the word first; RED only where the bit is still clear
+//           (Alg. 1's "if the bit is 1, continue")
+//   MODE 2  as 1, plus warp aggregation: lanes that still need a RED vote,
+//           __match_any_sync groups them by word, masks are OR-ed inside a
+//           group and its lowest lane issues one RED.
+template <int R, int MODE>
+__global__ void __launch_bounds__(256) k_scan_vec4(const uint4 *__restrict__ cand4,
+                                                   const uint4 *__restrict__ opp4, uint64_t nvec,
+                                                   uint32_t *__restrict__ words, DevParams p)
+{
+    const uint32_t lane = threadIdx.x & 31u;
+    const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+    const uint64_t warp0 = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int wshift = p.log2g - 5;
+    const uint64_t pol = policy_evict_first();
+
+    for (uint64_t base = warp0 * 32; base < nvec; base += nwarps * 32) {
+        const uint64_t v = base + lane;
+        const bool valid = v < nvec;
+        uint4 c = make_uint4(0, 0, 0, 0), o = make_uint4(0, 0, 0, 0);
+        if (valid) {
+            c = ld_stream_v4(cand4 + v, pol);
+            o = ld_stream_v4(opp4 + v, pol);
+        }
+        const uint32_t cs[4] = {c.x, c.y, c.z, c.w};
+        const uint32_t os[4] = {o.x, o.y, o.z, o.w};
+        uint32_t widx[4][R];
+        uint32_t mask[4];
+#pragma unroll
+        for (int j = 0; j < 4; j++) {
+            const uint64_t a = cs[j];
+            const uint32_t h = (uint32_t)mix64(p.state_h1 ^ (uint64_t)os[j]) & p.gmask;
+            const uint32_t d0 = (uint32_t)mix64(p.state_dh0 ^ a) & p.kmask;
+            mask[j] = 1u << (h & 31u);
+            const uint32_t hw = h >> 5;
+#pragma unroll
+            for (int i = 0; i < R; i++) {
+                const uint32_t idx =
+                    i == 0 ? d0 : (((uint32_t)(a >> ((i - 1) * p.alpha)) & p.kmask) ^ d0);
+                const uint32_t cell = ((uint32_t)i << p.k) | idx;
+                widx[j][i] = (cell << wshift) + hw;
+            }
+        }
+        if (MODE == 0) {
+            if (valid) {
+#pragma unroll
+                for (int j = 0; j < 4; j++)
+#pragma unroll
+                    for (int i = 0; i < R; i++) red_or(words + widx[j][i], mask[j]);
+            }
+        } else {
+        uint32_t w[4][R];
+#pragma unroll
+        for (int j = 0; j < 4; j++)
+#pragma unroll
+            for (int i = 0; i < R; i++) w[j][i] = valid ? ld_sketch(words + widx[j][i]) : 0xFFFFFFFFu;
+#pragma unroll
+        for (int j = 0; j < 4; j++) {
+#pragma unroll
+            for (int i = 0; i < R; i++) {
+                const bool need = (w[j][i] & mask[j]) == 0;
+                if (MODE == 1) {
+                    if (need) red_or(words + widx[j][i], mask[j]);
+                } else {
+                    const unsigned nm = __ballot_sync(0xFFFFFFFFu, need);
+                    if (nm == 0) continue;  // warp-uniform: nothing new in this slot
+                    if (need) {
+                        uint32_t m = mask[j];
+                        unsigned peers = 1u << lane;
+                        if (nm & (nm - 1)) {  // more than one lane: group by word
+                            peers = __match_any_sync(nm, widx[j][i]);
+                            if (peers & (peers - 1)) {  // every member folds every member's mask
+                                for (unsigned q = peers; q; q &= q - 1)
+                                    m |= __shfl_sync(peers, mask[j], __ffs(q) - 1);
+                            }
+                        }
+                        if (lane == (uint32_t)(__ffs(peers) - 1)) red_or(words + widx[j][i], m);
+                    }
+                }
+            }
+        }
+        }  // MODE != 0
+    }
+}
+
+// General path: any r <= 64, any g >= 8 (sub-word cells included), 64-bit bit
+// addressing, unaligned input pointers.  One packet per lane per trip.
+template <int MODE>
+__global__ void __launch_bounds__(256) k_scan_generic(const uint32_t *__restrict__ cand,
+                                                      const uint32_t *__restrict__ opp, uint64_t n,
+                                                      uint32_t *__restrict__ words, DevParams p)
+{
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    const uint64_t pol = policy_evict_first();
+    for (uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; t < n; t += stride) {
+        const uint64_t a = ld_stream_u32(cand + t, pol);
+        const uint64_t h = mix64(p.state_h1 ^ (uint64_t)ld_stream_u32(opp + t, pol)) & p.gmask;
+        const uint32_t d0 = (uint32_t)mix64(p.state_dh0 ^ a) & p.kmask;
+        for (int i = 0; i < p.r; i++) {
+            const uint64_t cell = ((uint64_t)i << p.k) | index_of(p, a, d0, i);
+            const uint64_t B = (cell << p.log2g) + h;
+            uint32_t *wp = words + (B >> 5);
+            const uint32_t m = 1u << (uint32_t)(B & 31);
+            if (MODE == 0 || (ld_sketch(wp) & m) == 0) red_or(wp, m);
+        }
+    }
+}
+
+// ------------------------------------------------- K2: per-cell estimation --
+//
+// Backend.zero_counts (pkg/src/dhsa/_core.pyx:89-118): zc = g - popcount(cell).
+// LANES lanes cooperate on one cell, each popcounting 16-byte vectors, so a
+// warp reads 512 contiguous bytes per step at g = 1024 (4 cells per warp).
+__global__ void __launch_bounds__(256) k_zero_counts_vec(const uint4 *__restrict__ bits16,
+                                                         int32_t *__restrict__ zc, uint64_t ncell,
+                                                         int vecs_per_cell, int lanes, int g)
+{
+    const uint64_t gtid = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const uint64_t cells_per_pass = ((uint64_t)gridDim.x * blockDim.x) / (uint64_t)lanes;
+    const uint32_t sub = (uint32_t)(gtid % (uint64_t)lanes);
+    // every lane runs the same number of passes (the shuffles below need full warps)
+    for (uint64_t cell0 = 0; cell0 < ncell; cell0 += cells_per_pass) {
+        const uint64_t cell = cell0 + gtid / (uint64_t)lanes;
+        int ones = 0;
+        if (cell < ncell) {
+            const uint4 *cp = bits16 + cell * (uint64_t)vecs_per_cell;
+            for (int v = sub; v < vecs_per_cell; v += lanes) {
+                const uint4 q = __ldg(cp + v);
+                ones += __popc(q.x) + __popc(q.y) + __popc(q.z) + __popc(q.w);
+            }
+        }
+        for (int d = lanes >> 1; d > 0; d >>= 1) ones += __shfl_xor_sync(0xFFFFFFFFu, ones, d);
+        if (sub == 0 && cell < ncell) zc[cell] = g - ones;
+    }
+}
+
+// Cells narrower than 16 bytes (g = 8 .. 64): one lane per cell, byte loads.
+__global__ void __launch_bounds__(256) k_zero_counts_small(const uint8_t *__restrict__ bits,
+                                                           int32_t *__restrict__ zc, uint64_t ncell,
+                                                           int bytes_per_cell, int g)
+{
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t cell = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; cell < ncell; cell += stride) {
+        int ones = 0;
+        for (int b = 0; b < bytes_per_cell; b++) ones += __popc((uint32_t)bits[cell * bytes_per_cell + b]);
+        zc[cell] = g - ones;
+    }
+}
+
+// Dhla.hot_sets (pkg/src/dhsa/dhla.py:111-119): HE(i) = { j : zc[i][j] < zmin },
+// ascending; plus the 2^k-bit hot bitmap of each array and ZR(i) = sum_j zc[i][j]
+// (dhla.py:126).  One 1024-thread CTA per array walks its cells in order and
+// compacts by ballot + scan, so the lists come out already sorted.
+__global__ void __launch_bounds__(1024) k_hot_sets(const int32_t *__restrict__ zc, double zmin, int k,
+                                                   uint32_t *__restrict__ lists,
+                                                   uint32_t *__restrict__ bitmaps,
+                                                   uint64_t bitmap_words_per_array, Control *ctl)
+{
+    __shared__ uint32_t warp_count[32];
+    __shared__ uint32_t warp_offset[32];
+    __shared__ unsigned long long warp_sum[32];
+    __shared__ unsigned long long base_s;
+    __shared__ uint32_t chunk_total_s;
+    const int arr = blockIdx.x;
+    const uint64_t m = 1ull << k;
+    const uint32_t lane = threadIdx.x & 31u, wid = threadIdx.x >> 5;
+    const int32_t *row = zc + (uint64_t)arr * m;
+    uint32_t *list = lists + (uint64_t)arr * m;
+    uint32_t *bmp = bitmaps + (uint64_t)arr * bitmap_words_per_array;
+    unsigned long long total = 0;
+    if (threadIdx.x == 0) base_s = 0;
+    __syncthreads();
+    for (uint64_t c0 = 0; c0 < m; c0 += 1024) {
+        const uint64_t j = c0 + threadIdx.x;
+        const bool in = j < m;
+        const int32_t z = in ? row[j] : 0;
+        const bool hot = in && ((double)z < zmin);
+        const unsigned bal = __ballot_sync(0xFFFFFFFFu, hot);
+        if (lane == 0) {
+            warp_count[wid] = __popc(bal);
+            if (c0 + wid * 32 < m) bmp[(c0 >> 5) + wid] = bal;
+        }
+        unsigned long long zs = (unsigned long long)z;
+        for (int d = 16; d > 0; d >>= 1) zs += __shfl_xor_sync(0xFFFFFFFFu, zs, d);
+        if (lane == 0) warp_sum[wid] = zs;
+        __syncthreads();
+        if (wid == 0) {
+            uint32_t cnt = warp_count[lane], inc = cnt;
+            for (int d = 1; d < 32; d <<= 1) {
+                uint32_t t = __shfl_up_sync(0xFFFFFFFFu, inc, d);
+                if (lane >= (uint32_t)d) inc += t;
+            }
+            warp_offset[lane] = inc - cnt;
+            unsigned long long ws = warp_sum[lane];
+            for (int d = 16; d > 0; d >>= 1) ws += __shfl_xor_sync(0xFFFFFFFFu, ws, d);
+            if (lane == 31) chunk_total_s = inc;
+            if (lane == 0) total += ws;
+        }
+        __syncthreads();
+        const unsigned long long base = base_s;
+        const uint32_t chunk_total = chunk_total_s;
+        if (hot) list[base + warp_offset[wid] + __popc(bal & ((1u << lane) - 1u))] = (uint32_t)j;
+        __syncthreads();
+        if (threadIdx.x == 0) base_s = base + chunk_total;
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        ctl->hot_counts[arr] = base_s;
+        ctl->zero_totals[arr] = (long long)total;
+    }
+}
+
+// Scalars of the read-out, one thread:
+//   flow count  = mean_i( -C ln(ZR(i)/C) ), ZR == 0 -> evaluate at 1, flag saturated
+//                 (pkg/src/dhsa/estimator.py:26-34, dhla.py:121-128)
+//   psi         = 1 - exp(-flow / C)                          (dhla.py:130-134)
+//   denom       = g (1 - psi^r)                               (dhla.py:184)
+// and the "any hot set empty -> no candidates" rule (dhla.py:208-209).
+__global__ void k_plan(Control *ctl, int r, int k, int g)
+{
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    const double cap = (double)g * (double)(1ull << k);
+    double acc = 0.0;
+    int sat = 0, empty = 0;
+    for (int i = 0; i < r; i++) {
+        long long z = ctl->zero_totals[i];
+        if (z == 0) {
+            sat = 1;
+            z = 1;
+        }
+        acc += -cap * log((double)z / cap);
+        if (ctl->hot_counts[i] == 0) empty = 1;
+    }
+    const double flow = acc / r;
+    const double psi = 1.0 - exp(-flow / cap);
+    ctl->flow_count = flow;
+    ctl->flow_saturated = sat;
+    ctl->psi = psi;
+    ctl->denom = g * (1.0 - pow(psi, (double)r));
+    ctl->any_empty = empty;
+    for (int i = 0; i < 64; i++) ctl->stage_counts[i] = 0;
+    ctl->n_candidates = 0;
+    ctl->n_reports = 0;
+    ctl->fail_stage = 0;
+    ctl->fail_count = 0;
+    ctl->sorted = 0;
+}
+
+// ------------------------------------------------------------ K3: restore --
+//
+// Dhla._candidate_hosts (pkg/src/dhsa/dhla.py:198-217).  The reference crosses
+// whole hot sets and keeps tuples whose neighbouring blocks agree on their
+// k - alpha overlapping bits.  Here the overlap rule is used constructively: a
+// partial key fixes the low k - alpha bits of the next block, so only its top
+// alpha bits are free -- 2^alpha candidate cells, each tested against the next
+// array's hot bitmap.  When the next hot set is smaller than 2^alpha its list is
+// walked instead (the reference's own enumeration).  Either way the survivor set
+// of every stage is exactly the reference's, so the per-stage counts and the
+// CapacityError they trigger (dhla.py:269-273, 294-298) are identical.
+
+__device__ __forceinline__ bool bitmap_test(const uint32_t *bmp, uint32_t idx)
+{
+    return (bmp[idx >> 5] >> (idx & 31u)) & 1u;
+}
+
+__device__ __forceinline__ bool stage_blocked(const Control *ctl, int stage_index,
+                                              unsigned long long max_candidates)
+{
+    // stage_index = number of stages already run.  Blocked when some hot set is
+    // empty, or an earlier stage overflowed (then nothing after it runs, like the
+    // exception in the reference).
+    if (ctl->any_empty) return true;
+    for (int s = 0; s < stage_index; s++)
+        if (ctl->stage_counts[s] > max_candidates) return true;
+    return false;
+}
+
+// Stage 1 (_stage_first, pkg/src/dhsa/dhla.py:252-274): (cl0, cl1) in HE0 x HE1,
+// b1 = cl0 ^ cl1 is the key's low block; cl2 = cl0 ^ b2 with
+// b2 & omask == b1 >> alpha; sub = b1 | (b2 >> (k - alpha)) << k.
+__global__ void __launch_bounds__(256) k_stage_first(const uint32_t *__restrict__ lists,
+                                                     const uint32_t *__restrict__ bitmaps,
+                                                     uint64_t bitmap_words_per_array, DevParams p,
+                                                     unsigned long long max_candidates,
+                                                     uint64_t *__restrict__ out_sub,
+                                                     uint32_t *__restrict__ out_cl0, Control *ctl)
+{
+    if (stage_blocked(ctl, 0, max_candidates)) return;
+    const uint64_t m = 1ull << p.k;
+    const uint64_t n0 = ctl->hot_counts[0], n1 = ctl->hot_counts[1], n2 = ctl->hot_counts[2];
+    const uint64_t next = 1ull << p.alpha;
+    const bool by_list = n2 < next;
+    const uint64_t E = by_list ? n2 : next;
+    const uint64_t total = n0 * n1 * E;
+    const int top = p.k - p.alpha;
+    const uint32_t omask = (uint32_t)((1ull << top) - 1);
+    const uint32_t *he0 = lists, *he1 = lists + m, *he2 = lists + 2 * m;
+    const uint32_t *bmp2 = bitmaps + 2 * bitmap_words_per_array;
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t f = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; f < total; f += stride) {
+        const uint64_t t = f % E, pair = f / E;
+        const uint32_t cl0 = he0[pair / n1];
+        const uint32_t b1 = cl0 ^ he1[pair % n1];
+        uint32_t b2;
+        bool ok;
+        if (by_list) {
+            b2 = cl0 ^ he2[t];
+            ok = (b1 >> p.alpha) == (b2 & omask);
+        } else {
+            b2 = ((uint32_t)t << top) | (b1 >> p.alpha);
+            ok = bitmap_test(bmp2, cl0 ^ b2);
+        }
+        if (ok) {
+            const unsigned long long pos = atomicAdd(&ctl->stage_counts[0], 1ull);
+            if (pos < max_candidates) {
+                out_sub[pos] = (uint64_t)b1 | ((uint64_t)(b2 >> top) << p.k);
+                out_cl0[pos] = cl0;
+            }
+        }
+    }
+}
+
+// Stage for array i >= 3 (_stage_next, pkg/src/dhsa/dhla.py:277-299):
+// blk = cl0 ^ cl_i must satisfy blk & omask == sub >> (i-1) alpha;
+// sub |= (blk >> (k - alpha)) << (k + (i-2) alpha).
+__global__ void __launch_bounds__(256) k_stage_next(int i, const uint32_t *__restrict__ lists,
+                                                    const uint32_t *__restrict__ bitmaps,
+                                                    uint64_t bitmap_words_per_array, DevParams p,
+                                                    unsigned long long max_candidates,
+                                                    const uint64_t *__restrict__ in_sub,
+                                                    const uint32_t *__restrict__ in_cl0,
+                                                    uint64_t *__restrict__ out_sub,
+                                                    uint32_t *__restrict__ out_cl0, Control *ctl)
+{
+    const int s = i - 2;  // stages already run
+    if (stage_blocked(ctl, s, max_candidates)) return;
+    const uint64_t m = 1ull << p.k;
+    const uint64_t np = ctl->stage_counts[s - 1], ni = ctl->hot_counts[i];
+    const uint64_t next = 1ull << p.alpha;
+    const bool by_list = ni < next;
+    const uint64_t E = by_list ? ni : next;
+    const uint64_t total = np * E;
+    const int top = p.k - p.alpha;
+    const uint32_t omask = (uint32_t)((1ull << top) - 1);
+    const int sh_chk = (i - 1) * p.alpha, sh_put = p.k + (i - 2) * p.alpha;
+    const uint32_t *he = lists + (uint64_t)i * m;
+    const uint32_t *bmp = bitmaps + (uint64_t)i * bitmap_words_per_array;
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t f = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; f < total; f += stride) {
+        const uint64_t t = f % E, q = f / E;
+        const uint64_t sp = in_sub[q];
+        const uint32_t cl0 = in_cl0[q];
+        const uint32_t want = (uint32_t)(sp >> sh_chk);  // k - alpha bits
+        uint32_t blk;
+        bool ok;
+        if (by_list) {
+            blk = cl0 ^ he[t];
+            ok = want == (blk & omask);
+        } else {
+            blk = ((uint32_t)t << top) | want;
+            ok = bitmap_test(bmp, cl0 ^ blk);
+        }
+        if (ok) {
+            const unsigned long long pos = atomicAdd(&ctl->stage_counts[s], 1ull);
+            if (pos < max_candidates) {
+                out_sub[pos] = sp | ((uint64_t)(blk >> top) << sh_put);
+                out_cl0[pos] = cl0;
+            }
+        }
+    }
+}
+
+// Tail of _candidate_hosts (pkg/src/dhsa/dhla.py:213-216): drop partials with bits
+// above key_width, keep those whose dh0 reproduces cl0.  A key determines cl0 and
+// the tuple <-> (sub, cl0) map is one-to-one, so survivors are already distinct.
+__global__ void __launch_bounds__(256) k_verify_keys(int n_stages, DevParams p,
+                                                     unsigned long long max_candidates,
+                                                     const uint64_t *__restrict__ in_sub,
+                                                     const uint32_t *__restrict__ in_cl0,
+                                                     uint64_t *__restrict__ keys, Control *ctl)
+{
+    if (stage_blocked(ctl, n_stages, max_candidates)) return;
+    const uint64_t np = ctl->stage_counts[n_stages - 1];
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t q = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; q < np; q += stride) {
+        const uint64_t sub = in_sub[q];
+        if (sub >> p.key_width) continue;
+        if (dh0_of(p, sub) != in_cl0[q]) continue;
+        const unsigned long long pos = atomicAdd(&ctl->n_candidates, 1ull);
+        keys[pos] = sub;  // pos < np <= max_candidates
+    }
+}
+
+// Records the first overflowing stage (the numbers of the CapacityError text).
+__global__ void k_capacity_check(int n_stages, unsigned long long max_candidates, Control *ctl)
+{
+    if (threadIdx.x != 0 || blockIdx.x != 0 || ctl->any_empty) return;
+    for (int s = 0; s < n_stages; s++)
+        if (ctl->stage_counts[s] > max_candidates) {
+            ctl->fail_stage = s + 1;  // stage 1, then i - 1 for array i (dhla.py:271,296)
+            ctl->fail_count = ctl->stage_counts[s];
+            return;
+        }
+}
+
+// ------------------------------- K4: re-estimate + threshold filter + order --
+
+// SZ of one key: g - popcount(AND of its r cells) (pkg/src/dhsa/dhla.py:136-143).
+// One warp per key, 16-byte vectors when cells are at least 16 bytes wide.
+__device__ __forceinline__ int shared_zero_count_warp(const uint8_t *__restrict__ bits,
+                                                      const DevParams &p, uint64_t key, uint32_t lane)
+{
+    const uint32_t d0 = dh0_of(p, key);
+    const uint64_t g = 1ull << p.log2g, bpe = g >> 3;
+    int ones = 0;
+    if (bpe >= 16) {
+        const int vecs = (int)(bpe >> 4);
+        for (int v = lane; v < vecs; v += 32) {
+            uint4 acc = make_uint4(~0u, ~0u, ~0u, ~0u);
+            for (int i = 0; i < p.r; i++) {
+                const uint64_t cell = ((uint64_t)i << p.k) | index_of(p, key, d0, i);
+                const uint4 q = *reinterpret_cast<const uint4 *>(bits + cell * bpe + (uint64_t)v * 16);
+                acc.x &= q.x, acc.y &= q.y, acc.z &= q.z, acc.w &= q.w;
+            }
+            ones += __popc(acc.x) + __popc(acc.y) + __popc(acc.z) + __popc(acc.w);
+        }
+    } else {
+        for (int b = lane; b < (int)bpe; b += 32) {
+            uint32_t acc = 0xFFu;
+            for (int i = 0; i < p.r; i++) {
+                const uint64_t cell = ((uint64_t)i << p.k) | index_of(p, key, d0, i);
+                acc &= bits[cell * bpe + b];
+            }
+            ones += __popc(acc);
+        }
+    }
+    for (int d = 16; d > 0; d >>= 1) ones += __shfl_xor_sync(0xFFFFFFFFu, ones, d);
+    return (int)g - ones;
+}
+
+__global__ void __launch_bounds__(256) k_shared_zero_counts(const uint8_t *__restrict__ bits, DevParams p,
+                                                            const uint64_t *__restrict__ keys, uint64_t n,
+                                                            int32_t *__restrict__ sz)
+{
+    const uint32_t lane = threadIdx.x & 31u;
+    const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+    for (uint64_t t = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; t < n; t += nwarps) {
+        const int z = shared_zero_count_warp(bits, p, keys[t], lane);
+        if (lane == 0) sz[t] = z;
+    }
+}
+
+// Sharing-corrected estimate (pkg/src/dhsa/dhla.py:183-189):
+//   SZ == 0 -> saturated, evaluate at 1;  SZ >= denom -> 0.0;  else -g ln(SZ/denom).
+__device__ __forceinline__ double corrected_estimate(int g, int sz_clamped, double denom)
+{
+    if ((double)sz_clamped >= denom) return 0.0;
+    return -(double)g * log((double)sz_clamped / denom);
+}
+
+// Sort key of one report.  The reference orders by (-estimate, host)
+// (dhla.py:195); the estimate is strictly decreasing in the clamped SZ below
+// denom and 0.0 from denom on, so (class, host) with class = clamped SZ, or one
+// shared value for the zero class, sorts identically with integers only.
+//   bits 63..33 class | bits 32..1 host | bit 0 saturated
+#define DHSA_ZERO_CLASS 0x7FFFFFFFull
+__device__ __forceinline__ uint64_t pack_report(int sz, double denom, uint64_t host)
+{
+    const int szc = sz == 0 ? 1 : sz;
+    const uint64_t cls = ((double)szc >= denom) ? DHSA_ZERO_CLASS : (uint64_t)szc;
+    return (cls << 33) | (host << 1) | (uint64_t)(sz == 0);
+}
+
+// For every candidate: SZ, estimate, keep if estimate >= theta (dhla.py:190-194).
+__global__ void __launch_bounds__(256) k_reestimate(const uint8_t *__restrict__ bits, DevParams p,
+                                                    double theta, const uint64_t *__restrict__ keys,
+                                                    uint64_t *__restrict__ packed, Control *ctl)
+{
+    const uint32_t lane = threadIdx.x & 31u;
+    const uint64_t n = ctl->n_candidates;
+    const double denom = ctl->denom;
+    const int g = 1 << p.log2g;
+    const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+    for (uint64_t t = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; t < n; t += nwarps) {
+        const uint64_t key = keys[t];
+        const int sz = shared_zero_count_warp(bits, p, key, lane);
+        if (lane == 0) {
+            const double est = corrected_estimate(g, sz == 0 ? 1 : sz, denom);
+            if (est >= theta) {
+                const unsigned long long pos = atomicAdd(&ctl->n_reports, 1ull);
+                packed[pos] = pack_report(sz, denom, key);
+            }
+        }
+    }
+}
+
+struct ReportOut {
+    uint64_t host;
+    double estimate;
+    int32_t saturated;
+    int32_t shared_zero_count;
+};
+
+__global__ void __launch_bounds__(256) k_emit_reports(const uint64_t *__restrict__ packed, int g,
+                                                      ReportOut *__restrict__ out, const Control *ctl)
+{
+    const uint64_t n = ctl->n_reports;
+    const double denom = ctl->denom;
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; t < n; t += stride) {
+        const uint64_t w = packed[t];
+        const uint64_t cls = w >> 33;
+        const int sat = (int)(w & 1ull);
+        ReportOut r;
+        r.host = (w >> 1) & 0xFFFFFFFFull;
+        r.saturated = sat;
+        if (cls == DHSA_ZERO_CLASS) {
+            r.estimate = 0.0;
+            r.shared_zero_count = -1;  // not recoverable from the zero class; unused by callers
+        } else {
+            r.estimate = corrected_estimate(g, (int)cls, denom);
+            r.shared_zero_count = sat ? 0 : (int)cls;
+        }
+        out[t] = r;
+    }
+}
+
+// ------------------------------------------------------------------- sort --
+// Ascending sort of u64 words.  Up to SORT_SMEM_MAX entries one CTA sorts in
+// shared memory with the count read from the device (no host round trip);
+// beyond that the host drives the global bitonic passes below.
+#define DHSA_SORT_SMEM_MAX 8192
+
+__global__ void __launch_bounds__(1024) k_sort_small(uint64_t *__restrict__ data,
+                                                     const unsigned long long *__restrict__ n_ptr,
+                                                     Control *ctl)
+{
+    extern __shared__ uint64_t sm[];
+    const uint64_t n = *n_ptr;
+    if (n > DHSA_SORT_SMEM_MAX) return;
+    uint32_t len = 1;
+    while (len < n) len <<= 1;
+    for (uint32_t t = threadIdx.x; t < len; t += blockDim.x) sm[t] = t < n ? data[t] : ~0ull;
+    __syncthreads();
+    for (uint32_t kk = 2; kk <= len; kk <<= 1) {
+        for (uint32_t j = kk >> 1; j > 0; j >>= 1) {
+            for (uint32_t t = threadIdx.x; t < len; t += blockDim.x) {
+                const uint32_t x = t ^ j;
+                if (x > t) {
+                    const uint64_t a = sm[t], b = sm[x];
+                    const bool up = (t & kk) == 0;
+                    if ((a > b) == up) {
+                        sm[t] = b;
+                        sm[x] = a;
+                    }
+                }
+            }
+            __syncthreads();
+        }
+    }
+    for (uint32_t t = threadIdx.x; t < n; t += blockDim.x) data[t] = sm[t];
+    if (threadIdx.x == 0) ctl->sorted = 1;
+}
+
+__global__ void __launch_bounds__(256) k_sort_pad(uint64_t *__restrict__ data, uint64_t n, uint64_t len)
+{
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t t = n + (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; t < len; t += stride) data[t] = ~0ull;
+}
+
+__global__ void __launch_bounds__(256) k_bitonic_pass(uint64_t *__restrict__ data, uint64_t len, uint64_t kk,
+                                                      uint64_t j)
+{
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; t < len; t += stride) {
+        const uint64_t x = t ^ j;
+        if (x > t) {
+            const uint64_t a = data[t], b = data[x];
+            const bool up = (t & kk) == 0;
+            if ((a > b) == up) {
+                data[t] = b;
+                data[x] = a;
+            }
+        }
+    }
+}
+
+// ------------------------------------------------------------- K5: merge --
+//
+// dhsa.dhla.merge (pkg/src/dhsa/dhla.py:305-318) is a bitwise OR of two bit
+// arrays.  Multi-GPU: each rank owns a byte range of the sketch and ORs that
+// range of every peer's private sketch into its own copy, reading the peers
+// straight over NVLink (peer / IPC-mapped pointers) with 16-byte loads -- a
+// reduce-scatter whose reduction is OR, which NCCL does not offer.
+#define DHSA_MAX_PEERS 16
+struct PeerPtrs {
+    const uint4 *p[DHSA_MAX_PEERS];
+};
+
+__global__ void __launch_bounds__(256) k_or_merge(uint4 *__restrict__ dst, PeerPtrs peers, int n_peers,
+                                                  uint64_t vec_lo, uint64_t vec_hi)
+{
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t v = vec_lo + (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; v < vec_hi; v += stride) {
+        uint4 acc = dst[v];
+        for (int q = 0; q < n_peers; q++) {
+            uint4 x;
+            // peer memory: bypass L1 so a later merge never sees a stale line
+            asm volatile("ld.global.cv.v4.u32 {%0,%1,%2,%3}, [%4];"
+                         : "=r"(x.x), "=r"(x.y), "=r"(x.z), "=r"(x.w)
+                         : "l"(peers.p[q] + v));
+            acc.x |= x.x, acc.y |= x.y, acc.z |= x.z, acc.w |= x.w;
+        }
+        dst[v] = acc;
+    }
+}
+
+__global__ void __launch_bounds__(256) k_copy_slice(uint4 *__restrict__ dst, const uint4 *__restrict__ src,
+                                                    uint64_t vec_lo, uint64_t vec_hi)
+{
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t v = vec_lo + (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; v < vec_hi; v += stride) {
+        uint4 x;
+        asm volatile("ld.global.cv.v4.u32 {%0,%1,%2,%3}, [%4];"
+                     : "=r"(x.x), "=r"(x.y), "=r"(x.z), "=r"(x.w)
+                     : "l"(src + v));
+        dst[v] = x;
+    }
+}
+
+// ------------------------------------------------------------ L2 probes --
+// Random-address 32-bit operations into a buffer that fits L2: the ceiling the
+// scan's sketch traffic runs against.  Addresses come from a multiply-xorshift
+// of a counter, so consecutive lanes hit unrelated sectors, like hashed cells.
+__device__ __forceinline__ uint32_t probe_hash(uint64_t x)
+{
+    x *= 0x9E3779B97F4A7C15ULL;
+    x ^= x >> 29;
+    x *= 0xBF58476D1CE4E5B9ULL;
+    return (uint32_t)(x >> 32);
+}
+
+template <int KIND>
+__global__ void __launch_bounds__(256) k_probe_l2(uint32_t *__restrict__ words, uint32_t word_mask,
+                                                  uint64_t ops, uint32_t *__restrict__ sink)
+{
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    uint32_t acc = 0;
+    for (uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; t < ops; t += stride * 4) {
+#pragma unroll
+        for (int u = 0; u < 4; u++) {
+            const uint64_t q = t + (uint64_t)u * stride;
+            if (q < ops) {
+                const uint32_t hsh = probe_hash(q);
+                uint32_t *wp = words + (hsh & word_mask);
+                if (KIND == 0)
+                    red_or(wp, 1u << (hsh >> 27));
+                else
+                    acc += ld_sketch(wp);
+            }
+        }
+    }
+    if (KIND == 1 && acc == 0x12345678u) *sink = acc;
+}
+
+}  // namespace dhsa

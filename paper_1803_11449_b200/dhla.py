@@ -1,0 +1,307 @@
+"""The device-resident sketch: drop-in for the reference's ``dhsa.dhla.Dhla``.
+
+Same constructor, attributes and methods as
+/root/reference/pkg/src/dhsa/dhla.py:57-196 (and ``merge`` :305-318), so the
+reference's window engine (pkg/src/dhsa/engine.py:57-103) can hold one of these
+where it holds a ``Dhla`` -- it only touches ``Dhla(params, backend=,
+window_id=)``, ``update_batch``, ``window_id`` and ``restore_superpoints(theta,
+max_candidates=, workers=)``.
+
+Every data-path method is a call into libdhsa_b200.so (include/dhsa_b200.h);
+Python only moves arguments and shapes results.  The one contract that differs
+from the reference is ``bits``: the array lives in HBM, so the attribute is a
+host *copy* taken after the sketch's stream drains, and ``load_bits`` is the
+explicit write (the reference writes ``sketch.bits[...]`` in place,
+pkg/src/dhsa/dhla.py:372, pkg/tests/test_dhla.py:88-90).
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import math
+import os
+from dataclasses import dataclass
+from typing import NamedTuple, Optional
+
+import numpy as np
+
+from . import _cabi
+from .dhg import DhgParams
+from .errors import ConfigError
+
+DEFAULT_MAX_CANDIDATES = 1 << 20  # pkg/src/dhsa/dhla.py:34
+
+SCAN_MODES = {"red": 0, "test": 1, "test_agg": 2}
+
+_REPORT_DTYPE = np.dtype([("host", "<u8"), ("estimate", "<f8"), ("saturated", "<i4"), ("sz", "<i4")])
+assert _REPORT_DTYPE.itemsize == C.sizeof(_cabi.Report)
+
+
+def hot_threshold(g: int, theta: int) -> float:
+    """Zmin = g exp(-theta/g) (pkg/src/dhsa/dhla.py:45-47)."""
+    return g * math.exp(-theta / g)
+
+
+@dataclass(frozen=True)
+class SuperPointReport:  # pkg/src/dhsa/dhla.py:50-54
+    host: int
+    estimate: float
+    saturated: bool
+
+
+class Estimate(NamedTuple):  # pkg/src/dhsa/estimator.py:21-23
+    value: float
+    saturated: bool
+
+
+def _default_device() -> int:
+    env = os.environ.get("DHSA_DEVICE", os.environ.get("LOCAL_RANK"))
+    return int(env) if env not in (None, "") else 0
+
+
+def _is_cuda_tensor(x) -> bool:
+    return hasattr(x, "data_ptr") and getattr(x, "is_cuda", False)
+
+
+class Dhla:
+    """r * 2^k byte-packed linear estimators in HBM, addressed by the hash group."""
+
+    def __init__(self, params, backend="auto", window_id: int = 0, device: Optional[int] = None):
+        if backend not in ("auto", "cuda"):
+            # the reference's names ("compiled", "python") are CPU kernels; none exist here
+            raise ConfigError(f"unknown backend {backend!r}; this build has only the CUDA path "
+                              f"(expected auto or cuda)")
+        self.params = DhgParams.coerce(params)
+        self.window_id = window_id
+        self.device = _default_device() if device is None else int(device)
+        p = self.params
+        self._cparams = _cabi.Params(p.r, p.g, p.k, p.alpha, p.key_width, 0, p.state_dh0, p.state_h1)
+        self._lib = _cabi.lib()
+        h = C.c_void_p()
+        _cabi.check(self._lib.dhsa_create(C.byref(self._cparams), self.device, C.byref(h)))
+        self._h = h
+        self.last_info: Optional[dict] = None
+
+    def __del__(self):
+        h, self._h = getattr(self, "_h", None), None
+        if h:
+            try:
+                self._lib.dhsa_destroy(h)
+            except Exception:
+                pass
+
+    # --- identity -----------------------------------------------------------
+
+    @property
+    def backend_name(self) -> str:
+        return "cuda"
+
+    @property
+    def memory_bytes(self) -> int:
+        n = C.c_uint64()
+        _cabi.check(self._lib.dhsa_sketch_bytes(self._h, C.byref(n)))
+        return int(n.value)
+
+    @property
+    def bits_device_ptr(self) -> int:
+        ptr = C.c_void_p()
+        _cabi.check(self._lib.dhsa_bits_device_ptr(self._h, C.byref(ptr)))
+        return int(ptr.value)
+
+    @property
+    def launch_count(self) -> int:
+        n = C.c_uint64()
+        _cabi.check(self._lib.dhsa_launch_count(self._h, C.byref(n)))
+        return int(n.value)
+
+    def use_stream(self, cuda_stream: Optional[int]) -> None:
+        """Launch on this CUDA stream handle (None -> the sketch's own stream)."""
+        _cabi.check(self._lib.dhsa_set_stream(self._h, C.c_void_p(cuda_stream or 0)))
+
+    def set_scan_mode(self, mode) -> None:
+        _cabi.check(self._lib.dhsa_set_scan_mode(self._h, SCAN_MODES.get(mode, mode)))
+
+    # --- the bits attribute ----------------------------------------------------
+
+    @property
+    def bits(self) -> np.ndarray:
+        """Host copy, shape (r, 2^k, g/8) uint8, the reference's layout."""
+        p = self.params
+        out = np.empty((p.r, p.index_count, p.g // 8), dtype=np.uint8)
+        _cabi.check(self._lib.dhsa_download_bits(self._h, out.ctypes.data, out.nbytes))
+        return out
+
+    def load_bits(self, bits: np.ndarray) -> None:
+        p = self.params
+        arr = np.ascontiguousarray(bits, dtype=np.uint8)
+        if arr.shape != (p.r, p.index_count, p.g // 8):
+            raise ConfigError(f"bits must have shape {(p.r, p.index_count, p.g // 8)}, got {arr.shape}")
+        _cabi.check(self._lib.dhsa_upload_bits(self._h, arr.ctypes.data, arr.nbytes))
+
+    # --- update phase ------------------------------------------------------------
+
+    def update(self, candidate: int, opposite: int) -> None:
+        self.update_batch(np.array([candidate], dtype=np.uint32), np.array([opposite], dtype=np.uint32))
+
+    def update_batch(self, candidates, opposites) -> None:
+        """Scan a batch of pairs (pkg/src/dhsa/dhla.py:87-95).
+
+        numpy (or any host array-like): staged to the device inside the call.
+        torch CUDA tensors (int32/uint32, contiguous): scanned in place on
+        torch's current stream.
+        """
+        if _is_cuda_tensor(candidates) or _is_cuda_tensor(opposites):
+            self._update_device(candidates, opposites)
+            return
+        cand = np.ascontiguousarray(candidates, dtype=np.uint32)
+        opp = np.ascontiguousarray(opposites, dtype=np.uint32)
+        if cand.shape != opp.shape or cand.ndim != 1:
+            raise ValueError("candidate and opposite arrays differ in length")
+        _cabi.check(self._lib.dhsa_update_host(self._h, cand.ctypes.data, opp.ctypes.data, len(cand)))
+
+    def _update_device(self, cand, opp) -> None:
+        import torch
+
+        if not (_is_cuda_tensor(cand) and _is_cuda_tensor(opp)):
+            raise ValueError("candidates and opposites must both be CUDA tensors")
+        if cand.numel() != opp.numel() or cand.dim() != 1 or opp.dim() != 1:
+            raise ValueError("candidate and opposite arrays differ in length")
+        for t in (cand, opp):
+            if t.element_size() != 4 or t.is_floating_point() or not t.is_contiguous():
+                raise ValueError("device inputs must be contiguous 32-bit integer tensors")
+            if t.device.index != self.device:
+                raise ConfigError(f"tensor on cuda:{t.device.index}, sketch on cuda:{self.device}")
+        self.use_stream(torch.cuda.current_stream(self.device).cuda_stream)
+        _cabi.check(self._lib.dhsa_update_device(self._h, cand.data_ptr(), opp.data_ptr(), cand.numel()))
+
+    def seal(self) -> None:
+        """Drain the stream: every update issued so far is in the bits."""
+        _cabi.check(self._lib.dhsa_seal(self._h))
+
+    def reset(self, window_id: int = 0) -> None:
+        _cabi.check(self._lib.dhsa_reset(self._h))
+        self.window_id = window_id
+
+    # --- read-out ------------------------------------------------------------------
+
+    def zero_counts(self) -> np.ndarray:
+        p = self.params
+        out = np.empty((p.r, p.index_count), dtype=np.int64)
+        _cabi.check(self._lib.dhsa_zero_counts(self._h, out.ctypes.data, None))
+        return out
+
+    def hot_sets(self, theta, zero_counts=None) -> list:
+        """Per-array ascending hot indices.  `zero_counts` is accepted for signature
+        compatibility; the device recomputes them from the bits (same values)."""
+        p = self.params
+        lists = np.empty((p.r, p.index_count), dtype=np.uint64)
+        counts = np.empty(p.r, dtype=np.uint64)
+        _cabi.check(self._lib.dhsa_hot_sets(self._h, float(theta), lists.ctypes.data, counts.ctypes.data))
+        return [lists[i, : int(counts[i])].copy() for i in range(p.r)]
+
+    def _info_dict(self, info: _cabi.RestoreInfo) -> dict:
+        r = self.params.r
+        return dict(
+            n_candidates=int(info.n_candidates), n_reports=int(info.n_reports),
+            fail_stage=int(info.fail_stage), fail_count=int(info.fail_count),
+            flow_count=float(info.flow_count), flow_saturated=bool(info.flow_saturated),
+            psi=float(info.psi), denom=float(info.denom),
+            hot_counts=[int(info.hot_counts[i]) for i in range(r)],
+            stage_counts=[int(info.stage_counts[i]) for i in range(r - 2)],
+            zero_totals=[int(info.zero_totals[i]) for i in range(r)],
+        )
+
+    def estimate(self, theta=0.0) -> dict:
+        """Zero totals, hot-set sizes, flow count, psi and denom in one device pass."""
+        info = _cabi.RestoreInfo()
+        _cabi.check(self._lib.dhsa_estimate(self._h, float(theta), C.byref(info)))
+        self.last_info = self._info_dict(info)
+        return self.last_info
+
+    def estimate_flow_count(self, zero_counts=None) -> Estimate:
+        d = self.estimate()
+        return Estimate(d["flow_count"], d["flow_saturated"])
+
+    def bit_set_probability(self, flow_count: float) -> float:
+        """psi = 1 - exp(-w / (g 2^k)) (pkg/src/dhsa/dhla.py:130-134)."""
+        if flow_count < 0:
+            raise ValueError("flow count must be nonnegative")
+        return 1.0 - math.exp(-flow_count / (self.params.g * self.params.index_count))
+
+    def shared_zero_counts(self, hosts) -> np.ndarray:
+        hosts = np.ascontiguousarray(hosts, dtype=np.uint64)
+        out = np.empty(len(hosts), dtype=np.int64)
+        _cabi.check(self._lib.dhsa_shared_zero_counts(self._h, hosts.ctypes.data, len(hosts),
+                                                      out.ctypes.data))
+        return out
+
+    def corrected_cardinality(self, host: int, psi: float) -> Estimate:
+        """One host's sharing-corrected estimate (pkg/src/dhsa/dhla.py:145-160)."""
+        g = self.params.g
+        sz = int(self.shared_zero_counts(np.asarray([host], dtype=np.uint64))[0])
+        denom = g * (1.0 - psi ** self.params.r)
+        saturated = sz == 0
+        if saturated:
+            sz = 1
+        if sz >= denom:
+            return Estimate(0.0, saturated)
+        return Estimate(-g * math.log(sz / denom), saturated)
+
+    def _candidate_hosts(self, theta, max_candidates: int = DEFAULT_MAX_CANDIDATES,
+                         workers: int = 1, zero_counts=None) -> np.ndarray:
+        """Distinct, forward-verified keys, ascending (pkg/src/dhsa/dhla.py:198-217)."""
+        info = _cabi.RestoreInfo()
+        cap = 4096
+        while True:
+            out = np.empty(cap, dtype=np.uint64)
+            rc = self._lib.dhsa_candidate_hosts(self._h, float(theta), int(max_candidates),
+                                                out.ctypes.data, cap, C.byref(info))
+            self.last_info = self._info_dict(info)
+            if rc == 3 and info.n_candidates > cap:
+                cap = int(info.n_candidates)
+                continue
+            _cabi.check(rc)
+            return out[: int(info.n_candidates)].copy()
+
+    def restore_superpoints(self, theta, max_candidates: int = DEFAULT_MAX_CANDIDATES,
+                            workers: int = 1) -> list:
+        """Every host whose corrected estimate reaches theta, sorted by
+        (-estimate, host) (pkg/src/dhsa/dhla.py:164-196).  `workers` is accepted
+        and ignored: the device chain has no host threads to size."""
+        info = _cabi.RestoreInfo()
+        cap = 1024
+        while True:
+            rows = np.empty(cap, dtype=_REPORT_DTYPE)
+            rc = self._lib.dhsa_restore(self._h, float(theta), int(max_candidates),
+                                        rows.ctypes.data, cap, C.byref(info))
+            self.last_info = self._info_dict(info)
+            if rc == 3 and info.n_reports > cap:
+                cap = int(info.n_reports)
+                continue
+            _cabi.check(rc)
+            n = int(info.n_reports)
+            return [SuperPointReport(int(h), float(e), bool(s))
+                    for h, e, s in zip(rows["host"][:n].tolist(), rows["estimate"][:n].tolist(),
+                                       rows["saturated"][:n].tolist())]
+
+    # --- merge -------------------------------------------------------------------------
+
+    def merge_from(self, other: "Dhla") -> None:
+        """self |= other, on the device (peer access when the devices differ)."""
+        if self.params != other.params:
+            raise ConfigError(
+                f"cannot merge sketches with different parameters: {self.params} vs {other.params}"
+            )
+        _cabi.check(self._lib.dhsa_or_merge(self._h, other._h))
+
+
+def merge(a: Dhla, b: Dhla) -> Dhla:
+    """Union of two sketches with identical parameters (pkg/src/dhsa/dhla.py:305-318)."""
+    if a.params != b.params:
+        raise ConfigError(
+            f"cannot merge sketches with different parameters: {a.params} vs {b.params}"
+        )
+    out = Dhla(a.params, window_id=a.window_id, device=a.device)
+    out.merge_from(a)
+    out.merge_from(b)
+    return out

@@ -1,0 +1,228 @@
+"""One detection window sharded over the GPUs of a node, one process per GPU.
+
+The sketch is a pure function of the window's distinct pair set and merging is a
+bitwise OR (/root/reference/pkg/src/dhsa/dhla.py:305-318), so the
+window shards by packets with no data-path collective during the scan:
+
+    rank p scans packets [p*N/P, (p+1)*N/P) into a private sketch
+    merge:  reduce-scatter with OR  -- rank p ORs byte range p of every peer's
+            sketch into its own, reading peers over NVLink through CUDA-IPC-mapped
+            pointers (csrc k_or_merge; NCCL has no OR reduction)
+            all-gather             -- rank p copies the merged range q from peer q
+    restore runs on the merged sketch (microseconds; every rank holds the result)
+
+``torch.distributed`` is plumbing only: rendezvous, the 64-byte IPC handle
+exchange and barriers.  If peer mapping is unavailable the merge falls back to
+``all_gather_into_tensor`` of whole sketches over NCCL followed by the local OR
+kernel -- still the CUDA path, never a CPU one.
+
+The collective choreography is written against a small ops interface so the
+world_size-2 gloo tests can drive exactly this code with host buffers.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+from typing import List, Optional, Sequence, Tuple
+
+import numpy as np
+
+from . import _cabi
+from .dhla import DEFAULT_MAX_CANDIDATES, Dhla
+from .errors import ConfigError
+
+
+def byte_ranges(nbytes: int, world: int, align: int = 16) -> List[Tuple[int, int]]:
+    """Cut [0, nbytes) into `world` contiguous ranges on `align`-byte boundaries.
+
+    nbytes is the padded allocation size (a multiple of `align`); ranges differ
+    by at most one alignment unit and cover everything exactly once."""
+    if world < 1:
+        raise ConfigError(f"world size must be positive (got {world})")
+    if nbytes % align:
+        raise ConfigError(f"sketch allocation {nbytes} is not a multiple of {align} bytes")
+    units = nbytes // align
+    cuts = [(units * p) // world * align for p in range(world + 1)]
+    return list(zip(cuts[:-1], cuts[1:]))
+
+
+def packet_slice(n_packets: int, rank: int, world: int, align: int = 4) -> Tuple[int, int]:
+    """Contiguous slice of a window's packets owned by `rank` (4-packet aligned so
+    every rank's slice starts on a 16-byte boundary of the uint32 arrays)."""
+    if not 0 <= rank < world:
+        raise ConfigError(f"rank {rank} outside world of {world}")
+    units = (n_packets + align - 1) // align
+    lo = min(n_packets, (units * rank) // world * align)
+    hi = min(n_packets, (units * (rank + 1)) // world * align)
+    return lo, hi
+
+
+class CudaMergeOps:
+    """Merge primitives of a device sketch (the product implementation)."""
+
+    def __init__(self, sketch: Dhla):
+        self.sketch = sketch
+        self._lib = _cabi.lib()
+        self._opened: List[int] = []
+
+    @property
+    def alloc_bytes(self) -> int:
+        return (self.sketch.memory_bytes + 15) & ~15
+
+    def seal(self) -> None:
+        self.sketch.seal()
+
+    def export_handle(self) -> bytes:
+        buf = (C.c_uint8 * 64)()
+        _cabi.check(self._lib.dhsa_ipc_export(self.sketch._h, buf))
+        return bytes(buf)
+
+    def open_handle(self, handle: bytes) -> int:
+        ptr = C.c_void_p()
+        buf = (C.c_uint8 * 64).from_buffer_copy(handle)
+        _cabi.check(self._lib.dhsa_ipc_open(self.sketch.device, buf, C.byref(ptr)))
+        self._opened.append(int(ptr.value))
+        return int(ptr.value)
+
+    def close_handles(self) -> None:
+        for ptr in self._opened:
+            self._lib.dhsa_ipc_close(self.sketch.device, C.c_void_p(ptr))
+        self._opened = []
+
+    def or_from_peers(self, peer_ptrs: Sequence[int], lo: int, hi: int) -> None:
+        arr = (C.c_void_p * len(peer_ptrs))(*peer_ptrs)
+        _cabi.check(self._lib.dhsa_or_merge_peers(self.sketch._h, arr, len(peer_ptrs), lo, hi))
+
+    def copy_from_peer(self, peer_ptr: int, lo: int, hi: int) -> None:
+        _cabi.check(self._lib.dhsa_copy_slice_from_peer(self.sketch._h, C.c_void_p(peer_ptr), lo, hi))
+
+    # all-gather fallback: whole sketch images as torch tensors on this device
+    def bits_tensor(self):
+        import torch
+
+        class _View:
+            pass
+
+        v = _View()
+        v.__cuda_array_interface__ = {
+            "shape": (self.sketch.memory_bytes,), "typestr": "|u1",
+            "data": (self.sketch.bits_device_ptr, False), "version": 2,
+        }
+        return torch.as_tensor(v, device=f"cuda:{self.sketch.device}")
+
+    def new_gather_buffer(self, world: int):
+        import torch
+
+        return torch.empty((world, self.sketch.memory_bytes), dtype=torch.uint8,
+                           device=f"cuda:{self.sketch.device}")
+
+    def or_from_buffer(self, row) -> None:
+        _cabi.check(self._lib.dhsa_or_merge_buffer(self.sketch._h, C.c_void_p(row.data_ptr()),
+                                                   self.sketch.memory_bytes))
+
+
+def merge_p2p(ops, dist, group=None) -> None:
+    """Reduce-scatter(OR) + all-gather over peer-mapped sketches.  Collective."""
+    world, rank = dist.get_world_size(group), dist.get_rank(group)
+    if world == 1:
+        return
+    ranges = byte_ranges(ops.alloc_bytes, world)
+    handles: List[Optional[bytes]] = [None] * world
+    dist.all_gather_object(handles, ops.export_handle(), group=group)
+    ptrs = {q: ops.open_handle(handles[q]) for q in range(world) if q != rank}
+    try:
+        ops.seal()             # my scan has landed ...
+        dist.barrier(group)    # ... and so has everyone's
+        lo, hi = ranges[rank]
+        ops.or_from_peers([ptrs[q] for q in sorted(ptrs)], lo, hi)
+        ops.seal()
+        dist.barrier(group)    # every owner's range is final
+        for q in sorted(ptrs):
+            ops.copy_from_peer(ptrs[q], *ranges[q])
+        ops.seal()
+        dist.barrier(group)    # nobody resets while a peer still reads
+    finally:
+        ops.close_handles()
+
+
+def merge_allgather(ops, dist, group=None) -> None:
+    """Fallback: NCCL all-gather of whole sketches, then the local OR kernel.  Collective."""
+    world, rank = dist.get_world_size(group), dist.get_rank(group)
+    if world == 1:
+        return
+    ops.seal()
+    buf = ops.new_gather_buffer(world)
+    dist.all_gather_into_tensor(buf.view(-1), ops.bits_tensor(), group=group)
+    for q in range(world):
+        if q != rank:
+            ops.or_from_buffer(buf[q])
+    ops.seal()
+
+
+class ShardedWindow:
+    """A window whose packets are split over the ranks of a process group."""
+
+    def __init__(self, params, theta: int = 1024, device: Optional[int] = None, group=None,
+                 max_candidates: int = DEFAULT_MAX_CANDIDATES, merge: str = "auto"):
+        import torch.distributed as dist
+
+        if merge not in ("auto", "p2p", "allgather"):
+            raise ConfigError(f"merge must be auto, p2p or allgather (got {merge!r})")
+        self._dist = dist
+        self.group = group
+        self.theta = theta
+        self.max_candidates = max_candidates
+        self.merge_mode = merge
+        self.sketch = Dhla(params, device=device)
+        self.ops = CudaMergeOps(self.sketch)
+        self.merged_with = None
+
+    @property
+    def world(self) -> int:
+        return self._dist.get_world_size(self.group) if self._dist.is_initialized() else 1
+
+    def reset(self) -> None:
+        self.sketch.reset()
+
+    def scan(self, candidates, opposites) -> None:
+        """This rank's slice of the window (numpy or torch CUDA tensors)."""
+        self.sketch.update_batch(candidates, opposites)
+
+    def merge(self) -> str:
+        """After this every rank's sketch is the union over all ranks."""
+        if self.world == 1:
+            self.merged_with = "none"
+            return self.merged_with
+        mode = self.merge_mode
+        if mode in ("auto", "p2p"):
+            ok = self._try_p2p()
+            if ok:
+                self.merged_with = "p2p"
+                return self.merged_with
+            if mode == "p2p":
+                raise ConfigError("peer-mapped merge requested but CUDA IPC mapping failed on some rank")
+        merge_allgather(self.ops, self._dist, self.group)
+        self.merged_with = "allgather"
+        return self.merged_with
+
+    def _try_p2p(self) -> bool:
+        import torch
+
+        dist = self._dist
+        # agree up front whether every rank can map its peers (collective decision)
+        can = 1
+        try:
+            for q in range(torch.cuda.device_count()):
+                if q != self.sketch.device and not torch.cuda.can_device_access_peer(self.sketch.device, q):
+                    can = 0
+        except Exception:
+            can = 0
+        flag = torch.tensor([can], dtype=torch.int32, device=f"cuda:{self.sketch.device}")
+        dist.all_reduce(flag, op=dist.ReduceOp.MIN, group=self.group)
+        if int(flag.item()) == 0:
+            return False
+        merge_p2p(self.ops, dist, self.group)
+        return True
+
+    def restore(self):
+        return self.sketch.restore_superpoints(self.theta, max_candidates=self.max_candidates)

@@ -1,0 +1,460 @@
+"""GPU parity: the CUDA path, called through the C ABI, against the CPU oracle,
+against the committed golden fixtures (recorded from the live reference), and
+-- at BASELINE.json's full sizes -- through properties that do not need a CPU
+run of the same size (the sketch is a pure function of the distinct pair set,
+/root/reference/SPEC.md:356).
+
+Bar: bit-exact on the DDH bit array, zero counts, hot sets, candidate hosts,
+per-stage survivor counts, CapacityError text and the reported host list and
+order; cardinality estimates within REL_TOL = 1e-6 relative (the north star's
+tolerance; observed agreement is ~1e-15, device fp64 log vs numpy's).
+"""
+import concurrent.futures
+import hashlib
+
+import numpy as np
+import pytest
+
+import paper_1803_11449_b200 as P
+from oracle import oracle as O
+
+from helpers import (case_batches, case_params, config1_pairs, load_json, oracle_for_case,
+                     restore_cases)
+
+pytestmark = pytest.mark.gpu
+
+REL_TOL = 1e-6
+CASES = restore_cases()
+PARAM_SETS = {
+    "default": dict(),
+    "toy": dict(r=4, g=64, k=8, alpha=4, key_width=16),
+    "small": dict(r=5, g=256, k=10, alpha=8, key_width=32, seed_dh0=1, seed_h1=2),
+    "min_r3": dict(r=3, g=256, k=18, alpha=14, key_width=32, seed_dh0=3, seed_h1=4),
+    "six": dict(r=6, g=512, k=12, alpha=5),
+    "g8": dict(r=3, g=8, k=8, alpha=8, key_width=16),
+    "g16": dict(r=4, g=16, k=10, alpha=8, key_width=24, seed_dh0=11, seed_h1=12),
+    "g32": dict(r=4, g=32, k=9, alpha=8, key_width=24),
+    "r7_generic": dict(r=7, g=128, k=10, alpha=4, key_width=30),
+    "big_g": dict(r=3, g=8192, k=11, alpha=11, key_width=22),
+}
+
+
+def sha(a):
+    return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()
+
+
+def gpu_for_case(case, mode="test_agg"):
+    sk = P.Dhla(P.DhgParams(**case["params"]))
+    sk.set_scan_mode(mode)
+    for c, o in case_batches(case):
+        sk.update_batch(c, o)
+    return sk
+
+
+# ------------------------------------------------------------------------ scan --
+
+
+@pytest.mark.parametrize("mode", ["red", "test", "test_agg"])
+@pytest.mark.parametrize("name", list(PARAM_SETS))
+def test_update_batch_bits_equal_oracle(name, mode):
+    # pkg/tests/test_kernels.py:37-48 (compiled == numpy), here CUDA == oracle
+    kw = PARAM_SETS[name]
+    cand, opp = O.distinct_pairs(50_000, 3)
+    ora = O.OracleSketch(**kw)
+    ora.update_batch(cand, opp)
+    sk = P.Dhla(P.DhgParams(**kw))
+    sk.set_scan_mode(mode)
+    sk.update_batch(cand, opp)
+    assert np.array_equal(sk.bits, ora.bits)
+    assert np.array_equal(sk.zero_counts(), ora.zero_counts())
+    if name == "default":
+        assert sha(sk.bits) == "38d4cac25b1922468b09d87d40a536699a03d0a58ac44cdc776a8ed1995dd136"
+
+
+def test_single_update_sets_exactly_r_bits():
+    # pkg/tests/test_dhla.py:49-52 and the byte/mask constants of SURVEY 8(c)
+    const = load_json("constants.json")
+    sk = P.Dhla(P.DhgParams())
+    sk.update(0xC0A80101, 0x08080808)
+    bits = sk.bits
+    got = [[int(i), int(j), int(b), int(bits[i, j, b])] for i, j, b in np.argwhere(bits)]
+    assert got == const["single_update"]
+    assert sk.memory_bytes == 10_485_760
+
+
+@pytest.mark.parametrize("n", [0, 1, 2, 3, 4, 5, 31, 33, 1023, 4097])
+def test_ragged_lengths_and_empty_batches(n):
+    cand, opp = O.distinct_pairs(max(n, 1), 8)
+    cand, opp = cand[:n], opp[:n]
+    ora = O.OracleSketch()
+    ora.update_batch(cand, opp)
+    sk = P.Dhla(P.DhgParams())
+    sk.update_batch(cand, opp)
+    assert np.array_equal(sk.bits, ora.bits)
+
+
+def test_length_mismatch_raises_value_error():
+    # pkg/src/dhsa/_core.pyx:73-74
+    sk = P.Dhla(P.DhgParams())
+    with pytest.raises(ValueError):
+        sk.update_batch(np.zeros(4, np.uint32), np.zeros(5, np.uint32))
+
+
+def test_update_is_idempotent_and_permutation_invariant():
+    # pkg/tests/test_dhla.py:55-78
+    cand, opp = O.distinct_pairs(10_000, 3)
+    order = np.random.default_rng(4).permutation(len(cand))
+    a, b, c = (P.Dhla(P.DhgParams()) for _ in range(3))
+    a.update_batch(cand, opp)
+    b.update_batch(cand[order], opp[order])
+    c.update_batch(cand, opp)
+    c.update_batch(cand, opp)
+    ref = a.bits
+    assert np.array_equal(ref, b.bits) and np.array_equal(ref, c.bits)
+
+
+def test_device_tensor_inputs_including_unaligned_views():
+    import torch
+
+    cand, opp = O.distinct_pairs(100_003, 9)
+    ora = O.OracleSketch()
+    ora.update_batch(cand[1:], opp[1:])
+    ct = torch.from_numpy(cand.view(np.int32)).cuda()
+    ot = torch.from_numpy(opp.view(np.int32)).cuda()
+    sk = P.Dhla(P.DhgParams())
+    sk.update_batch(ct[1:], ot[1:])  # 4-byte aligned only: takes the general kernel
+    assert np.array_equal(sk.bits, ora.bits)
+    sk2 = P.Dhla(P.DhgParams())
+    sk2.update_batch(ct[4:], ot[4:])  # 16-byte aligned: vector kernel + scalar tail
+    sk2.update_batch(ct[1:4], ot[1:4])
+    assert np.array_equal(sk2.bits, ora.bits)
+
+
+def test_concurrent_updates_from_threads_are_lossless():
+    # pkg/tests/test_kernels.py:62-74
+    cand, opp = O.distinct_pairs(400_000, 5)
+    ora = O.OracleSketch()
+    ora.update_batch(cand, opp, threads=4)
+    shared = P.Dhla(P.DhgParams())
+    chunks = [(cand[s::8], opp[s::8]) for s in range(8)]
+    with concurrent.futures.ThreadPoolExecutor(max_workers=8) as pool:
+        list(pool.map(lambda co: shared.update_batch(*co), chunks))
+    assert np.array_equal(shared.bits, ora.bits)
+
+
+@pytest.mark.parametrize("mode", ["red", "test", "test_agg"])
+def test_ddos_contention_all_packets_hit_the_same_cells(mode):
+    # BASELINE config 4 shape: many sources -> few victims, victims as candidates
+    rng = np.random.default_rng(44)
+    victims = rng.integers(0, 2 ** 32, size=4, dtype=np.uint64).astype(np.uint32)
+    n = 2_000_000
+    cand = victims[rng.zipf(1.2, size=n) % 4]
+    opp = rng.integers(0, 2 ** 32, size=n, dtype=np.uint64).astype(np.uint32)
+    ora = O.OracleSketch()
+    ora.update_batch(cand, opp, threads=4)
+    sk = P.Dhla(P.DhgParams())
+    sk.set_scan_mode(mode)
+    sk.update_batch(cand, opp)
+    assert np.array_equal(sk.bits, ora.bits)
+    got, want = sk.restore_superpoints(1024), ora.restore_superpoints(1024)
+    assert [(r.host, r.saturated) for r in got] == [(r.host, r.saturated) for r in want]
+    assert all(r.saturated for r in got) and len(got) == 4
+
+
+def test_reset_and_load_bits_round_trip():
+    sk = P.Dhla(P.DhgParams(**PARAM_SETS["small"]))
+    rnd = np.random.default_rng(2).integers(0, 256, size=sk.bits.shape, dtype=np.uint8)
+    sk.load_bits(rnd)
+    assert np.array_equal(sk.bits, rnd)
+    sk.reset(window_id=7)
+    assert sk.window_id == 7 and not sk.bits.any()
+
+
+# -------------------------------------------------------------------- read-out --
+
+
+@pytest.mark.parametrize("g", [8, 16, 32, 64, 128, 1024, 4096])
+def test_zero_counts_match_unpackbits(g):
+    # pkg/tests/test_kernels.py:51-59
+    sk = P.Dhla(P.DhgParams(r=3, g=g, k=8, alpha=8, key_width=16))
+    rnd = np.random.default_rng(4).integers(0, 256, size=(3, 256, g // 8), dtype=np.uint8)
+    sk.load_bits(rnd)
+    assert np.array_equal(sk.zero_counts(), g - np.unpackbits(rnd, axis=2).sum(axis=2))
+
+
+def test_hot_threshold_boundary_376_hot_377_not():
+    # pkg/tests/test_dhla.py:84-95
+    sk = P.Dhla(P.DhgParams())
+    bits = np.zeros((5, 16384, 128), dtype=np.uint8)
+    bits[0, 5, :81] = 0xFF
+    bits[1, 9, :80] = 0xFF
+    bits[1, 9, 80] = 0x7F
+    sk.load_bits(bits)
+    zc = sk.zero_counts()
+    assert zc[0, 5] == 376 and zc[1, 9] == 377
+    hot = sk.hot_sets(1024)
+    assert hot[0].tolist() == [5] and hot[1].tolist() == []
+    assert sk.restore_superpoints(1024) == []  # an empty hot set ends the restore
+
+
+def test_empty_sketch():
+    sk = P.Dhla(P.DhgParams())
+    assert all(len(h) == 0 for h in sk.hot_sets(1024))
+    assert sk.restore_superpoints(1024) == []
+    assert sk.estimate_flow_count() == (0.0, False)
+    assert sk._candidate_hosts(1024).tolist() == []
+
+
+@pytest.mark.parametrize("case", CASES, ids=[c["name"] for c in CASES])
+def test_readout_matches_reference_fixture(case):
+    sk = gpu_for_case(case)
+    theta, mc = case["theta"], case["max_candidates"]
+    assert sha(sk.bits) == case["bits_sha256"]
+    zc = sk.zero_counts()
+    assert zc.dtype == np.int64 and sha(zc) == case["zero_counts_sha256"]
+    hot = sk.hot_sets(theta)
+    assert [len(h) for h in hot] == case["hot_sizes"]
+    assert [sha(h.astype(np.uint64)) for h in hot] == case["hot_sha256"]
+    est = sk.estimate(theta)
+    assert est["zero_totals"] == case["zero_totals"]
+    assert est["flow_count"] == pytest.approx(case["flow_count"], rel=REL_TOL)
+    assert est["flow_saturated"] == case["flow_saturated"]
+    assert est["psi"] == pytest.approx(case["psi"], rel=REL_TOL)
+    if "capacity_error" in case:
+        with pytest.raises(P.CapacityError) as err:
+            sk._candidate_hosts(theta, mc)
+        assert str(err.value) == case["capacity_error"]
+        with pytest.raises(P.CapacityError) as err:
+            sk.restore_superpoints(theta, max_candidates=mc)
+        assert str(err.value) == case["capacity_error"]
+        return
+    hosts = sk._candidate_hosts(theta, mc)
+    assert hosts.dtype == np.uint64 and hosts.tolist() == case["candidates"]
+    if case["stage_counts"]:
+        assert sk.last_info["stage_counts"] == case["stage_counts"]
+    assert sk.shared_zero_counts(hosts).tolist() == case["shared_zero_counts"]
+    reps = sk.restore_superpoints(theta, max_candidates=mc)
+    assert [r.host for r in reps] == [h for h, _, _ in case["reports"]]
+    assert [r.saturated for r in reps] == [s for _, _, s in case["reports"]]
+    for r, (_, e, _) in zip(reps, case["reports"]):
+        assert r.estimate == pytest.approx(e, rel=REL_TOL)
+
+
+@pytest.mark.parametrize("case", [c for c in CASES if c["name"] in
+                                  ("small_dense", "toy_dense", "six_dense", "default_60_plants_noise1m")],
+                         ids=lambda c: c["name"])
+def test_readout_matches_live_oracle(case):
+    """Same sketches against the C oracle's literal HE0 x HE1 x HE2 enumeration."""
+    ora = oracle_for_case(case)
+    sk = gpu_for_case(case)
+    theta, mc = case["theta"], case["max_candidates"]
+    hosts, stages = ora.candidate_hosts(theta, mc, return_stage_counts=True)
+    assert sk._candidate_hosts(theta, mc).tolist() == hosts.tolist()
+    assert sk.last_info["stage_counts"] == stages
+    got, want = sk.restore_superpoints(theta, max_candidates=mc), ora.restore_superpoints(theta, mc)
+    assert [(r.host, r.saturated) for r in got] == [(r.host, r.saturated) for r in want]
+    for a, b in zip(got, want):
+        assert a.estimate == pytest.approx(b.estimate, rel=REL_TOL)
+
+
+def test_config1_trace_matches_reference_fixture():
+    exp = load_json("config1_expected.json")
+    src, dst = config1_pairs()
+    sk = P.Dhla(P.DhgParams())
+    sk.update_batch(src, dst)
+    assert sha(sk.bits) == exp["bits_sha256"]
+    reps = sk.restore_superpoints(1024)
+    assert [r.host for r in reps] == [h for h, _, _ in exp["reports"]]
+    assert sorted(r.host for r in reps) == [h for h, _ in exp["truth_supers"]]
+    assert sk.last_info["stage_counts"] == exp["stage_counts"]
+    for r, (_, e, _) in zip(reps, exp["reports"]):
+        assert r.estimate == pytest.approx(e, rel=REL_TOL)
+
+
+def test_planted_host_golden_values():
+    sk = P.Dhla(P.DhgParams())
+    sk.update_batch(*O.plant_pairs(0xC63A1B02, 2048, 10))
+    assert int(sk.shared_zero_counts([0xC63A1B02])[0]) == 147
+    (rep,) = sk.restore_superpoints(1024)
+    assert rep.host == 0xC63A1B02 and not rep.saturated
+    assert rep.estimate == pytest.approx(1987.624160072414, rel=REL_TOL)
+    est = sk.corrected_cardinality(0xC63A1B02, sk.bit_set_probability(sk.estimate_flow_count().value))
+    assert est.value == pytest.approx(rep.estimate, rel=REL_TOL)
+
+
+def test_restore_ties_break_by_ascending_host():
+    # pkg/tests/test_dhla.py:255-269
+    _, opp = O.plant_pairs(0, 2000, 12)
+    sk = P.Dhla(P.DhgParams())
+    for host in (5000, 4000):
+        sk.update_batch(np.full(len(opp), host, dtype=np.uint32), opp)
+    reps = sk.restore_superpoints(1024)
+    assert [r.host for r in reps] == [4000, 5000]
+    assert reps[0].estimate == reps[1].estimate
+
+
+def test_all_cells_hot_large_sort_and_zero_class():
+    """Every cell full: 2^16 candidates (> the single-CTA sorter's 8192), all
+    saturated with estimate 0.0 (SZ clamp 1 >= denom), reported only at theta 0
+    and then ordered by host alone."""
+    kw = PARAM_SETS["toy"]
+    sk = P.Dhla(P.DhgParams(**kw))
+    full = np.full((4, 256, 8), 0xFF, dtype=np.uint8)
+    sk.load_bits(full)
+    ora = O.OracleSketch(**kw)
+    ora.bits[:] = 0xFF
+    with pytest.raises(P.CapacityError) as err:
+        sk.restore_superpoints(0, max_candidates=1 << 20)
+    with pytest.raises(O.OracleCapacityError) as want:
+        ora.restore_superpoints(0, 1 << 20)
+    assert str(err.value) == str(want.value)
+    mc = 1 << 24
+    hosts = sk._candidate_hosts(0, mc)
+    assert hosts.tolist() == list(range(1 << 16))
+    assert sk.last_info["stage_counts"] == [1 << 20, 1 << 24]
+    reps = sk.restore_superpoints(0, max_candidates=mc)
+    assert [r.host for r in reps] == list(range(1 << 16))
+    assert all(r.saturated and r.estimate == 0.0 for r in reps)
+    assert sk.restore_superpoints(1, max_candidates=mc) == []
+
+
+def test_many_reports_sorted_like_the_reference():
+    """65536 reports with many tied estimates through the global bitonic sorter:
+    random 60%-full cells make every cell hot and every 16-bit key a candidate."""
+    kw = PARAM_SETS["toy"]
+    rnd = (np.random.default_rng(77).random((4, 256, 64)) < 0.6)
+    bits = np.packbits(rnd, axis=2, bitorder="little")
+    ora = O.OracleSketch(**kw)
+    ora.bits[:] = bits
+    sk = P.Dhla(P.DhgParams(**kw))
+    sk.load_bits(bits)
+    theta, mc = 0, 1 << 24
+    want = ora.restore_superpoints(theta, mc)
+    got = sk.restore_superpoints(theta, max_candidates=mc)
+    assert len(want) == 1 << 16 and len({r.estimate for r in want}) > 8
+    assert [(r.host, r.saturated) for r in got] == [(r.host, r.saturated) for r in want]
+    for a, b in zip(got, want):
+        assert a.estimate == pytest.approx(b.estimate, rel=REL_TOL)
+    theta = 3
+    want = ora.restore_superpoints(theta, mc)
+    got = sk.restore_superpoints(theta, max_candidates=mc)
+    assert 0 < len(want) < 1 << 16
+    assert [(r.host, r.saturated) for r in got] == [(r.host, r.saturated) for r in want]
+
+
+# ----------------------------------------------------------------------- merge --
+
+
+def test_merge_algebra():
+    # pkg/tests/test_dhla.py:317-336
+    cand, opp = O.distinct_pairs(20_000, 17)
+    p = P.DhgParams()
+    a, b, whole, empty = (P.Dhla(p) for _ in range(4))
+    a.update_batch(cand[:10_000], opp[:10_000])
+    b.update_batch(cand[10_000:], opp[10_000:])
+    whole.update_batch(cand, opp)
+    wb = whole.bits
+    assert np.array_equal(P.merge(a, b).bits, wb)
+    assert np.array_equal(P.merge(b, a).bits, wb)
+    assert np.array_equal(P.merge(a, empty).bits, a.bits)
+    m = P.merge(a, b)
+    assert m.restore_superpoints(1024) == whole.restore_superpoints(1024)
+
+
+def test_merge_rejects_parameter_mismatch():
+    # pkg/tests/test_dhla.py:339-344
+    p = P.DhgParams()
+    other = P.DhgParams(seed_h1=p.seed_h1 + 1)
+    with pytest.raises(P.ConfigError) as err:
+        P.merge(P.Dhla(p), P.Dhla(other))
+    assert str(p.seed_h1) in str(err.value) and str(other.seed_h1) in str(err.value)
+
+
+def test_or_merge_peers_slices_equal_whole_merge():
+    """The multi-GPU merge protocol on one device: each 'rank' ORs its byte range."""
+    import ctypes as C
+
+    from paper_1803_11449_b200 import _cabi
+
+    p = P.DhgParams()
+    parts = []
+    for s in range(4):
+        sk = P.Dhla(p)
+        sk.update_batch(*O.distinct_pairs(30_000, 40 + s))
+        parts.append(sk)
+    want = parts[0].bits
+    for sk in parts[1:]:
+        want |= sk.bits
+    n = p.sketch_bytes
+    dst = parts[0]
+    for sk in parts[1:]:
+        sk.seal()
+    ptrs = (C.c_void_p * 3)(*[sk.bits_device_ptr for sk in parts[1:]])
+    cuts = [0, n // 4, n // 2, 3 * n // 4, n]
+    for lo, hi in zip(cuts[:-1], cuts[1:]):
+        _cabi.check(_cabi.lib().dhsa_or_merge_peers(dst._h, ptrs, 3, lo, hi))
+    assert np.array_equal(dst.bits, want)
+
+
+# ------------------------------------------------- BASELINE sizes, by property --
+
+
+def _window(n_packets, n_hosts, n_scanners, seed):
+    """Distinct flows of a synthetic window + a shuffled, repeated packet stream on the GPU."""
+    import torch
+
+    rng = np.random.default_rng(seed)
+    hosts = np.unique(rng.integers(0, 2 ** 32, size=n_hosts + n_scanners + 64, dtype=np.uint64))
+    rng.shuffle(hosts)
+    hosts = hosts[: n_hosts + n_scanners].astype(np.uint32)
+    cards = np.minimum(rng.zipf(1.5, size=n_hosts), 256)
+    cards = np.concatenate([cards, rng.integers(2048, 8193, size=n_scanners)])
+    src = np.repeat(hosts, cards)
+    dst = rng.integers(0, 2 ** 32, size=len(src), dtype=np.uint64).astype(np.uint32)
+    g = torch.Generator(device="cuda")
+    g.manual_seed(seed)
+    pick = torch.randint(0, len(src), (n_packets,), device="cuda", generator=g)
+    pick[: len(src)] = torch.arange(len(src), device="cuda")  # every flow at least once
+    ct = torch.from_numpy(src.view(np.int32)).cuda()[pick]
+    ot = torch.from_numpy(dst.view(np.int32)).cuda()[pick]
+    return src, dst, ct, ot, hosts[n_hosts:]
+
+
+@pytest.mark.parametrize("mode", ["test", "test_agg", "red"])
+def test_100m_packet_window_bits_and_superpoints_equal_oracle(mode):
+    """BASELINE config 2 size.  The oracle scans the distinct flows only; the GPU
+    scans all 100M packets; bits, super point set and estimates must agree."""
+    src, dst, ct, ot, scanners = _window(100_000_000, 150_000, 50, seed=100)
+    ora = O.OracleSketch()
+    ora.update_batch(src, dst, threads=8)
+    sk = P.Dhla(P.DhgParams())
+    sk.set_scan_mode(mode)
+    sk.update_batch(ct, ot)
+    assert sha(sk.bits) == sha(ora.bits)
+    got, want = sk.restore_superpoints(1024), ora.restore_superpoints(1024)
+    assert [(r.host, r.saturated) for r in got] == [(r.host, r.saturated) for r in want]
+    assert set(scanners.tolist()) <= {r.host for r in got}
+    for a, b in zip(got, want):
+        assert a.estimate == pytest.approx(b.estimate, rel=REL_TOL)
+    # idempotence at full size: a second pass over the same window changes nothing
+    before = sk.estimate()["zero_totals"]
+    sk.update_batch(ct, ot)
+    assert sk.estimate()["zero_totals"] == before
+
+
+def test_sharded_scan_plus_or_merge_equals_single_scan():
+    """BASELINE config 3 shape on one device: 8 private sketches over 8 slices of
+    the window, OR-merged, equal one sketch over the whole window."""
+    src, dst, ct, ot, _ = _window(16_000_000, 100_000, 30, seed=101)
+    whole = P.Dhla(P.DhgParams())
+    whole.update_batch(ct, ot)
+    shards = []
+    per = (len(ct) // 8 + 3) & ~3
+    for rnk in range(8):
+        sk = P.Dhla(P.DhgParams())
+        sk.update_batch(ct[rnk * per:(rnk + 1) * per], ot[rnk * per:(rnk + 1) * per])
+        shards.append(sk)
+    for sk in shards[1:]:
+        shards[0].merge_from(sk)
+    assert sha(shards[0].bits) == sha(whole.bits)
+    assert shards[0].restore_superpoints(1024) == whole.restore_superpoints(1024)

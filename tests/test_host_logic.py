@@ -1,0 +1,122 @@
+"""CPU-side checks: parameter validation, the C-ABI surface, loud failure without a GPU."""
+import ctypes as C
+import os
+import re
+
+import pytest
+
+import paper_1803_11449_b200 as P
+from paper_1803_11449_b200 import _cabi, dhg
+
+from helpers import load_json
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+CONST = load_json("constants.json")
+
+
+def _have_gpu():
+    try:
+        import torch
+
+        return torch.cuda.is_available()
+    except Exception:
+        return False
+
+
+def test_default_params_and_states_match_reference():
+    p = P.DhgParams()
+    assert (p.r, p.g, p.k, p.alpha, p.key_width) == (5, 1024, 14, 6, 32)
+    assert p.state_dh0 == CONST["state_dh0"] and p.state_h1 == CONST["state_h1"]
+    assert p.sketch_bytes == 10_485_760 and p.index_count == 16384
+    for x, want in CONST["mix64"].items():
+        assert dhg.mix64(int(x)) == want
+    for a, want in CONST["forward"].items():
+        assert list(dhg.forward(p, int(a))) == want
+    for b, want in CONST["h1"].items():
+        assert dhg.h1(p, int(b)) == want
+
+
+@pytest.mark.parametrize("kw, fragment", [
+    # pkg/tests/test_dhg.py:152-175 -- every rule names its inequality
+    (dict(r=2), "r >= 3"),
+    (dict(g=100), "power of two"),
+    (dict(g=4), "power of two"),
+    (dict(k=0), "1 <= k <= 30"),
+    (dict(k=31), "1 <= k <= 30"),
+    (dict(key_width=7), "8 <= key_width <= 32"),
+    (dict(key_width=33), "8 <= key_width <= 32"),
+    (dict(k=14, key_width=12), "k <= key_width"),
+    (dict(alpha=0), "1 <= alpha <= k"),
+    (dict(alpha=15), "1 <= alpha <= k"),
+    (dict(r=3, alpha=6, k=14), "(r-2)*alpha + k >= key_width"),
+    (dict(r=5, k=30, alpha=30, key_width=32), "<= 64"),
+    (dict(seed_dh0=-1), "unsigned 64-bit"),
+    (dict(seed_h1=2 ** 64), "unsigned 64-bit"),
+])
+def test_param_validation_names_the_rule(kw, fragment):
+    with pytest.raises(P.ConfigError) as err:
+        P.DhgParams(**kw)
+    assert fragment in str(err.value)
+    assert isinstance(err.value, ValueError)  # ConfigError is a ValueError, as in the reference
+
+
+def test_coerce_accepts_reference_shaped_records():
+    from types import SimpleNamespace
+
+    rec = SimpleNamespace(r=4, g=64, k=8, alpha=4, key_width=16, seed_dh0=1, seed_h1=2)
+    p = P.DhgParams.coerce(rec)
+    assert (p.r, p.g, p.k, p.alpha, p.key_width, p.seed_dh0, p.seed_h1) == (4, 64, 8, 4, 16, 1, 2)
+
+
+def _declared_symbols():
+    text = open(os.path.join(ROOT, "include", "dhsa_b200.h")).read()
+    text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
+    return sorted(set(re.findall(r"\b(dhsa_[a-z0-9_]+)\s*\(", text)))
+
+
+def test_library_exports_every_declared_symbol():
+    lib = _cabi.lib()
+    declared = _declared_symbols()
+    assert len(declared) >= 25
+    for name in declared:
+        assert hasattr(lib, name), f"{name} declared in include/dhsa_b200.h but not exported"
+    assert sorted(_cabi.SIGNATURES) == declared
+    assert lib.dhsa_abi_version() == 1
+
+
+def test_struct_layouts_match_header():
+    assert C.sizeof(_cabi.Params) == 40
+    assert C.sizeof(_cabi.Report) == 24
+    assert C.sizeof(_cabi.RestoreInfo) == 8 * 2 + 4 * 2 + 8 + 8 * 3 + 64 * 8 * 3
+
+
+def test_c_side_validation_maps_to_config_error():
+    lib = _cabi.lib()
+    bad = _cabi.Params(2, 1024, 14, 6, 32, 0, 1, 2)
+    h = C.c_void_p()
+    rc = lib.dhsa_create(C.byref(bad), 0, C.byref(h))
+    assert rc == 2
+    with pytest.raises(P.ConfigError, match="r >= 3"):
+        _cabi.check(rc)
+
+
+def test_unknown_backend_is_config_error():
+    # pkg/tests/test_kernels.py:89-91: closed set of names; CPU names do not exist here
+    for name in ("compiled", "python", "numpy"):
+        with pytest.raises(P.ConfigError):
+            P.Dhla(P.DhgParams(), backend=name)
+
+
+@pytest.mark.skipif(_have_gpu(), reason="only meaningful without a GPU")
+def test_no_gpu_fails_loudly_not_silently():
+    with pytest.raises(P.CudaError):
+        P.Dhla(P.DhgParams())
+
+
+def test_product_package_never_imports_the_oracle():
+    pkg = os.path.join(ROOT, "paper_1803_11449_b200")
+    for base, _, files in os.walk(pkg):
+        for f in files:
+            if f.endswith((".py", ".cu", ".cuh", ".h")):
+                text = open(os.path.join(base, f)).read()
+                assert "oracle" not in text.replace("no CPU oracle", ""), f"{f} mentions the oracle"
