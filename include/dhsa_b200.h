@@ -47,6 +47,7 @@ extern "C" {
 #define DHSA_SCAN_RED_ONLY 0      /* one atomic OR per (packet, array), unconditionally        */
 #define DHSA_SCAN_TEST_RED 1      /* load the word, atomic only if the bit is still clear      */
 #define DHSA_SCAN_TEST_AGG_RED 2  /* as 1, and lanes of a warp hitting one word merge first    */
+#define DHSA_SCAN_FLOW_CACHE 3    /* as 2 behind an exact L2-resident cache of scanned pairs   */
 
 typedef struct dhsa_sketch dhsa_sketch_t; /* opaque; replaces dhsa.dhla.Dhla, pkg/src/dhsa/dhla.py:57-68 */
 
@@ -103,10 +104,20 @@ int dhsa_reset(dhsa_sketch_t *s);
 int dhsa_sketch_bytes(const dhsa_sketch_t *s, uint64_t *nbytes);
 /* Device address of the bit array (for peers, snapshots, torch views). */
 int dhsa_bits_device_ptr(dhsa_sketch_t *s, void **bits_dev);
-/* Launch stream: NULL selects the sketch's own stream (the default). */
+/* Launch stream.  A new sketch launches on a private non-blocking stream;
+ * dhsa_set_stream switches to the caller's cudaStream_t (0 is CUDA's legacy default
+ * stream, as torch's default stream reports it), dhsa_set_own_stream switches back.
+ * Work queued on the old stream is ordered before work on the new one. */
 int dhsa_set_stream(dhsa_sketch_t *s, void *cuda_stream);
+int dhsa_set_own_stream(dhsa_sketch_t *s);
 int dhsa_get_stream(dhsa_sketch_t *s, void **cuda_stream);
 int dhsa_set_scan_mode(dhsa_sketch_t *s, int mode);
+/* Flow cache of DHSA_SCAN_FLOW_CACHE: n_sets sets x 32 bytes (default 2^21 -> 64 MiB,
+ * allocated on first use; 1024 <= n_sets <= 2^27).  The cache only ever skips a packet whose
+ * exact (cand, opp) pair was already scanned into this sketch since its last reset, so the
+ * bits are identical with or without it.  stats: pairs looked up / found since the reset. */
+int dhsa_set_flow_cache(dhsa_sketch_t *s, uint64_t n_sets);
+int dhsa_flow_cache_stats(dhsa_sketch_t *s, uint64_t *lookups, uint64_t *hits);
 /* Kernel launches issued through this handle so far (bench.py's gpu_launches). */
 int dhsa_launch_count(const dhsa_sketch_t *s, uint64_t *n);
 

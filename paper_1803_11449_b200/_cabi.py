@@ -53,8 +53,11 @@ SIGNATURES = {
     "dhsa_sketch_bytes": [_vp, C.POINTER(_u64)],
     "dhsa_bits_device_ptr": [_vp, C.POINTER(_vp)],
     "dhsa_set_stream": [_vp, _vp],
+    "dhsa_set_own_stream": [_vp],
     "dhsa_get_stream": [_vp, C.POINTER(_vp)],
     "dhsa_set_scan_mode": [_vp, C.c_int],
+    "dhsa_set_flow_cache": [_vp, _u64],
+    "dhsa_flow_cache_stats": [_vp, C.POINTER(_u64), C.POINTER(_u64)],
     "dhsa_launch_count": [_vp, C.POINTER(_u64)],
     "dhsa_update_device": [_vp, _vp, _vp, _u64],
     "dhsa_update_host": [_vp, _vp, _vp, _u64],

@@ -67,6 +67,12 @@ struct dhsa_sketch {
     std::mutex mu;
     uint64_t launches;
 
+    // flow cache of scan mode 3
+    unsigned long long *fcache;
+    unsigned long long *fc_stats;  // device: lookups, hits
+    uint32_t fc_sets;              // requested size in sets; the table is allocated on first use
+    bool fc_dirty;                 // holds entries since the last clear
+
     // read-out workspaces
     Control *ctl;           // device
     Control *ctl_host;      // pinned mirror
@@ -177,6 +183,7 @@ extern "C" int dhsa_create(const dhsa_params_t *params, int device, dhsa_sketch_
     s->device = device;
     CU(cudaDeviceGetAttribute(&s->sm_count, cudaDevAttrMultiProcessorCount, device));
     s->scan_mode = DHSA_SCAN_TEST_AGG_RED;
+    s->fc_sets = 1u << 21;
     const uint64_t m = 1ull << params->k;
     s->nbytes = (uint64_t)params->r * m * ((uint64_t)params->g / 8);
     s->alloc_bytes = (s->nbytes + 15) & ~15ull;
@@ -224,11 +231,66 @@ extern "C" int dhsa_destroy(dhsa_sketch_t *s)
         }
     }
     cudaFree(s->bits);
+    cudaFree(s->fcache);
+    cudaFree(s->fc_stats);
     cudaFree(s->ctl);
     cudaFreeHost(s->ctl_host);
     cudaStreamDestroy(s->own_stream);
     cudaStreamDestroy(s->copy_stream);
     delete s;
+    return DHSA_OK;
+}
+
+// The flow cache asserts "this pair's bits are in the sketch": it must be emptied
+// whenever bits can disappear (reset, upload).  Stream-ordered with the scans.
+static int clear_flow_cache_locked(dhsa_sketch *s)
+{
+    if (!s->fcache || !s->fc_dirty) return DHSA_OK;
+    CU(cudaMemsetAsync(s->fcache, 0, (size_t)32 * s->dp.fc_sets, s->stream));
+    CU(cudaMemsetAsync(s->fc_stats, 0, 2 * sizeof(unsigned long long), s->stream));
+    s->fc_dirty = false;
+    return DHSA_OK;
+}
+
+static int ensure_flow_cache_locked(dhsa_sketch *s)
+{
+    if (s->fcache && s->dp.fc_sets == s->fc_sets) return DHSA_OK;
+    CU(cudaStreamSynchronize(s->stream));
+    cudaFree(s->fcache);
+    s->fcache = nullptr;
+    if (!s->fc_stats) CU(cudaMalloc(&s->fc_stats, 2 * sizeof(unsigned long long)));
+    CU(cudaMalloc(&s->fcache, (size_t)32 * s->fc_sets));
+    s->dp.fc_sets = s->fc_sets;
+    s->dp.fcache = s->fcache;
+    s->dp.fc_stats = s->fc_stats;
+    s->fc_dirty = true;
+    return clear_flow_cache_locked(s);
+}
+
+extern "C" int dhsa_set_flow_cache(dhsa_sketch_t *s, uint64_t n_sets)
+{
+    NEED(s);
+    if (n_sets < 1024 || n_sets > (1ull << 27))
+        return fail(DHSA_ECONFIG, "flow cache size must satisfy 1024 <= n_sets <= 2^27 (got %llu)",
+                    (unsigned long long)n_sets);
+    std::lock_guard<std::mutex> lk(s->mu);
+    s->fc_sets = (uint32_t)n_sets;
+    return DHSA_OK;
+}
+
+extern "C" int dhsa_flow_cache_stats(dhsa_sketch_t *s, uint64_t *lookups, uint64_t *hits)
+{
+    NEED(s);
+    NEED(lookups);
+    NEED(hits);
+    *lookups = *hits = 0;
+    std::lock_guard<std::mutex> lk(s->mu);
+    if (!s->fc_stats) return DHSA_OK;
+    if (int rc = use_device(s)) return rc;
+    unsigned long long v[2];
+    CU(cudaMemcpyAsync(v, s->fc_stats, sizeof v, cudaMemcpyDeviceToHost, s->stream));
+    CU(cudaStreamSynchronize(s->stream));
+    *lookups = v[0], *hits = v[1];
     return DHSA_OK;
 }
 
@@ -238,7 +300,7 @@ extern "C" int dhsa_reset(dhsa_sketch_t *s)
     std::lock_guard<std::mutex> lk(s->mu);
     if (int rc = use_device(s)) return rc;
     CU(cudaMemsetAsync(s->bits, 0, s->alloc_bytes, s->stream));
-    return DHSA_OK;
+    return clear_flow_cache_locked(s);
 }
 
 extern "C" int dhsa_sketch_bytes(const dhsa_sketch_t *s, uint64_t *nbytes)
@@ -257,22 +319,33 @@ extern "C" int dhsa_bits_device_ptr(dhsa_sketch_t *s, void **bits_dev)
     return DHSA_OK;
 }
 
+static int switch_stream_locked(dhsa_sketch *s, cudaStream_t next)
+{
+    if (next == s->stream) return DHSA_OK;
+    // work already queued on the old stream must precede work on the new one
+    cudaEvent_t ev;
+    CU(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+    CU(cudaEventRecord(ev, s->stream));
+    CU(cudaStreamWaitEvent(next, ev, 0));
+    CU(cudaEventDestroy(ev));
+    s->stream = next;
+    return DHSA_OK;
+}
+
 extern "C" int dhsa_set_stream(dhsa_sketch_t *s, void *cuda_stream)
 {
     NEED(s);
     std::lock_guard<std::mutex> lk(s->mu);
     if (int rc = use_device(s)) return rc;
-    // work already queued on the old stream must precede work on the new one
-    cudaStream_t next = cuda_stream ? (cudaStream_t)cuda_stream : s->own_stream;
-    if (next != s->stream) {
-        cudaEvent_t ev;
-        CU(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
-        CU(cudaEventRecord(ev, s->stream));
-        CU(cudaStreamWaitEvent(next, ev, 0));
-        CU(cudaEventDestroy(ev));
-        s->stream = next;
-    }
-    return DHSA_OK;
+    return switch_stream_locked(s, (cudaStream_t)cuda_stream);
+}
+
+extern "C" int dhsa_set_own_stream(dhsa_sketch_t *s)
+{
+    NEED(s);
+    std::lock_guard<std::mutex> lk(s->mu);
+    if (int rc = use_device(s)) return rc;
+    return switch_stream_locked(s, s->own_stream);
 }
 
 extern "C" int dhsa_get_stream(dhsa_sketch_t *s, void **cuda_stream)
@@ -286,7 +359,7 @@ extern "C" int dhsa_get_stream(dhsa_sketch_t *s, void **cuda_stream)
 extern "C" int dhsa_set_scan_mode(dhsa_sketch_t *s, int mode)
 {
     NEED(s);
-    if (mode < 0 || mode > 2) return fail(DHSA_ECONFIG, "scan mode must be 0, 1 or 2 (got %d)", mode);
+    if (mode < 0 || mode > 3) return fail(DHSA_ECONFIG, "scan mode must be 0, 1, 2 or 3 (got %d)", mode);
     s->scan_mode = mode;
     return DHSA_OK;
 }
@@ -308,7 +381,8 @@ static void launch_scan_vec(dhsa_sketch *s, int mode, int grid, const uint4 *c4,
     switch (mode) {
     case 0: k_scan_vec4<R, 0><<<grid, 256, 0, s->stream>>>(c4, o4, nvec, w, s->dp); break;
     case 1: k_scan_vec4<R, 1><<<grid, 256, 0, s->stream>>>(c4, o4, nvec, w, s->dp); break;
-    default: k_scan_vec4<R, 2><<<grid, 256, 0, s->stream>>>(c4, o4, nvec, w, s->dp); break;
+    case 2: k_scan_vec4<R, 2><<<grid, 256, 0, s->stream>>>(c4, o4, nvec, w, s->dp); break;
+    default: k_scan_flowcache<R><<<grid, 256, 0, s->stream>>>(c4, o4, nvec, w, s->dp); break;
     }
 }
 
@@ -318,8 +392,9 @@ static int scan_blocks_per_sm()
     static int cached = 0;
     if (!cached) {
         int nb = 0;
-        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_scan_vec4<R, MODE>, 256, 0) != cudaSuccess || nb < 1)
-            nb = 2;
+        cudaError_t e = MODE == 3 ? cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_scan_flowcache<R>, 256, 0)
+                                  : cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_scan_vec4<R, MODE == 3 ? 2 : MODE>, 256, 0);
+        if (e != cudaSuccess || nb < 1) nb = 2;
         cached = nb;
     }
     return cached;
@@ -328,7 +403,8 @@ static int scan_blocks_per_sm()
 static int scan_occupancy(int r, int mode)
 {
 #define OCC(R_)                                                                                   \
-    (mode == 0 ? scan_blocks_per_sm<R_, 0>() : mode == 1 ? scan_blocks_per_sm<R_, 1>() : scan_blocks_per_sm<R_, 2>())
+    (mode == 0 ? scan_blocks_per_sm<R_, 0>() : mode == 1 ? scan_blocks_per_sm<R_, 1>() : \
+     mode == 2 ? scan_blocks_per_sm<R_, 2>() : scan_blocks_per_sm<R_, 3>())
     switch (r) {
     case 3: return OCC(3);
     case 4: return OCC(4);
@@ -349,6 +425,10 @@ static int scan_locked(dhsa_sketch *s, const uint32_t *cand, const uint32_t *opp
                       (((uintptr_t)cand | (uintptr_t)opp) & 15u) == 0;
     uint64_t done = 0;
     if (fast && n >= 4) {
+        if (s->scan_mode == DHSA_SCAN_FLOW_CACHE) {
+            if (int rc = ensure_flow_cache_locked(s)) return rc;
+            s->fc_dirty = true;
+        }
         const uint64_t nvec = n / 4;
         const int occ = scan_occupancy(p.r, s->scan_mode);
         const int grid = grid_for(s, nvec, 256, occ);
@@ -462,6 +542,7 @@ extern "C" int dhsa_upload_bits(dhsa_sketch_t *s, const uint8_t *bits_host, uint
     std::lock_guard<std::mutex> lk(s->mu);
     if (int rc = use_device(s)) return rc;
     CU(cudaMemcpyAsync(s->bits, bits_host, nbytes, cudaMemcpyHostToDevice, s->stream));
+    if (int rc = clear_flow_cache_locked(s)) return rc;
     CU(cudaStreamSynchronize(s->stream));
     return DHSA_OK;
 }

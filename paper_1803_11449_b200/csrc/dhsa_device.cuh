@@ -25,6 +25,10 @@ struct DevParams {
     uint64_t state_dh0, state_h1;
     uint64_t ncell;   // r * 2^k
     uint64_t nwords;  // 32-bit words backing the bit array (allocation is padded to 16 B)
+    // flow cache (scan mode 3): fc_sets sets of 4 ways x 8 B, one 32-byte sector per set
+    unsigned long long *fcache;
+    uint32_t fc_sets;
+    unsigned long long *fc_stats;  // [0] lookups, [1] hits
 };
 
 // Device-resident control block of one read-out: every stage kernel reads its
@@ -116,6 +120,21 @@ __device__ __forceinline__ uint32_t ld_sketch(const uint32_t *ptr)
     return v;
 }
 
+// One flow-cache set: 4 ways x 8 B = one 32-byte sector, fetched with a single
+// 256-bit load (sm_100a).  Served from L2 only: the table is far larger than L1.
+__device__ __forceinline__ void ld_fc_set(const unsigned long long *set, unsigned long long (&e)[4])
+{
+    asm volatile("ld.global.cg.v4.u64 {%0,%1,%2,%3}, [%4];"
+                 : "=l"(e[0]), "=l"(e[1]), "=l"(e[2]), "=l"(e[3])
+                 : "l"(set)
+                 : "memory");
+}
+
+__device__ __forceinline__ void st_fc_way(unsigned long long *slot, unsigned long long v)
+{
+    asm volatile("st.global.cg.u64 [%0], %1;" ::"l"(slot), "l"(v) : "memory");
+}
+
 // Fire-and-forget atomic OR (SASS: RED.E.OR), resolved in the L2 slice that owns the word.
 __device__ __forceinline__ void red_or(uint32_t *ptr, uint32_t m)
 {
@@ -138,6 +157,42 @@ __device__ __forceinline__ void red_or(uint32_t *ptr, uint32_t m)
 //   MODE 2  as 1, plus warp aggregation: lanes that still need a RED vote,
 //           __match_any_sync groups them by word, masks are OR-ed inside a
 //           group and its lowest lane issues one RED.
+//   (the flow-cache variant, scan mode 3, is k_scan_flowcache below)
+
+// Warp-aggregated RED of one (word, mask) per lane: lanes that need one vote,
+// __match_any_sync groups them by word, the group's masks are OR-ed and its
+// lowest lane issues a single RED.  Called by all 32 lanes.
+__device__ __forceinline__ void red_or_aggregated(uint32_t *words, uint32_t widx, uint32_t mask, bool need,
+                                                  uint32_t lane)
+{
+    const unsigned nm = __ballot_sync(0xFFFFFFFFu, need);
+    if (nm == 0) return;  // warp-uniform: nothing new in this slot
+    if (need) {
+        uint32_t m = mask;
+        unsigned peers = 1u << lane;
+        if (nm & (nm - 1)) {  // more than one lane: group by word
+            peers = __match_any_sync(nm, widx);
+            if (peers & (peers - 1)) {  // every member folds every member's mask
+                for (unsigned q = peers; q; q &= q - 1) m |= __shfl_sync(peers, mask, __ffs(q) - 1);
+            }
+        }
+        if (lane == (uint32_t)(__ffs(peers) - 1)) red_or(words + widx, m);
+    }
+}
+
+template <int R>
+__device__ __forceinline__ void packet_slots(const DevParams &p, int wshift, uint32_t cand, uint32_t h, uint32_t d0,
+                                             uint32_t (&widx)[R])
+{
+    const uint32_t hw = h >> 5;
+#pragma unroll
+    for (int i = 0; i < R; i++) {
+        const uint32_t idx = i == 0 ? d0 : (((uint32_t)((uint64_t)cand >> ((i - 1) * p.alpha)) & p.kmask) ^ d0);
+        const uint32_t cell = ((uint32_t)i << p.k) | idx;
+        widx[i] = (cell << wshift) + hw;
+    }
+}
+
 template <int R, int MODE>
 __global__ void __launch_bounds__(256) k_scan_vec4(const uint4 *__restrict__ cand4,
                                                    const uint4 *__restrict__ opp4, uint64_t nvec,
@@ -159,22 +214,15 @@ __global__ void __launch_bounds__(256) k_scan_vec4(const uint4 *__restrict__ can
         }
         const uint32_t cs[4] = {c.x, c.y, c.z, c.w};
         const uint32_t os[4] = {o.x, o.y, o.z, o.w};
+
         uint32_t widx[4][R];
         uint32_t mask[4];
 #pragma unroll
         for (int j = 0; j < 4; j++) {
-            const uint64_t a = cs[j];
             const uint32_t h = (uint32_t)mix64(p.state_h1 ^ (uint64_t)os[j]) & p.gmask;
-            const uint32_t d0 = (uint32_t)mix64(p.state_dh0 ^ a) & p.kmask;
+            const uint32_t d0 = (uint32_t)mix64(p.state_dh0 ^ (uint64_t)cs[j]) & p.kmask;
             mask[j] = 1u << (h & 31u);
-            const uint32_t hw = h >> 5;
-#pragma unroll
-            for (int i = 0; i < R; i++) {
-                const uint32_t idx =
-                    i == 0 ? d0 : (((uint32_t)(a >> ((i - 1) * p.alpha)) & p.kmask) ^ d0);
-                const uint32_t cell = ((uint32_t)i << p.k) | idx;
-                widx[j][i] = (cell << wshift) + hw;
-            }
+            packet_slots<R>(p, wshift, cs[j], h, d0, widx[j]);
         }
         if (MODE == 0) {
             if (valid) {
@@ -184,39 +232,163 @@ __global__ void __launch_bounds__(256) k_scan_vec4(const uint4 *__restrict__ can
                     for (int i = 0; i < R; i++) red_or(words + widx[j][i], mask[j]);
             }
         } else {
-        uint32_t w[4][R];
+            // all 4 * R test loads are issued before the first is consumed
+            uint32_t w[4][R];
 #pragma unroll
-        for (int j = 0; j < 4; j++)
+            for (int j = 0; j < 4; j++)
 #pragma unroll
-            for (int i = 0; i < R; i++) w[j][i] = valid ? ld_sketch(words + widx[j][i]) : 0xFFFFFFFFu;
+                for (int i = 0; i < R; i++) w[j][i] = valid ? ld_sketch(words + widx[j][i]) : 0xFFFFFFFFu;
 #pragma unroll
-        for (int j = 0; j < 4; j++) {
+            for (int j = 0; j < 4; j++) {
 #pragma unroll
-            for (int i = 0; i < R; i++) {
-                const bool need = (w[j][i] & mask[j]) == 0;
-                if (MODE == 1) {
-                    if (need) red_or(words + widx[j][i], mask[j]);
-                } else {
-                    const unsigned nm = __ballot_sync(0xFFFFFFFFu, need);
-                    if (nm == 0) continue;  // warp-uniform: nothing new in this slot
-                    if (need) {
-                        uint32_t m = mask[j];
-                        unsigned peers = 1u << lane;
-                        if (nm & (nm - 1)) {  // more than one lane: group by word
-                            peers = __match_any_sync(nm, widx[j][i]);
-                            if (peers & (peers - 1)) {  // every member folds every member's mask
-                                for (unsigned q = peers; q; q &= q - 1)
-                                    m |= __shfl_sync(peers, mask[j], __ffs(q) - 1);
-                            }
-                        }
-                        if (lane == (uint32_t)(__ffs(peers) - 1)) red_or(words + widx[j][i], m);
+                for (int i = 0; i < R; i++) {
+                    const bool need = (w[j][i] & mask[j]) == 0;
+                    if (MODE == 1) {
+                        if (need) red_or(words + widx[j][i], mask[j]);
+                    } else {
+                        red_or_aggregated(words, widx[j][i], mask[j], need, lane);
                     }
                 }
             }
         }
-        }  // MODE != 0
     }
 }
+
+// K1, scan mode 3: the scan behind an exact flow cache.
+//
+// ncu shows k_scan_vec4 pinned at one L1-miss request per clock per SM
+// (l1tex__m_l1tex2xbar_req_cycles_active 92%) with 5 sketch sectors per packet,
+// so the lever is fewer scattered accesses per packet.  Real windows carry many
+// packets per flow (BASELINE config 2: ~26), and a repeated (cand, opp) pair
+// changes nothing in the sketch.  The cache is a 4-way set-associative table of
+// whole pairs in L2, one 32-byte sector per set, read with a single 256-bit load:
+// a packet whose pair is present was scanned earlier in this window and is
+// dropped after ONE scattered access instead of five.
+//
+//   exactness  an entry is written only by a lane that has just issued the
+//              pair's own test+RED, the table is cleared whenever bits can
+//              disappear (reset, upload), and nothing reads bits before the
+//              kernel ends -- so "present => bits set at kernel end" always holds
+//              and a missing / evicted / racing entry only costs a rescan.
+//   encoding   entries hold ~pair, 0 = empty; the all-ones pair therefore never
+//              hits and is always rescanned.
+//   misses     are compacted by ballot into a per-warp shared-memory queue and
+//              drained 32 at a time, one missed packet per lane with its R test
+//              loads in flight together, so a miss costs one more L2 round trip
+//              per 32 misses, not per packet slot.
+//   pipeline   the next trip's packets are requested before this trip's table
+//              sets are consumed.
+#define DHSA_FC_QCAP 160  // < 32 left over + up to 128 pushed per trip
+
+struct FcMiss {
+    uint32_t cand, opp, slot;  // slot = set * 4 + way to fill
+};
+
+template <int R>
+__device__ __forceinline__ void fc_drain32(uint32_t *__restrict__ words, const DevParams &p, int wshift,
+                                           const FcMiss *q, uint32_t n_active, uint32_t lane)
+{
+    const bool act = lane < n_active;
+    FcMiss m = {0u, 0u, 0u};
+    if (act) m = q[lane];
+    const uint32_t h = (uint32_t)mix64(p.state_h1 ^ (uint64_t)m.opp) & p.gmask;
+    const uint32_t d0 = (uint32_t)mix64(p.state_dh0 ^ (uint64_t)m.cand) & p.kmask;
+    const uint32_t mask = 1u << (h & 31u);
+    uint32_t widx[R], w[R];
+    packet_slots<R>(p, wshift, m.cand, h, d0, widx);
+#pragma unroll
+    for (int i = 0; i < R; i++) w[i] = act ? ld_sketch(words + widx[i]) : 0xFFFFFFFFu;
+#pragma unroll
+    for (int i = 0; i < R; i++) red_or_aggregated(words, widx[i], mask, (w[i] & mask) == 0, lane);
+    // the pair now counts as scanned: its tests/REDs above are issued before this store
+    if (act) st_fc_way(p.fcache + m.slot, ~(((unsigned long long)m.cand << 32) | (unsigned long long)m.opp));
+}
+
+template <int R>
+__global__ void __launch_bounds__(256, 3) k_scan_flowcache(const uint4 *__restrict__ cand4,
+                                                           const uint4 *__restrict__ opp4, uint64_t nvec,
+                                                           uint32_t *__restrict__ words, DevParams p)
+{
+    __shared__ FcMiss queue_s[8][DHSA_FC_QCAP];
+    const uint32_t lane = threadIdx.x & 31u;
+    FcMiss *q = queue_s[threadIdx.x >> 5];
+    uint32_t qn = 0;  // warp-uniform queue length
+    const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+    const uint64_t warp0 = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int wshift = p.log2g - 5;
+    const uint64_t pol = policy_evict_first();
+    const uint32_t lt_mask = (1u << lane) - 1u;
+    unsigned long long fc_hits = 0, fc_lookups = 0;
+
+    uint64_t base = warp0 * 32;
+    uint4 c_next = make_uint4(0, 0, 0, 0), o_next = make_uint4(0, 0, 0, 0);
+    if (base + lane < nvec) {
+        c_next = ld_stream_v4(cand4 + base + lane, pol);
+        o_next = ld_stream_v4(opp4 + base + lane, pol);
+    }
+    for (; base < nvec; base += nwarps * 32) {
+        const bool valid = base + lane < nvec;
+        const uint32_t cs[4] = {c_next.x, c_next.y, c_next.z, c_next.w};
+        const uint32_t os[4] = {o_next.x, o_next.y, o_next.z, o_next.w};
+        {   // request the next trip's packets now; they land while the table sets are in flight
+            const uint64_t vn = base + nwarps * 32 + lane;
+            if (vn < nvec) {
+                c_next = ld_stream_v4(cand4 + vn, pol);
+                o_next = ld_stream_v4(opp4 + vn, pol);
+            }
+        }
+        unsigned long long e[4][4];
+        uint32_t set_idx[4], way_hint[4];
+#pragma unroll
+        for (int j = 0; j < 4; j++) {
+            const uint64_t hh = mix64(p.state_h1 ^ (uint64_t)os[j]);
+            const uint64_t hd = mix64(p.state_dh0 ^ (uint64_t)cs[j]);
+            // set index from the high halves of both hashes (their low bits feed h and d0)
+            // (multiply-shift range reduction: any set count, not only powers of two)
+            set_idx[j] = __umulhi((uint32_t)(hh >> 32) + (uint32_t)(hd >> 32) * 0x9E3779B1u, p.fc_sets);
+            way_hint[j] = (uint32_t)(hd >> 30) & 3u;
+            if (valid) ld_fc_set(p.fcache + ((size_t)set_idx[j] << 2), e[j]);
+        }
+#pragma unroll
+        for (int j = 0; j < 4; j++) {
+            const unsigned long long inv_key = ~(((unsigned long long)cs[j] << 32) | (unsigned long long)os[j]);
+            const bool hit = valid && inv_key != 0ull &&
+                             (e[j][0] == inv_key || e[j][1] == inv_key || e[j][2] == inv_key || e[j][3] == inv_key);
+            const bool miss = valid && !hit;
+            fc_hits += hit;
+            const unsigned bal = __ballot_sync(0xFFFFFFFFu, miss);
+            if (bal == 0) continue;
+            if (miss) {
+                // first empty way of the set as loaded, else a hashed victim (a race only loses an entry)
+                uint32_t way = way_hint[j];
+                if (e[j][3] == 0ull) way = 3;
+                if (e[j][2] == 0ull) way = 2;
+                if (e[j][1] == 0ull) way = 1;
+                if (e[j][0] == 0ull) way = 0;
+                FcMiss m = {cs[j], os[j], (set_idx[j] << 2) | way};
+                q[qn + __popc(bal & lt_mask)] = m;
+            }
+            qn += __popc(bal);
+        }
+        fc_lookups += valid ? 4 : 0;
+        __syncwarp();
+        while (qn >= 32) {  // dense drains: the newest 32 entries, one per lane
+            qn -= 32;
+            fc_drain32<R>(words, p, wshift, q + qn, 32, lane);
+        }
+        __syncwarp();
+    }
+    if (qn) fc_drain32<R>(words, p, wshift, q, qn, lane);
+    for (int d = 16; d > 0; d >>= 1) {
+        fc_hits += __shfl_xor_sync(0xFFFFFFFFu, fc_hits, d);
+        fc_lookups += __shfl_xor_sync(0xFFFFFFFFu, fc_lookups, d);
+    }
+    if (lane == 0 && fc_lookups) {
+        atomicAdd(p.fc_stats + 0, fc_lookups);
+        atomicAdd(p.fc_stats + 1, fc_hits);
+    }
+}
+
 
 // General path: any r <= 64, any g >= 8 (sub-word cells included), 64-bit bit
 // addressing, unaligned input pointers.  One packet per lane per trip.

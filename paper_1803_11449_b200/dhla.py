@@ -31,7 +31,7 @@ from .errors import ConfigError
 
 DEFAULT_MAX_CANDIDATES = 1 << 20  # pkg/src/dhsa/dhla.py:34
 
-SCAN_MODES = {"red": 0, "test": 1, "test_agg": 2}
+SCAN_MODES = {"red": 0, "test": 1, "test_agg": 2, "flow_cache": 3}
 
 _REPORT_DTYPE = np.dtype([("host", "<u8"), ("estimate", "<f8"), ("saturated", "<i4"), ("sz", "<i4")])
 assert _REPORT_DTYPE.itemsize == C.sizeof(_cabi.Report)
@@ -115,11 +115,25 @@ class Dhla:
         return int(n.value)
 
     def use_stream(self, cuda_stream: Optional[int]) -> None:
-        """Launch on this CUDA stream handle (None -> the sketch's own stream)."""
-        _cabi.check(self._lib.dhsa_set_stream(self._h, C.c_void_p(cuda_stream or 0)))
+        """Launch on this cudaStream_t handle (0 = CUDA's legacy default stream, which is
+        what torch's default stream reports); None -> back to the sketch's own stream."""
+        if cuda_stream is None:
+            _cabi.check(self._lib.dhsa_set_own_stream(self._h))
+        else:
+            _cabi.check(self._lib.dhsa_set_stream(self._h, C.c_void_p(int(cuda_stream))))
 
     def set_scan_mode(self, mode) -> None:
         _cabi.check(self._lib.dhsa_set_scan_mode(self._h, SCAN_MODES.get(mode, mode)))
+
+    def set_flow_cache(self, n_sets: int) -> None:
+        """Size of the flow cache used by scan mode "flow_cache": n_sets x 32 bytes."""
+        _cabi.check(self._lib.dhsa_set_flow_cache(self._h, int(n_sets)))
+
+    def flow_cache_stats(self) -> tuple:
+        """(pairs looked up, pairs found) since the last reset."""
+        a, b = C.c_uint64(), C.c_uint64()
+        _cabi.check(self._lib.dhsa_flow_cache_stats(self._h, C.byref(a), C.byref(b)))
+        return int(a.value), int(b.value)
 
     # --- the bits attribute ----------------------------------------------------
 

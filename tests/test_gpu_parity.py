@@ -54,7 +54,10 @@ def gpu_for_case(case, mode="test_agg"):
 # ------------------------------------------------------------------------ scan --
 
 
-@pytest.mark.parametrize("mode", ["red", "test", "test_agg"])
+MODES = ["red", "test", "test_agg", "flow_cache"]
+
+
+@pytest.mark.parametrize("mode", MODES)
 @pytest.mark.parametrize("name", list(PARAM_SETS))
 def test_update_batch_bits_equal_oracle(name, mode):
     # pkg/tests/test_kernels.py:37-48 (compiled == numpy), here CUDA == oracle
@@ -142,7 +145,7 @@ def test_concurrent_updates_from_threads_are_lossless():
     assert np.array_equal(shared.bits, ora.bits)
 
 
-@pytest.mark.parametrize("mode", ["red", "test", "test_agg"])
+@pytest.mark.parametrize("mode", MODES)
 def test_ddos_contention_all_packets_hit_the_same_cells(mode):
     # BASELINE config 4 shape: many sources -> few victims, victims as candidates
     rng = np.random.default_rng(44)
@@ -159,6 +162,47 @@ def test_ddos_contention_all_packets_hit_the_same_cells(mode):
     got, want = sk.restore_superpoints(1024), ora.restore_superpoints(1024)
     assert [(r.host, r.saturated) for r in got] == [(r.host, r.saturated) for r in want]
     assert all(r.saturated for r in got) and len(got) == 4
+
+
+@pytest.mark.parametrize("n_sets", [1024, 50_000, 1 << 21])
+def test_flow_cache_is_exact_across_batches_resets_and_uploads(n_sets):
+    """The cache may only skip pairs whose bits are already in the sketch: heavy
+    duplication over several batches, tiny tables that evict constantly, the
+    all-ones pair (never cached), then reset and load_bits, which must empty it."""
+    rng = np.random.default_rng(5)
+    base_c, base_o = O.distinct_pairs(60_000, 31)
+    base_c = np.concatenate([base_c, np.array([0xFFFFFFFF, 0, 0xFFFFFFFF], np.uint32)])
+    base_o = np.concatenate([base_o, np.array([0xFFFFFFFF, 0, 0], np.uint32)])
+    sk = P.Dhla(P.DhgParams())
+    sk.set_scan_mode("flow_cache")
+    sk.set_flow_cache(n_sets)
+    ora = O.OracleSketch()
+    for _ in range(3):
+        pick = rng.integers(0, len(base_c), size=400_000)
+        sk.update_batch(base_c[pick], base_o[pick])
+        ora.update_batch(base_c[pick], base_o[pick], threads=4)
+        assert np.array_equal(sk.bits, ora.bits)
+    lookups, hits = sk.flow_cache_stats()
+    assert lookups == 1_200_000 and 0 < hits < lookups
+    # reset: same pairs again must set their bits again
+    sk.reset()
+    pick = rng.integers(0, len(base_c), size=100_000)
+    sk.update_batch(base_c[pick], base_o[pick])
+    fresh = O.OracleSketch()
+    fresh.update_batch(base_c[pick], base_o[pick])
+    assert np.array_equal(sk.bits, fresh.bits)
+    # load_bits with cleared cells: cached pairs must not be trusted afterwards
+    sk.load_bits(np.zeros_like(fresh.bits))
+    sk.update_batch(base_c[pick], base_o[pick])
+    assert np.array_equal(sk.bits, fresh.bits)
+    # merge only adds bits: the cache stays valid and the result is still exact
+    other = P.Dhla(P.DhgParams())
+    oc, oo = O.distinct_pairs(10_000, 32)
+    other.update_batch(oc, oo)
+    sk.merge_from(other)
+    sk.update_batch(base_c[pick], base_o[pick])
+    fresh.update_batch(oc, oo)
+    assert np.array_equal(sk.bits, fresh.bits)
 
 
 def test_reset_and_load_bits_round_trip():
@@ -420,7 +464,7 @@ def _window(n_packets, n_hosts, n_scanners, seed):
     return src, dst, ct, ot, hosts[n_hosts:]
 
 
-@pytest.mark.parametrize("mode", ["test", "test_agg", "red"])
+@pytest.mark.parametrize("mode", ["flow_cache", "test_agg", "test", "red"])
 def test_100m_packet_window_bits_and_superpoints_equal_oracle(mode):
     """BASELINE config 2 size.  The oracle scans the distinct flows only; the GPU
     scans all 100M packets; bits, super point set and estimates must agree."""
