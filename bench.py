@@ -319,7 +319,7 @@ def run_ours(args, rank: int, local_rank: int, world: int) -> None:
         else:
             peak, peak_src = 6650.0, "fallback (B200_PROFILING.md)"
         achieved = 8.0 * n / (scan_ms * 1e-3) / 1e9
-        kernel = "k_scan_flowcache<5>" if args.scan_mode == "flow_cache" else \
+        kernel = "k_scan_flowcache<5>" if args.scan_mode in ("flow_cache", "auto") else \
             f"k_scan_vec4<5,{P.dhla.SCAN_MODES[args.scan_mode]}>"
         roofline = {
             "bound": "hbm", "kernel": kernel,
@@ -328,6 +328,15 @@ def run_ours(args, rank: int, local_rank: int, world: int) -> None:
             "launch_ms": scan_ms, "packets_per_launch": n, "scan_gpps": n / (scan_ms * 1e-3) / 1e9,
             "traffic": args.traffic_bytes,
         }
+        if roofline["traffic"] is None:
+            # dram__bytes_read.sum + dram__bytes_write.sum of one 100M-packet launch, from the committed ncu capture
+            tpath = os.path.join(ROOT, "profiles", "r01_traffic.json")
+            if os.path.exists(tpath) and n == 100_000_000:
+                entry = json.load(open(tpath)).get(kernel.split(",")[0] + (",2>" if "vec4" in kernel else ""), None) \
+                    or json.load(open(tpath)).get(kernel)
+                if entry:
+                    roofline["traffic"] = entry["dram_bytes_per_launch"]
+                    roofline["traffic_source"] = "profiles/r01_traffic.json (ncu --set full)"
         if l2:
             # The ceiling that actually binds (north star: the slower of HBM streaming and the sketch's
             # L2 traffic): ncu shows the scan limited by one L1-miss request per clock per SM
@@ -338,7 +347,7 @@ def run_ours(args, rank: int, local_rank: int, world: int) -> None:
             roofline["hbm_ceiling_gpps"] = peak / 8.0
             roofline["sketch_ceiling_gpps_5_accesses"] = l2["ld_gops"] / 5.25
             roofline["red_ceiling_gpps_5_atomics"] = l2["red_gops"] / 5.0
-            req = 1.25 if args.scan_mode == "flow_cache" else (5.0 if args.scan_mode == "red" else 5.25)
+            req = 1.25 if args.scan_mode in ("flow_cache", "auto") else (5.0 if args.scan_mode == "red" else 5.25)
             rate = l2["red_gops"] if args.scan_mode == "red" else l2["ld_gops"]
             roofline["binding_ceiling_gpps"] = min(peak / 8.0, rate / req)
             roofline["binding_requests_per_packet"] = req
@@ -353,7 +362,7 @@ def run_ours(args, rank: int, local_rank: int, world: int) -> None:
                        "scan_mode": args.scan_mode, "merge": win.merged_with,
                        "flow_cache": ({"mib": args.flow_cache_mib,
                                        "hit_rate": (fc_hits / fc_lookups) if fc_lookups else None}
-                                      if args.scan_mode == "flow_cache" else None),
+                                      if args.scan_mode in ("flow_cache", "auto") else None),
                        "l2": "inputs (800 MB per GPU) larger than L2; sketch (10 MiB) L2-resident by design"},
             "phase_ms": {"scan": scan_ms, "merge+estimate+restore+filter": readout_ms},
             "roofline": roofline,
@@ -363,7 +372,7 @@ def run_ours(args, rank: int, local_rank: int, world: int) -> None:
         if parity:
             line["parity"] = parity
         if e2e:
-            reports_bytes = 24 * e2e[1] + 1584  # dhsa_report_t rows + the control block read back per window
+            reports_bytes = 24 * e2e[1] + 1608  # dhsa_report_t rows + the 1608-byte control block read back per window
             line["e2e"] = {"value": world * n * args.steps / (e2e_ms * 1e-3) / 1e6, "unit": "Mpps",
                            "h2d_bytes_per_step": 8 * n, "d2h_bytes_per_step": reports_bytes,
                            "ms_per_step": e2e_ms / args.steps}
@@ -392,7 +401,7 @@ def main() -> None:
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--packets", type=int, default=100_000_000, help="packets per GPU per window")
     ap.add_argument("--seed", type=int, default=100)
-    ap.add_argument("--scan-mode", default="flow_cache", choices=["red", "test", "test_agg", "flow_cache"])
+    ap.add_argument("--scan-mode", default="auto", choices=["red", "test", "test_agg", "flow_cache", "auto"])
     ap.add_argument("--flow-cache-mib", type=int, default=64, help="flow cache size; flow_cache mode only")
     ap.add_argument("--merge", default="auto", choices=["auto", "p2p", "allgather"])
     ap.add_argument("--cpu-sample", type=int, default=50_000_000)

@@ -12,6 +12,7 @@
 #include <math.h>
 #include <stdarg.h>
 #include <stdio.h>
+#include <stdlib.h>
 #include <string.h>
 
 #include <mutex>
@@ -72,6 +73,10 @@ struct dhsa_sketch {
     unsigned long long *fc_stats;  // device: lookups, hits
     uint32_t fc_sets;              // requested size in sets; the table is allocated on first use
     bool fc_dirty;                 // holds entries since the last clear
+    unsigned long long *fc_stats_host;  // pinned snapshot of fc_stats for the auto policy
+    cudaEvent_t fc_stats_ev;
+    bool fc_stats_pending;
+    bool auto_fell_back;           // auto mode: this window's flows do not repeat, use the 5-access kernel
 
     // read-out workspaces
     Control *ctl;           // device
@@ -182,7 +187,7 @@ extern "C" int dhsa_create(const dhsa_params_t *params, int device, dhsa_sketch_
     s->params = *params;
     s->device = device;
     CU(cudaDeviceGetAttribute(&s->sm_count, cudaDevAttrMultiProcessorCount, device));
-    s->scan_mode = DHSA_SCAN_TEST_AGG_RED;
+    s->scan_mode = DHSA_SCAN_AUTO;
     s->fc_sets = 1u << 21;
     const uint64_t m = 1ull << params->k;
     s->nbytes = (uint64_t)params->r * m * ((uint64_t)params->g / 8);
@@ -233,6 +238,10 @@ extern "C" int dhsa_destroy(dhsa_sketch_t *s)
     cudaFree(s->bits);
     cudaFree(s->fcache);
     cudaFree(s->fc_stats);
+    if (s->fc_stats_host) {
+        cudaFreeHost(s->fc_stats_host);
+        cudaEventDestroy(s->fc_stats_ev);
+    }
     cudaFree(s->ctl);
     cudaFreeHost(s->ctl_host);
     cudaStreamDestroy(s->own_stream);
@@ -249,6 +258,7 @@ static int clear_flow_cache_locked(dhsa_sketch *s)
     CU(cudaMemsetAsync(s->fcache, 0, (size_t)32 * s->dp.fc_sets, s->stream));
     CU(cudaMemsetAsync(s->fc_stats, 0, 2 * sizeof(unsigned long long), s->stream));
     s->fc_dirty = false;
+    s->auto_fell_back = false;  // a new window may repeat flows again
     return DHSA_OK;
 }
 
@@ -258,7 +268,12 @@ static int ensure_flow_cache_locked(dhsa_sketch *s)
     CU(cudaStreamSynchronize(s->stream));
     cudaFree(s->fcache);
     s->fcache = nullptr;
-    if (!s->fc_stats) CU(cudaMalloc(&s->fc_stats, 2 * sizeof(unsigned long long)));
+    if (!s->fc_stats) {
+        CU(cudaMalloc(&s->fc_stats, 2 * sizeof(unsigned long long)));
+        CU(cudaMallocHost(&s->fc_stats_host, 2 * sizeof(unsigned long long)));
+        CU(cudaEventCreateWithFlags(&s->fc_stats_ev, cudaEventDisableTiming));
+        s->fc_stats_host[0] = s->fc_stats_host[1] = 0;
+    }
     CU(cudaMalloc(&s->fcache, (size_t)32 * s->fc_sets));
     s->dp.fc_sets = s->fc_sets;
     s->dp.fcache = s->fcache;
@@ -359,7 +374,7 @@ extern "C" int dhsa_get_stream(dhsa_sketch_t *s, void **cuda_stream)
 extern "C" int dhsa_set_scan_mode(dhsa_sketch_t *s, int mode)
 {
     NEED(s);
-    if (mode < 0 || mode > 3) return fail(DHSA_ECONFIG, "scan mode must be 0, 1, 2 or 3 (got %d)", mode);
+    if (mode < 0 || mode > 4) return fail(DHSA_ECONFIG, "scan mode must be 0..4 (got %d)", mode);
     s->scan_mode = mode;
     return DHSA_OK;
 }
@@ -374,6 +389,40 @@ extern "C" int dhsa_launch_count(const dhsa_sketch_t *s, uint64_t *n)
 
 // -------------------------------------------------------------------- scan --
 
+// Tuning variants of the flow-cache kernel (experiments: DHSA_FC_VARIANT=0..5).
+static int fc_variant()
+{
+    static int v = -1;
+    if (v < 0) {
+        const char *e = getenv("DHSA_FC_VARIANT");
+        v = e ? atoi(e) : 0;
+    }
+    return v;
+}
+
+template <int R>
+static void launch_flowcache(dhsa_sketch *s, int grid_unused, const uint4 *c4, const uint4 *o4, uint64_t nvec)
+{
+    uint32_t *w = reinterpret_cast<uint32_t *>(s->bits);
+    (void)grid_unused;
+#define FC_LAUNCH(NV_, MINB_, EVL_)                                                                          \
+    do {                                                                                                     \
+        static int occ = 0;                                                                                  \
+        if (!occ && (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_scan_flowcache<R, NV_, MINB_, EVL_>, \
+                                                                   256, 0) != cudaSuccess || occ < 1))       \
+            occ = MINB_;                                                                                     \
+        const int g = grid_for(s, (nvec + NV_ - 1) / NV_, 256, occ);                                         \
+        k_scan_flowcache<R, NV_, MINB_, EVL_><<<g, 256, 0, s->stream>>>(c4, o4, nvec, w, s->dp);             \
+    } while (0)
+    // measured on B200 (profiles/r01_flowcache_variants.txt): 4 packets per lane at 3 CTAs/SM wins;
+    // 8 packets per lane, 4 CTAs/SM (spills) and L2::evict_last table loads were all slower or equal
+    switch (fc_variant()) {
+    case 2: FC_LAUNCH(2, 2, false); break;
+    default: FC_LAUNCH(1, 3, false); break;
+    }
+#undef FC_LAUNCH
+}
+
 template <int R>
 static void launch_scan_vec(dhsa_sketch *s, int mode, int grid, const uint4 *c4, const uint4 *o4, uint64_t nvec)
 {
@@ -382,7 +431,7 @@ static void launch_scan_vec(dhsa_sketch *s, int mode, int grid, const uint4 *c4,
     case 0: k_scan_vec4<R, 0><<<grid, 256, 0, s->stream>>>(c4, o4, nvec, w, s->dp); break;
     case 1: k_scan_vec4<R, 1><<<grid, 256, 0, s->stream>>>(c4, o4, nvec, w, s->dp); break;
     case 2: k_scan_vec4<R, 2><<<grid, 256, 0, s->stream>>>(c4, o4, nvec, w, s->dp); break;
-    default: k_scan_flowcache<R><<<grid, 256, 0, s->stream>>>(c4, o4, nvec, w, s->dp); break;
+    default: launch_flowcache<R>(s, grid, c4, o4, nvec); break;
     }
 }
 
@@ -392,8 +441,7 @@ static int scan_blocks_per_sm()
     static int cached = 0;
     if (!cached) {
         int nb = 0;
-        cudaError_t e = MODE == 3 ? cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_scan_flowcache<R>, 256, 0)
-                                  : cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_scan_vec4<R, MODE == 3 ? 2 : MODE>, 256, 0);
+        cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_scan_vec4<R, MODE == 3 ? 2 : MODE>, 256, 0);
         if (e != cudaSuccess || nb < 1) nb = 2;
         cached = nb;
     }
@@ -425,19 +473,39 @@ static int scan_locked(dhsa_sketch *s, const uint32_t *cand, const uint32_t *opp
                       (((uintptr_t)cand | (uintptr_t)opp) & 15u) == 0;
     uint64_t done = 0;
     if (fast && n >= 4) {
-        if (s->scan_mode == DHSA_SCAN_FLOW_CACHE) {
+        int mode = s->scan_mode;
+        if (mode == DHSA_SCAN_AUTO) {
+            // Auto: scan behind the flow cache, watch its hit rate through an asynchronous
+            // snapshot (never a sync), and fall back to the 5-access kernel for the rest of the
+            // window when flows do not repeat.  Break-even is a hit rate of about 1/3:
+            // 1 + 11 (1 - h) requests per packet with the cache against 5 + 5 (1 - h) without.
+            if (s->fc_stats_pending && cudaEventQuery(s->fc_stats_ev) == cudaSuccess) {
+                s->fc_stats_pending = false;
+                const unsigned long long lookups = s->fc_stats_host[0], hits = s->fc_stats_host[1];
+                if (lookups >= (1ull << 22) && hits * 10 < lookups * 3) s->auto_fell_back = true;
+            }
+            (void)cudaGetLastError();
+            mode = s->auto_fell_back ? DHSA_SCAN_TEST_AGG_RED : DHSA_SCAN_FLOW_CACHE;
+        }
+        if (mode == DHSA_SCAN_FLOW_CACHE) {
             if (int rc = ensure_flow_cache_locked(s)) return rc;
             s->fc_dirty = true;
         }
         const uint64_t nvec = n / 4;
-        const int occ = scan_occupancy(p.r, s->scan_mode);
+        const int occ = scan_occupancy(p.r, mode);
         const int grid = grid_for(s, nvec, 256, occ);
         const uint4 *c4 = reinterpret_cast<const uint4 *>(cand), *o4 = reinterpret_cast<const uint4 *>(opp);
         switch (p.r) {
-        case 3: launch_scan_vec<3>(s, s->scan_mode, grid, c4, o4, nvec); break;
-        case 4: launch_scan_vec<4>(s, s->scan_mode, grid, c4, o4, nvec); break;
-        case 5: launch_scan_vec<5>(s, s->scan_mode, grid, c4, o4, nvec); break;
-        default: launch_scan_vec<6>(s, s->scan_mode, grid, c4, o4, nvec); break;
+        case 3: launch_scan_vec<3>(s, mode, grid, c4, o4, nvec); break;
+        case 4: launch_scan_vec<4>(s, mode, grid, c4, o4, nvec); break;
+        case 5: launch_scan_vec<5>(s, mode, grid, c4, o4, nvec); break;
+        default: launch_scan_vec<6>(s, mode, grid, c4, o4, nvec); break;
+        }
+        if (s->scan_mode == DHSA_SCAN_AUTO && mode == DHSA_SCAN_FLOW_CACHE && !s->fc_stats_pending) {
+            CU(cudaMemcpyAsync(s->fc_stats_host, s->fc_stats, 2 * sizeof(unsigned long long), cudaMemcpyDeviceToHost,
+                               s->stream));
+            CU(cudaEventRecord(s->fc_stats_ev, s->stream));
+            s->fc_stats_pending = true;
         }
         s->launches++;
         done = nvec * 4;
@@ -445,7 +513,7 @@ static int scan_locked(dhsa_sketch *s, const uint32_t *cand, const uint32_t *opp
     if (done < n) {
         const uint64_t rest = n - done;
         const int grid = grid_for(s, rest, 256, 8);
-        if (s->scan_mode == 0)
+        if (s->scan_mode == DHSA_SCAN_RED_ONLY)
             k_scan_generic<0><<<grid, 256, 0, s->stream>>>(cand + done, opp + done, rest, words, s->dp);
         else
             k_scan_generic<1><<<grid, 256, 0, s->stream>>>(cand + done, opp + done, rest, words, s->dp);
@@ -619,10 +687,9 @@ static int launch_estimate(dhsa_sketch *s, double theta)
     if (int rc = ensure_readout(s)) return rc;
     if (int rc = launch_zero_counts(s)) return rc;
     const double zmin = (double)s->params.g * exp(-theta / (double)s->params.g);  // dhla.py:45-47
-    k_hot_sets<<<s->params.r, 1024, 0, s->stream>>>(s->zc, zmin, s->params.k, s->lists, s->bitmaps, s->bitmap_words,
-                                                   s->ctl);
-    k_plan<<<1, 32, 0, s->stream>>>(s->ctl, s->params.r, s->params.k, s->params.g);
-    s->launches += 2;
+    k_hot_sets<<<s->params.r, 1024, 0, s->stream>>>(s->zc, zmin, s->params.r, s->params.k, s->params.g, s->lists,
+                                                   s->bitmaps, s->bitmap_words, s->ctl);
+    s->launches += 1;
     CU(cudaGetLastError());
     return DHSA_OK;
 }
@@ -641,10 +708,9 @@ static int launch_restore_stages(dhsa_sketch *s, uint64_t max_candidates)
                                                   s->sub[cur], s->cl0[cur], s->sub[cur ^ 1], s->cl0[cur ^ 1], s->ctl);
         cur ^= 1;
     }
-    k_capacity_check<<<1, 32, 0, s->stream>>>(n_stages, max_candidates, s->ctl);
     k_verify_keys<<<grid, 256, 0, s->stream>>>(n_stages, s->dp, max_candidates, s->sub[cur], s->cl0[cur], s->keys,
                                                s->ctl);
-    s->launches += (uint64_t)n_stages + 2;
+    s->launches += (uint64_t)n_stages + 1;
     CU(cudaGetLastError());
     return DHSA_OK;
 }

@@ -44,6 +44,8 @@ struct Control {
     int flow_saturated;
     int any_empty;  // some hot set is empty -> no candidates (dhla.py:208-209)
     int sorted;     // reports/candidates were sorted on the device by the single-CTA sorter
+    unsigned int blocks_done;  // k_hot_sets: CTAs finished (the last one computes the scalars)
+    unsigned int pad_;
     double flow_count, psi, denom;
 };
 
@@ -125,6 +127,14 @@ __device__ __forceinline__ uint32_t ld_sketch(const uint32_t *ptr)
 __device__ __forceinline__ void ld_fc_set(const unsigned long long *set, unsigned long long (&e)[4])
 {
     asm volatile("ld.global.cg.v4.u64 {%0,%1,%2,%3}, [%4];"
+                 : "=l"(e[0]), "=l"(e[1]), "=l"(e[2]), "=l"(e[3])
+                 : "l"(set)
+                 : "memory");
+}
+
+__device__ __forceinline__ void ld_fc_set_evict_last(const unsigned long long *set, unsigned long long (&e)[4])
+{
+    asm volatile("ld.global.L1::no_allocate.L2::evict_last.v4.b64 {%0,%1,%2,%3}, [%4];"
                  : "=l"(e[0]), "=l"(e[1]), "=l"(e[2]), "=l"(e[3])
                  : "l"(set)
                  : "memory");
@@ -278,7 +288,6 @@ __global__ void __launch_bounds__(256) k_scan_vec4(const uint4 *__restrict__ can
 //              per 32 misses, not per packet slot.
 //   pipeline   the next trip's packets are requested before this trip's table
 //              sets are consumed.
-#define DHSA_FC_QCAP 160  // < 32 left over + up to 128 pushed per trip
 
 struct FcMiss {
     uint32_t cand, opp, slot;  // slot = set * 4 + way to fill
@@ -304,58 +313,79 @@ __device__ __forceinline__ void fc_drain32(uint32_t *__restrict__ words, const D
     if (act) st_fc_way(p.fcache + m.slot, ~(((unsigned long long)m.cand << 32) | (unsigned long long)m.opp));
 }
 
-template <int R>
-__global__ void __launch_bounds__(256, 3) k_scan_flowcache(const uint4 *__restrict__ cand4,
-                                                           const uint4 *__restrict__ opp4, uint64_t nvec,
-                                                           uint32_t *__restrict__ words, DevParams p)
+template <int R, int NV, int MINB, bool EVL>
+__global__ void __launch_bounds__(256, MINB) k_scan_flowcache(const uint4 *__restrict__ cand4,
+                                                              const uint4 *__restrict__ opp4, uint64_t nvec,
+                                                              uint32_t *__restrict__ words, DevParams p)
 {
-    __shared__ FcMiss queue_s[8][DHSA_FC_QCAP];
+    constexpr int NP = 4 * NV;  // packets per lane per trip
+    __shared__ FcMiss queue_s[8][32 + 32 * NP];
     const uint32_t lane = threadIdx.x & 31u;
     FcMiss *q = queue_s[threadIdx.x >> 5];
     uint32_t qn = 0;  // warp-uniform queue length
     const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
     const uint64_t warp0 = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const uint64_t step = nwarps * 32 * NV;
     const int wshift = p.log2g - 5;
     const uint64_t pol = policy_evict_first();
     const uint32_t lt_mask = (1u << lane) - 1u;
     unsigned long long fc_hits = 0, fc_lookups = 0;
 
-    uint64_t base = warp0 * 32;
-    uint4 c_next = make_uint4(0, 0, 0, 0), o_next = make_uint4(0, 0, 0, 0);
-    if (base + lane < nvec) {
-        c_next = ld_stream_v4(cand4 + base + lane, pol);
-        o_next = ld_stream_v4(opp4 + base + lane, pol);
+    uint64_t base = warp0 * 32 * NV;
+    uint4 c_next[NV], o_next[NV];
+#pragma unroll
+    for (int u = 0; u < NV; u++) {
+        c_next[u] = make_uint4(0, 0, 0, 0), o_next[u] = make_uint4(0, 0, 0, 0);
+        const uint64_t v = base + (uint64_t)u * 32 + lane;
+        if (v < nvec) {
+            c_next[u] = ld_stream_v4(cand4 + v, pol);
+            o_next[u] = ld_stream_v4(opp4 + v, pol);
+        }
     }
-    for (; base < nvec; base += nwarps * 32) {
-        const bool valid = base + lane < nvec;
-        const uint32_t cs[4] = {c_next.x, c_next.y, c_next.z, c_next.w};
-        const uint32_t os[4] = {o_next.x, o_next.y, o_next.z, o_next.w};
-        {   // request the next trip's packets now; they land while the table sets are in flight
-            const uint64_t vn = base + nwarps * 32 + lane;
+    for (; base < nvec; base += step) {
+        uint32_t cs[NP], os[NP];
+        bool valid[NV];
+#pragma unroll
+        for (int u = 0; u < NV; u++) {
+            valid[u] = base + (uint64_t)u * 32 + lane < nvec;
+            cs[4 * u + 0] = c_next[u].x, cs[4 * u + 1] = c_next[u].y, cs[4 * u + 2] = c_next[u].z, cs[4 * u + 3] = c_next[u].w;
+            os[4 * u + 0] = o_next[u].x, os[4 * u + 1] = o_next[u].y, os[4 * u + 2] = o_next[u].z, os[4 * u + 3] = o_next[u].w;
+        }
+        // request the next trip's packets now; they land while the table sets are in flight
+#pragma unroll
+        for (int u = 0; u < NV; u++) {
+            const uint64_t vn = base + step + (uint64_t)u * 32 + lane;
             if (vn < nvec) {
-                c_next = ld_stream_v4(cand4 + vn, pol);
-                o_next = ld_stream_v4(opp4 + vn, pol);
+                c_next[u] = ld_stream_v4(cand4 + vn, pol);
+                o_next[u] = ld_stream_v4(opp4 + vn, pol);
             }
         }
-        unsigned long long e[4][4];
-        uint32_t set_idx[4], way_hint[4];
+        unsigned long long e[NP][4];
+        uint32_t set_idx[NP], way_hint[NP];
 #pragma unroll
-        for (int j = 0; j < 4; j++) {
+        for (int j = 0; j < NP; j++) {
             const uint64_t hh = mix64(p.state_h1 ^ (uint64_t)os[j]);
             const uint64_t hd = mix64(p.state_dh0 ^ (uint64_t)cs[j]);
-            // set index from the high halves of both hashes (their low bits feed h and d0)
-            // (multiply-shift range reduction: any set count, not only powers of two)
+            // set index from the high halves of both hashes (their low bits feed h and d0);
+            // multiply-shift range reduction, so any set count works, not only powers of two
             set_idx[j] = __umulhi((uint32_t)(hh >> 32) + (uint32_t)(hd >> 32) * 0x9E3779B1u, p.fc_sets);
             way_hint[j] = (uint32_t)(hd >> 30) & 3u;
-            if (valid) ld_fc_set(p.fcache + ((size_t)set_idx[j] << 2), e[j]);
+            if (valid[j >> 2]) {
+                if (EVL)
+                    ld_fc_set_evict_last(p.fcache + ((size_t)set_idx[j] << 2), e[j]);
+                else
+                    ld_fc_set(p.fcache + ((size_t)set_idx[j] << 2), e[j]);
+            }
         }
 #pragma unroll
-        for (int j = 0; j < 4; j++) {
+        for (int j = 0; j < NP; j++) {
+            const bool ok = valid[j >> 2];
             const unsigned long long inv_key = ~(((unsigned long long)cs[j] << 32) | (unsigned long long)os[j]);
-            const bool hit = valid && inv_key != 0ull &&
+            const bool hit = ok && inv_key != 0ull &&
                              (e[j][0] == inv_key || e[j][1] == inv_key || e[j][2] == inv_key || e[j][3] == inv_key);
-            const bool miss = valid && !hit;
+            const bool miss = ok && !hit;
             fc_hits += hit;
+            fc_lookups += ok;
             const unsigned bal = __ballot_sync(0xFFFFFFFFu, miss);
             if (bal == 0) continue;
             if (miss) {
@@ -370,7 +400,6 @@ __global__ void __launch_bounds__(256, 3) k_scan_flowcache(const uint4 *__restri
             }
             qn += __popc(bal);
         }
-        fc_lookups += valid ? 4 : 0;
         __syncwarp();
         while (qn >= 32) {  // dense drains: the newest 32 entries, one per lane
             qn -= 32;
@@ -388,7 +417,6 @@ __global__ void __launch_bounds__(256, 3) k_scan_flowcache(const uint4 *__restri
         atomicAdd(p.fc_stats + 1, fc_hits);
     }
 }
-
 
 // General path: any r <= 64, any g >= 8 (sub-word cells included), 64-bit bit
 // addressing, unaligned input pointers.  One packet per lane per trip.
@@ -454,78 +482,14 @@ __global__ void __launch_bounds__(256) k_zero_counts_small(const uint8_t *__rest
     }
 }
 
-// Dhla.hot_sets (pkg/src/dhsa/dhla.py:111-119): HE(i) = { j : zc[i][j] < zmin },
-// ascending; plus the 2^k-bit hot bitmap of each array and ZR(i) = sum_j zc[i][j]
-// (dhla.py:126).  One 1024-thread CTA per array walks its cells in order and
-// compacts by ballot + scan, so the lists come out already sorted.
-__global__ void __launch_bounds__(1024) k_hot_sets(const int32_t *__restrict__ zc, double zmin, int k,
-                                                   uint32_t *__restrict__ lists,
-                                                   uint32_t *__restrict__ bitmaps,
-                                                   uint64_t bitmap_words_per_array, Control *ctl)
-{
-    __shared__ uint32_t warp_count[32];
-    __shared__ uint32_t warp_offset[32];
-    __shared__ unsigned long long warp_sum[32];
-    __shared__ unsigned long long base_s;
-    __shared__ uint32_t chunk_total_s;
-    const int arr = blockIdx.x;
-    const uint64_t m = 1ull << k;
-    const uint32_t lane = threadIdx.x & 31u, wid = threadIdx.x >> 5;
-    const int32_t *row = zc + (uint64_t)arr * m;
-    uint32_t *list = lists + (uint64_t)arr * m;
-    uint32_t *bmp = bitmaps + (uint64_t)arr * bitmap_words_per_array;
-    unsigned long long total = 0;
-    if (threadIdx.x == 0) base_s = 0;
-    __syncthreads();
-    for (uint64_t c0 = 0; c0 < m; c0 += 1024) {
-        const uint64_t j = c0 + threadIdx.x;
-        const bool in = j < m;
-        const int32_t z = in ? row[j] : 0;
-        const bool hot = in && ((double)z < zmin);
-        const unsigned bal = __ballot_sync(0xFFFFFFFFu, hot);
-        if (lane == 0) {
-            warp_count[wid] = __popc(bal);
-            if (c0 + wid * 32 < m) bmp[(c0 >> 5) + wid] = bal;
-        }
-        unsigned long long zs = (unsigned long long)z;
-        for (int d = 16; d > 0; d >>= 1) zs += __shfl_xor_sync(0xFFFFFFFFu, zs, d);
-        if (lane == 0) warp_sum[wid] = zs;
-        __syncthreads();
-        if (wid == 0) {
-            uint32_t cnt = warp_count[lane], inc = cnt;
-            for (int d = 1; d < 32; d <<= 1) {
-                uint32_t t = __shfl_up_sync(0xFFFFFFFFu, inc, d);
-                if (lane >= (uint32_t)d) inc += t;
-            }
-            warp_offset[lane] = inc - cnt;
-            unsigned long long ws = warp_sum[lane];
-            for (int d = 16; d > 0; d >>= 1) ws += __shfl_xor_sync(0xFFFFFFFFu, ws, d);
-            if (lane == 31) chunk_total_s = inc;
-            if (lane == 0) total += ws;
-        }
-        __syncthreads();
-        const unsigned long long base = base_s;
-        const uint32_t chunk_total = chunk_total_s;
-        if (hot) list[base + warp_offset[wid] + __popc(bal & ((1u << lane) - 1u))] = (uint32_t)j;
-        __syncthreads();
-        if (threadIdx.x == 0) base_s = base + chunk_total;
-        __syncthreads();
-    }
-    if (threadIdx.x == 0) {
-        ctl->hot_counts[arr] = base_s;
-        ctl->zero_totals[arr] = (long long)total;
-    }
-}
-
-// Scalars of the read-out, one thread:
+// Scalars of the read-out:
 //   flow count  = mean_i( -C ln(ZR(i)/C) ), ZR == 0 -> evaluate at 1, flag saturated
 //                 (pkg/src/dhsa/estimator.py:26-34, dhla.py:121-128)
 //   psi         = 1 - exp(-flow / C)                          (dhla.py:130-134)
 //   denom       = g (1 - psi^r)                               (dhla.py:184)
 // and the "any hot set empty -> no candidates" rule (dhla.py:208-209).
-__global__ void k_plan(Control *ctl, int r, int k, int g)
+__device__ __forceinline__ void plan_readout(Control *ctl, int r, int k, int g)
 {
-    if (threadIdx.x != 0 || blockIdx.x != 0) return;
     const double cap = (double)g * (double)(1ull << k);
     double acc = 0.0;
     int sat = 0, empty = 0;
@@ -551,6 +515,103 @@ __global__ void k_plan(Control *ctl, int r, int k, int g)
     ctl->fail_stage = 0;
     ctl->fail_count = 0;
     ctl->sorted = 0;
+}
+
+// Dhla.hot_sets (pkg/src/dhsa/dhla.py:111-119): HE(i) = { j : zc[i][j] < zmin },
+// ascending; plus the 2^k-bit hot bitmap of each array and ZR(i) = sum_j zc[i][j]
+// (dhla.py:126).  One 1024-thread CTA per array; each thread owns 16 consecutive
+// cells (64 contiguous bytes of zero counts), so the default 2^14-cell array is
+// one pass: thread-local 16-bit hot mask, one block scan, in-order list writes.
+// The last CTA to finish computes the scalars above (no extra launch).
+#define DHSA_HOT_CPT 16
+__global__ void __launch_bounds__(1024) k_hot_sets(const int32_t *__restrict__ zc, double zmin, int r, int k, int g,
+                                                   uint32_t *__restrict__ lists,
+                                                   uint32_t *__restrict__ bitmaps,
+                                                   uint64_t bitmap_words_per_array, Control *ctl)
+{
+    __shared__ uint32_t warp_count[32];
+    __shared__ unsigned long long warp_sum[32];
+    __shared__ uint32_t chunk_total_s;
+    __shared__ unsigned long long chunk_sum_s;
+    __shared__ bool is_last_s;
+    const int arr = blockIdx.x;
+    const uint64_t m = 1ull << k;
+    const uint32_t lane = threadIdx.x & 31u, wid = threadIdx.x >> 5;
+    const int32_t *row = zc + (uint64_t)arr * m;
+    uint32_t *list = lists + (uint64_t)arr * m;
+    uint32_t *bmp = bitmaps + (uint64_t)arr * bitmap_words_per_array;
+    unsigned long long base = 0, total = 0;
+    for (uint64_t c0 = 0; c0 < m; c0 += 1024ull * DHSA_HOT_CPT) {
+        const uint64_t j0 = c0 + (uint64_t)threadIdx.x * DHSA_HOT_CPT;
+        uint32_t hot = 0;
+        unsigned long long zs = 0;
+        if (j0 + DHSA_HOT_CPT <= m) {
+            const int4 *v = reinterpret_cast<const int4 *>(row + j0);
+#pragma unroll
+            for (int q = 0; q < DHSA_HOT_CPT / 4; q++) {
+                const int4 z = v[q];
+                hot |= (uint32_t)((double)z.x < zmin) << (4 * q + 0);
+                hot |= (uint32_t)((double)z.y < zmin) << (4 * q + 1);
+                hot |= (uint32_t)((double)z.z < zmin) << (4 * q + 2);
+                hot |= (uint32_t)((double)z.w < zmin) << (4 * q + 3);
+                zs += (unsigned long long)z.x + (unsigned long long)z.y + (unsigned long long)z.z +
+                      (unsigned long long)z.w;
+            }
+        } else {
+            for (int q = 0; q < DHSA_HOT_CPT; q++)
+                if (j0 + q < m) {
+                    const int32_t z = row[j0 + q];
+                    hot |= (uint32_t)((double)z < zmin) << q;
+                    zs += (unsigned long long)z;
+                }
+        }
+        // bitmap: two threads share a 32-bit word
+        const uint32_t other = __shfl_xor_sync(0xFFFFFFFFu, hot, 1);
+        if ((threadIdx.x & 1u) == 0 && j0 < m) bmp[j0 >> 5] = hot | (other << 16);
+        // ordered compaction: exclusive scan of the per-thread counts
+        const uint32_t cnt = __popc(hot);
+        uint32_t inc = cnt;
+        for (int d = 1; d < 32; d <<= 1) {
+            const uint32_t t = __shfl_up_sync(0xFFFFFFFFu, inc, d);
+            if (lane >= (uint32_t)d) inc += t;
+        }
+        for (int d = 16; d > 0; d >>= 1) zs += __shfl_xor_sync(0xFFFFFFFFu, zs, d);
+        if (lane == 31) warp_count[wid] = inc;
+        if (lane == 0) warp_sum[wid] = zs;
+        __syncthreads();
+        if (wid == 0) {
+            const uint32_t wc = warp_count[lane];
+            uint32_t winc = wc;
+            for (int d = 1; d < 32; d <<= 1) {
+                const uint32_t t = __shfl_up_sync(0xFFFFFFFFu, winc, d);
+                if (lane >= (uint32_t)d) winc += t;
+            }
+            unsigned long long ws = warp_sum[lane];
+            for (int d = 16; d > 0; d >>= 1) ws += __shfl_xor_sync(0xFFFFFFFFu, ws, d);
+            __syncwarp();
+            warp_count[lane] = winc - wc;  // exclusive offset of each warp
+            if (lane == 31) chunk_total_s = winc;
+            if (lane == 0) chunk_sum_s = ws;
+        }
+        __syncthreads();
+        uint32_t pos = (uint32_t)base + warp_count[wid] + (inc - cnt);
+        for (uint32_t hbits = hot; hbits; hbits &= hbits - 1) list[pos++] = (uint32_t)(j0 + (__ffs(hbits) - 1));
+        base += chunk_total_s;
+        total += chunk_sum_s;
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        ctl->hot_counts[arr] = base;
+        ctl->zero_totals[arr] = (long long)total;
+        __threadfence();
+        is_last_s = atomicAdd(&ctl->blocks_done, 1u) == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (is_last_s && threadIdx.x == 0) {
+        __threadfence();
+        plan_readout(ctl, r, k, g);
+        ctl->blocks_done = 0;
+    }
 }
 
 // ------------------------------------------------------------ K3: restore --
@@ -686,6 +747,16 @@ __global__ void __launch_bounds__(256) k_verify_keys(int n_stages, DevParams p,
                                                      const uint32_t *__restrict__ in_cl0,
                                                      uint64_t *__restrict__ keys, Control *ctl)
 {
+    if (blockIdx.x == 0 && threadIdx.x == 0 && !ctl->any_empty) {
+        // record the first overflowing stage: the numbers of the CapacityError text
+        // (stage 1, then i - 1 for array i; dhla.py:269-273, 294-298)
+        for (int st = 0; st < n_stages; st++)
+            if (ctl->stage_counts[st] > max_candidates) {
+                ctl->fail_stage = st + 1;
+                ctl->fail_count = ctl->stage_counts[st];
+                break;
+            }
+    }
     if (stage_blocked(ctl, n_stages, max_candidates)) return;
     const uint64_t np = ctl->stage_counts[n_stages - 1];
     const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
@@ -696,18 +767,6 @@ __global__ void __launch_bounds__(256) k_verify_keys(int n_stages, DevParams p,
         const unsigned long long pos = atomicAdd(&ctl->n_candidates, 1ull);
         keys[pos] = sub;  // pos < np <= max_candidates
     }
-}
-
-// Records the first overflowing stage (the numbers of the CapacityError text).
-__global__ void k_capacity_check(int n_stages, unsigned long long max_candidates, Control *ctl)
-{
-    if (threadIdx.x != 0 || blockIdx.x != 0 || ctl->any_empty) return;
-    for (int s = 0; s < n_stages; s++)
-        if (ctl->stage_counts[s] > max_candidates) {
-            ctl->fail_stage = s + 1;  // stage 1, then i - 1 for array i (dhla.py:271,296)
-            ctl->fail_count = ctl->stage_counts[s];
-            return;
-        }
 }
 
 // ------------------------------- K4: re-estimate + threshold filter + order --

@@ -31,7 +31,7 @@ from .errors import ConfigError
 
 DEFAULT_MAX_CANDIDATES = 1 << 20  # pkg/src/dhsa/dhla.py:34
 
-SCAN_MODES = {"red": 0, "test": 1, "test_agg": 2, "flow_cache": 3}
+SCAN_MODES = {"red": 0, "test": 1, "test_agg": 2, "flow_cache": 3, "auto": 4}
 
 _REPORT_DTYPE = np.dtype([("host", "<u8"), ("estimate", "<f8"), ("saturated", "<i4"), ("sz", "<i4")])
 assert _REPORT_DTYPE.itemsize == C.sizeof(_cabi.Report)

@@ -54,7 +54,7 @@ def gpu_for_case(case, mode="test_agg"):
 # ------------------------------------------------------------------------ scan --
 
 
-MODES = ["red", "test", "test_agg", "flow_cache"]
+MODES = ["red", "test", "test_agg", "flow_cache", "auto"]
 
 
 @pytest.mark.parametrize("mode", MODES)
@@ -203,6 +203,23 @@ def test_flow_cache_is_exact_across_batches_resets_and_uploads(n_sets):
     sk.update_batch(base_c[pick], base_o[pick])
     fresh.update_batch(oc, oo)
     assert np.array_equal(sk.bits, fresh.bits)
+
+
+def test_auto_mode_falls_back_when_flows_do_not_repeat():
+    """All-distinct pairs: the hit rate stays ~0, auto switches kernels mid-window; bits stay exact."""
+    cand, opp = O.distinct_pairs(12_000_000, 90)
+    ora = O.OracleSketch(r=5, g=1024, k=16, alpha=6)
+    ora.update_batch(cand, opp, threads=8)
+    sk = P.Dhla(P.DhgParams(r=5, g=1024, k=16, alpha=6))
+    for s in range(0, len(cand), 2_000_000):   # several launches so the policy sees the statistics
+        sk.update_batch(cand[s:s + 2_000_000], opp[s:s + 2_000_000])
+        sk.seal()
+    assert sha(sk.bits) == sha(ora.bits)
+    lookups, hits = sk.flow_cache_stats()
+    assert 0 < lookups < len(cand) and hits * 10 < lookups   # later batches bypassed the cache
+    sk.reset()                                               # next window starts behind the cache again
+    sk.update_batch(cand[:1_000_000], opp[:1_000_000])
+    assert sk.flow_cache_stats()[0] == 1_000_000
 
 
 def test_reset_and_load_bits_round_trip():
