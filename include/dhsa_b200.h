@@ -166,6 +166,34 @@ int dhsa_shared_zero_counts(dhsa_sketch_t *s, const uint64_t *hosts_host, uint64
 int dhsa_restore(dhsa_sketch_t *s, double theta, uint64_t max_candidates,
                  dhsa_report_t *reports_host, uint64_t reports_cap, dhsa_restore_info_t *info);
 
+/* ---- record streams: the window engine's per-record work, fused into the scan --------
+ * Records are the reference's 12-byte IPPR trace records (pkg/src/dhsa/ingest.py:20): u32
+ * timestamp little-endian, then src and dst IPv4 as u32 big-endian.
+ *
+ * dhsa_plan_windows: DetectionEngine._run's windowing (pkg/src/dhsa/engine.py:140-149).  A record
+ * arrives during the running maximum of ts // window_seconds over the stream so far (seeded with
+ * open_window, -1 = none), so the stream splits into contiguous segments, one per window, at the
+ * records where that maximum rises; out_host receives those (position, window id) pairs in
+ * position order.  DHSA_EDATA if there are more than cap.
+ *
+ * dhsa_update_records_device: scan records [rec_lo, rec_hi) of a device buffer holding
+ * n_in_buffer records into window `window_id`: records with ts // window_seconds == window_id
+ * are fed under the direction policy (split_pairs, pkg/src/dhsa/engine.py:179-194: 0 "src",
+ * 1 "dst", 2 "both"), the others are late and only counted (engine.py:148-156).
+ * dhsa_record_tally: records fed / dropped since the last dhsa_reset (WindowResult.pairs counts
+ * fed pairs, i.e. twice the records under "both"; engine.py:49-54,87). */
+typedef struct {
+    uint64_t position;
+    int64_t window_id;
+} dhsa_boundary_t;
+int dhsa_plan_windows(dhsa_sketch_t *s, const void *records_dev, uint64_t n_records,
+                      uint32_t window_seconds, int64_t open_window, dhsa_boundary_t *out_host,
+                      uint32_t cap, uint32_t *n_out);
+int dhsa_update_records_device(dhsa_sketch_t *s, const void *records_dev, uint64_t n_in_buffer,
+                               uint64_t rec_lo, uint64_t rec_hi, uint32_t window_seconds,
+                               uint32_t window_id, int direction);
+int dhsa_record_tally(dhsa_sketch_t *s, uint64_t *records_fed, uint64_t *records_dropped);
+
 /* ---- merge: dhsa.dhla.merge (pkg/src/dhsa/dhla.py:305-318) ------------------------ */
 
 /* dst |= src; both handles in this process (same or peer device).  Parameter

@@ -293,6 +293,81 @@ class OracleSketch:
 
 
 # ---------------------------------------------------------------------------
+# Window engine restatement (numpy; small cases).
+# ---------------------------------------------------------------------------
+
+TRACE_DTYPE = np.dtype([("ts", "<u4"), ("src", ">u4"), ("dst", ">u4")])  # pkg/src/dhsa/ingest.py:20
+
+
+def run_windows(records: np.ndarray, window_seconds: int, theta, direction: str = "src",
+                max_candidates: int = 1 << 20, **sketch_kw):
+    """Tumbling-window detection over a record stream, as the reference's engine defines it
+    (pkg/src/dhsa/engine.py:132-176; chunking there does not change the result):
+
+      window of a record   ts // window_seconds                              engine.py:140
+      arrival window       running maximum of the window ids so far          engine.py:143-145
+      late record          window < arrival window: dropped, counted in the  engine.py:148,154
+                           window that was open when it arrived
+      direction policy     src: (src, dst); dst: (dst, src); both: both      engine.py:179-194
+      a window is sealed and restored when a later one opens, or at the end  engine.py:150-152,159
+
+    Returns [(window_id, pairs, dropped, [OracleReport])]."""
+    if len(records) == 0:
+        return []
+    wins = records["ts"].astype(np.int64) // window_seconds
+    arrival = np.maximum.accumulate(wins)
+    src = records["src"].astype(np.uint32)
+    dst = records["dst"].astype(np.uint32)
+    out = []
+    for wid in np.unique(arrival):
+        span = arrival == wid
+        on_time = span & (wins == arrival)
+        s, d = src[on_time], dst[on_time]
+        if direction == "src":
+            cand, opp = s, d
+        elif direction == "dst":
+            cand, opp = d, s
+        elif direction == "both":
+            cand, opp = np.concatenate([s, d]), np.concatenate([d, s])
+        else:
+            raise ValueError(direction)
+        sk = OracleSketch(**sketch_kw)
+        sk.update_batch(cand, opp)
+        out.append((int(wid), int(len(cand)), int(span.sum() - on_time.sum()),
+                    sk.restore_superpoints(theta, max_candidates)))
+    return out
+
+
+def engine_trace(seed: int, n_noise: int = 90_000, window_seconds: int = 300):
+    """A deterministic multi-window trace with late records, built from mix64 only (no
+    library RNG): three and a half windows of background pairs in time order, three hosts
+    planted in windows 1, 1 and 2 with 2048..2600 destinations, 3% of records re-stamped
+    up to two windows into the past (late), and one early record far in the future that
+    opens window 5 before the rest of the trace ends."""
+    cand, opp = distinct_pairs(n_noise, seed)
+    ts = (np.arange(n_noise, dtype=np.uint64) * np.uint64(int(3.5 * window_seconds))) // np.uint64(n_noise)
+    parts_c, parts_o, parts_t = [cand], [opp], [ts.astype(np.uint32)]
+    for n, (host, fan, win) in enumerate(((0x0A0B0C0D, 2048, 1), (0xC0A80001, 2600, 1), (0x08080404, 2300, 2))):
+        c2 = np.full(fan, host, dtype=np.uint32)
+        o2 = (mix64_many(np.arange(fan, dtype=np.uint64) ^ np.uint64((seed + n + 1) << 40)) &
+              np.uint64(0xFFFFFFFF)).astype(np.uint32)
+        t2 = (np.uint64(win * window_seconds) +
+              mix64_many(np.arange(fan, dtype=np.uint64) ^ np.uint64(77 + n)) % np.uint64(window_seconds))
+        parts_c.append(c2), parts_o.append(o2), parts_t.append(t2.astype(np.uint32))
+    cand, opp, ts = np.concatenate(parts_c), np.concatenate(parts_o), np.concatenate(parts_t)
+    order = np.argsort(ts, kind="stable")
+    cand, opp, ts = cand[order], opp[order], ts[order].astype(np.int64)
+    pick = mix64_many(np.arange(len(ts), dtype=np.uint64) ^ np.uint64(seed * 1315423911))
+    late = (pick % np.uint64(100)) < np.uint64(3)
+    back = ((pick >> np.uint64(20)) % np.uint64(2 * window_seconds)).astype(np.int64)
+    ts = np.where(late, np.maximum(ts - back, 0), ts)
+    ts[len(ts) * 3 // 4] = 5 * window_seconds + 7   # a jump ahead: everything after it in windows < 5 is late
+    rec = np.empty(len(ts), dtype=TRACE_DTYPE)
+    rec["ts"], rec["src"], rec["dst"] = ts.astype(np.uint32), cand, opp
+    return rec
+
+
+# ---------------------------------------------------------------------------
 # The reference's own compiled loops (oracle/_ref), when they were built.
 # ---------------------------------------------------------------------------
 

@@ -16,6 +16,9 @@ GPU every data-path call raises.
 from .dhg import DhgParams
 from .dhla import (DEFAULT_MAX_CANDIDATES, Dhla, Estimate, SuperPointReport, hot_threshold,
                    merge)
+from .engine import (DetectionEngine, TRACE_DTYPE, WindowConfig, WindowResult, WindowSession,
+                     split_pairs)
+from .snapshot import read_snapshot, write_snapshot
 from .errors import (CapacityError, ConfigError, CudaError, DataError, DhsaError,
                      SealedWindowError)
 
@@ -23,6 +26,7 @@ __version__ = "0.1.0"
 
 __all__ = [
     "DhgParams", "Dhla", "SuperPointReport", "Estimate", "merge", "hot_threshold",
-    "DEFAULT_MAX_CANDIDATES", "DhsaError", "ConfigError", "DataError", "CapacityError",
+    "DEFAULT_MAX_CANDIDATES", "DetectionEngine", "WindowConfig", "WindowResult", "WindowSession",
+    "split_pairs", "TRACE_DTYPE", "read_snapshot", "write_snapshot", "DhsaError", "ConfigError", "DataError", "CapacityError",
     "SealedWindowError", "CudaError",
 ]

@@ -20,6 +20,7 @@
 
 using namespace dhsa;
 
+
 // ------------------------------------------------------------------ errors --
 
 static thread_local char g_err[512];
@@ -95,6 +96,15 @@ struct dhsa_sketch {
     uint64_t *hosts_in;     // shared_zero_counts input
     int32_t *sz_out;
     uint64_t hosts_in_cap;
+
+    // record streams
+    unsigned long long *tally;      // device: records fed, records dropped
+    uint32_t *plan_block_max;
+    long long *plan_carry;
+    PlanBoundary *plan_out;
+    unsigned int *plan_count;
+    uint64_t plan_blocks_cap;
+    uint32_t plan_out_cap;
 
     // host-input staging
     uint32_t *stage_cand[kStageBufs], *stage_opp[kStageBufs];
@@ -210,6 +220,8 @@ extern "C" int dhsa_create(const dhsa_params_t *params, int device, dhsa_sketch_
     CU(cudaStreamCreateWithFlags(&s->copy_stream, cudaStreamNonBlocking));
     s->stream = s->own_stream;
     CU(cudaMalloc(&s->ctl, sizeof(Control)));
+    CU(cudaMalloc(&s->tally, 2 * sizeof(unsigned long long)));
+    CU(cudaMemsetAsync(s->tally, 0, 2 * sizeof(unsigned long long), s->stream));
     CU(cudaMallocHost(&s->ctl_host, sizeof(Control)));
     CU(cudaMemsetAsync(s->bits, 0, s->alloc_bytes, s->stream));
     CU(cudaMemsetAsync(s->ctl, 0, sizeof(Control), s->stream));
@@ -236,6 +248,11 @@ extern "C" int dhsa_destroy(dhsa_sketch_t *s)
         }
     }
     cudaFree(s->bits);
+    cudaFree(s->tally);
+    cudaFree(s->plan_block_max);
+    cudaFree(s->plan_carry);
+    cudaFree(s->plan_out);
+    cudaFree(s->plan_count);
     cudaFree(s->fcache);
     cudaFree(s->fc_stats);
     if (s->fc_stats_host) {
@@ -315,6 +332,7 @@ extern "C" int dhsa_reset(dhsa_sketch_t *s)
     std::lock_guard<std::mutex> lk(s->mu);
     if (int rc = use_device(s)) return rc;
     CU(cudaMemsetAsync(s->bits, 0, s->alloc_bytes, s->stream));
+    CU(cudaMemsetAsync(s->tally, 0, 2 * sizeof(unsigned long long), s->stream));
     return clear_flow_cache_locked(s);
 }
 
@@ -389,126 +407,105 @@ extern "C" int dhsa_launch_count(const dhsa_sketch_t *s, uint64_t *n)
 
 // -------------------------------------------------------------------- scan --
 
-// Tuning variants of the flow-cache kernel (experiments: DHSA_FC_VARIANT=0..5).
-static int fc_variant()
-{
-    static int v = -1;
-    if (v < 0) {
-        const char *e = getenv("DHSA_FC_VARIANT");
-        v = e ? atoi(e) : 0;
-    }
-    return v;
-}
-
-template <int R>
-static void launch_flowcache(dhsa_sketch *s, int grid_unused, const uint4 *c4, const uint4 *o4, uint64_t nvec)
+template <int R, typename SRC>
+static void launch_scan_src(dhsa_sketch *s, int mode, const SRC &src)
 {
     uint32_t *w = reinterpret_cast<uint32_t *>(s->bits);
-    (void)grid_unused;
-#define FC_LAUNCH(NV_, MINB_, EVL_)                                                                          \
-    do {                                                                                                     \
-        static int occ = 0;                                                                                  \
-        if (!occ && (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_scan_flowcache<R, NV_, MINB_, EVL_>, \
-                                                                   256, 0) != cudaSuccess || occ < 1))       \
-            occ = MINB_;                                                                                     \
-        const int g = grid_for(s, (nvec + NV_ - 1) / NV_, 256, occ);                                         \
-        k_scan_flowcache<R, NV_, MINB_, EVL_><<<g, 256, 0, s->stream>>>(c4, o4, nvec, w, s->dp);             \
+    const uint64_t nvec = src.vectors();
+    // persistent grid: SMs x resident CTAs of the chosen kernel
+#define LAUNCH(KERNEL, FALLBACK_OCC)                                                                       \
+    do {                                                                                                   \
+        static int occ = 0;                                                                                \
+        if (!occ && (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, KERNEL, 256, 0) != cudaSuccess || occ < 1)) \
+            occ = FALLBACK_OCC;                                                                            \
+        KERNEL<<<grid_for(s, nvec, 256, occ), 256, 0, s->stream>>>(src, w, s->dp);                         \
     } while (0)
-    // measured on B200 (profiles/r01_flowcache_variants.txt): 4 packets per lane at 3 CTAs/SM wins;
-    // 8 packets per lane, 4 CTAs/SM (spills) and L2::evict_last table loads were all slower or equal
-    switch (fc_variant()) {
-    case 2: FC_LAUNCH(2, 2, false); break;
-    default: FC_LAUNCH(1, 3, false); break;
-    }
-#undef FC_LAUNCH
-}
-
-template <int R>
-static void launch_scan_vec(dhsa_sketch *s, int mode, int grid, const uint4 *c4, const uint4 *o4, uint64_t nvec)
-{
-    uint32_t *w = reinterpret_cast<uint32_t *>(s->bits);
     switch (mode) {
-    case 0: k_scan_vec4<R, 0><<<grid, 256, 0, s->stream>>>(c4, o4, nvec, w, s->dp); break;
-    case 1: k_scan_vec4<R, 1><<<grid, 256, 0, s->stream>>>(c4, o4, nvec, w, s->dp); break;
-    case 2: k_scan_vec4<R, 2><<<grid, 256, 0, s->stream>>>(c4, o4, nvec, w, s->dp); break;
-    default: launch_flowcache<R>(s, grid, c4, o4, nvec); break;
+    case DHSA_SCAN_RED_ONLY: LAUNCH((k_scan_vec4<R, 0, SRC>), 8); break;
+    case DHSA_SCAN_TEST_RED: LAUNCH((k_scan_vec4<R, 1, SRC>), 3); break;
+    case DHSA_SCAN_TEST_AGG_RED: LAUNCH((k_scan_vec4<R, 2, SRC>), 2); break;
+    // flow cache: 4 packets per lane at 3 CTAs/SM measured best on B200 (profiles/r01_flowcache_variants.txt);
+    // 8 packets per lane, 4 CTAs/SM (spills) and L2::evict_last table loads were slower or equal
+    default: LAUNCH((k_scan_flowcache<R, SRC>), 3); break;
+    }
+#undef LAUNCH
+    s->launches++;
+}
+
+template <typename SRC>
+static void launch_scan_any_r(dhsa_sketch *s, int mode, const SRC &src)
+{
+    switch (s->params.r) {
+    case 3: launch_scan_src<3>(s, mode, src); break;
+    case 4: launch_scan_src<4>(s, mode, src); break;
+    case 5: launch_scan_src<5>(s, mode, src); break;
+    default: launch_scan_src<6>(s, mode, src); break;
     }
 }
 
-template <int R, int MODE>
-static int scan_blocks_per_sm()
+// Which fast kernel this launch uses (lock held).  Auto: scan behind the flow cache, watch its
+// hit rate through an asynchronous snapshot (never a sync), and fall back to the 5-access kernel
+// for the rest of the window when flows do not repeat.  Break-even is a hit rate of about 1/3:
+// 1 + 11 (1 - h) requests per packet with the cache against 5 + 5 (1 - h) without.
+static int pick_scan_mode_locked(dhsa_sketch *s)
 {
-    static int cached = 0;
-    if (!cached) {
-        int nb = 0;
-        cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_scan_vec4<R, MODE == 3 ? 2 : MODE>, 256, 0);
-        if (e != cudaSuccess || nb < 1) nb = 2;
-        cached = nb;
+    int mode = s->scan_mode;
+    if (mode == DHSA_SCAN_AUTO) {
+        if (s->fc_stats_pending && cudaEventQuery(s->fc_stats_ev) == cudaSuccess) {
+            s->fc_stats_pending = false;
+            const unsigned long long lookups = s->fc_stats_host[0], hits = s->fc_stats_host[1];
+            if (lookups >= (1ull << 22) && hits * 10 < lookups * 3) s->auto_fell_back = true;
+        }
+        (void)cudaGetLastError();
+        mode = s->auto_fell_back ? DHSA_SCAN_TEST_AGG_RED : DHSA_SCAN_FLOW_CACHE;
     }
-    return cached;
+    return mode;
 }
 
-static int scan_occupancy(int r, int mode)
+static int before_fast_scan_locked(dhsa_sketch *s, int mode)
 {
-#define OCC(R_)                                                                                   \
-    (mode == 0 ? scan_blocks_per_sm<R_, 0>() : mode == 1 ? scan_blocks_per_sm<R_, 1>() : \
-     mode == 2 ? scan_blocks_per_sm<R_, 2>() : scan_blocks_per_sm<R_, 3>())
-    switch (r) {
-    case 3: return OCC(3);
-    case 4: return OCC(4);
-    case 5: return OCC(5);
-    case 6: return OCC(6);
-    default: return 8;
+    if (mode == DHSA_SCAN_FLOW_CACHE) {
+        if (int rc = ensure_flow_cache_locked(s)) return rc;
+        s->fc_dirty = true;
     }
-#undef OCC
+    return DHSA_OK;
+}
+
+static int after_fast_scan_locked(dhsa_sketch *s, int mode)
+{
+    if (s->scan_mode == DHSA_SCAN_AUTO && mode == DHSA_SCAN_FLOW_CACHE && !s->fc_stats_pending) {
+        CU(cudaMemcpyAsync(s->fc_stats_host, s->fc_stats, 2 * sizeof(unsigned long long), cudaMemcpyDeviceToHost,
+                           s->stream));
+        CU(cudaEventRecord(s->fc_stats_ev, s->stream));
+        s->fc_stats_pending = true;
+    }
+    return DHSA_OK;
+}
+
+// The vectorised kernels cover r in 3..6, cells of at least one word, sketches under 16 GiB.
+static bool fast_params(const dhsa_sketch *s)
+{
+    const dhsa_params_t &p = s->params;
+    return p.r >= 3 && p.r <= 6 && s->dp.log2g >= 5 && s->dp.nwords <= 0xFFFFFFFFull;
 }
 
 // Launches the scan of n device-resident packets on s->stream (lock held).
 static int scan_locked(dhsa_sketch *s, const uint32_t *cand, const uint32_t *opp, uint64_t n)
 {
     if (n == 0) return DHSA_OK;
-    const dhsa_params_t &p = s->params;
     uint32_t *words = reinterpret_cast<uint32_t *>(s->bits);
-    const bool fast = p.r >= 3 && p.r <= 6 && s->dp.log2g >= 5 && s->dp.nwords <= 0xFFFFFFFFull &&
-                      (((uintptr_t)cand | (uintptr_t)opp) & 15u) == 0;
+    const bool fast = fast_params(s) && (((uintptr_t)cand | (uintptr_t)opp) & 15u) == 0;
     uint64_t done = 0;
     if (fast && n >= 4) {
-        int mode = s->scan_mode;
-        if (mode == DHSA_SCAN_AUTO) {
-            // Auto: scan behind the flow cache, watch its hit rate through an asynchronous
-            // snapshot (never a sync), and fall back to the 5-access kernel for the rest of the
-            // window when flows do not repeat.  Break-even is a hit rate of about 1/3:
-            // 1 + 11 (1 - h) requests per packet with the cache against 5 + 5 (1 - h) without.
-            if (s->fc_stats_pending && cudaEventQuery(s->fc_stats_ev) == cudaSuccess) {
-                s->fc_stats_pending = false;
-                const unsigned long long lookups = s->fc_stats_host[0], hits = s->fc_stats_host[1];
-                if (lookups >= (1ull << 22) && hits * 10 < lookups * 3) s->auto_fell_back = true;
-            }
-            (void)cudaGetLastError();
-            mode = s->auto_fell_back ? DHSA_SCAN_TEST_AGG_RED : DHSA_SCAN_FLOW_CACHE;
-        }
-        if (mode == DHSA_SCAN_FLOW_CACHE) {
-            if (int rc = ensure_flow_cache_locked(s)) return rc;
-            s->fc_dirty = true;
-        }
-        const uint64_t nvec = n / 4;
-        const int occ = scan_occupancy(p.r, mode);
-        const int grid = grid_for(s, nvec, 256, occ);
-        const uint4 *c4 = reinterpret_cast<const uint4 *>(cand), *o4 = reinterpret_cast<const uint4 *>(opp);
-        switch (p.r) {
-        case 3: launch_scan_vec<3>(s, mode, grid, c4, o4, nvec); break;
-        case 4: launch_scan_vec<4>(s, mode, grid, c4, o4, nvec); break;
-        case 5: launch_scan_vec<5>(s, mode, grid, c4, o4, nvec); break;
-        default: launch_scan_vec<6>(s, mode, grid, c4, o4, nvec); break;
-        }
-        if (s->scan_mode == DHSA_SCAN_AUTO && mode == DHSA_SCAN_FLOW_CACHE && !s->fc_stats_pending) {
-            CU(cudaMemcpyAsync(s->fc_stats_host, s->fc_stats, 2 * sizeof(unsigned long long), cudaMemcpyDeviceToHost,
-                               s->stream));
-            CU(cudaEventRecord(s->fc_stats_ev, s->stream));
-            s->fc_stats_pending = true;
-        }
-        s->launches++;
-        done = nvec * 4;
+        const int mode = pick_scan_mode_locked(s);
+        if (int rc = before_fast_scan_locked(s, mode)) return rc;
+        SoaSource src;
+        src.cand4 = reinterpret_cast<const uint4 *>(cand);
+        src.opp4 = reinterpret_cast<const uint4 *>(opp);
+        src.nvec = n / 4;
+        launch_scan_any_r(s, mode, src);
+        if (int rc = after_fast_scan_locked(s, mode)) return rc;
+        done = src.nvec * 4;
     }
     if (done < n) {
         const uint64_t rest = n - done;
@@ -520,6 +517,152 @@ static int scan_locked(dhsa_sketch *s, const uint32_t *cand, const uint32_t *opp
         s->launches++;
     }
     CU(cudaGetLastError());
+    return DHSA_OK;
+}
+
+// One orientation of a record segment (lock held): whole quads inside the buffer through the
+// fast kernels, ragged ends (and non-fast parameters) through the one-record-per-lane kernel.
+static int scan_records_locked(dhsa_sketch *s, const uint8_t *records, uint64_t n_in_buffer, uint64_t rec_lo,
+                               uint64_t rec_hi, uint32_t window_seconds, uint32_t window_id, int cand_is_dst,
+                               int tally_late)
+{
+    uint32_t *words = reinterpret_cast<uint32_t *>(s->bits);
+    const uint32_t *rec_words = reinterpret_cast<const uint32_t *>(records);
+    uint64_t covered_hi = rec_lo;  // records [rec_lo, covered_hi) were handled by the fast kernel
+    if (fast_params(s) && ((uintptr_t)records & 15u) == 0) {
+        const uint64_t q_lo = rec_lo / 4, q_hi = (rec_hi + 3) / 4, q_buf = n_in_buffer / 4;  // whole quads only
+        const uint64_t q_end = q_hi < q_buf ? q_hi : q_buf;
+        if (q_end > q_lo) {
+            const int mode = pick_scan_mode_locked(s);
+            if (int rc = before_fast_scan_locked(s, mode)) return rc;
+            RecordSource src;
+            src.rec4 = reinterpret_cast<const uint4 *>(records) + 3 * q_lo;
+            src.nquads = q_end - q_lo;
+            src.first_rec = 4 * q_lo;
+            src.rec_lo = rec_lo;
+            src.rec_hi = rec_hi;
+            src.window_seconds = window_seconds;
+            src.window_id = window_id;
+            src.cand_is_dst = cand_is_dst;
+            src.tally = s->tally;
+            src.tally_late = tally_late;
+            launch_scan_any_r(s, mode, src);
+            if (int rc = after_fast_scan_locked(s, mode)) return rc;
+            covered_hi = 4 * q_end < rec_hi ? 4 * q_end : rec_hi;
+        }
+    }
+    if (covered_hi < rec_hi) {  // at most 3 trailing records, or everything on the general path
+        const int grid = grid_for(s, rec_hi - covered_hi, 256, 8);
+        if (s->scan_mode == DHSA_SCAN_RED_ONLY)
+            k_scan_records_generic<0><<<grid, 256, 0, s->stream>>>(rec_words, covered_hi, rec_hi, window_seconds,
+                                                                   window_id, cand_is_dst, s->tally, tally_late, words, s->dp);
+        else
+            k_scan_records_generic<1><<<grid, 256, 0, s->stream>>>(rec_words, covered_hi, rec_hi, window_seconds,
+                                                                   window_id, cand_is_dst, s->tally, tally_late, words, s->dp);
+        s->launches++;
+    }
+    CU(cudaGetLastError());
+    return DHSA_OK;
+}
+
+extern "C" int dhsa_update_records_device(dhsa_sketch_t *s, const void *records_dev, uint64_t n_in_buffer,
+                                          uint64_t rec_lo, uint64_t rec_hi, uint32_t window_seconds,
+                                          uint32_t window_id, int direction)
+{
+    NEED(s);
+    if (rec_lo >= rec_hi) return DHSA_OK;
+    NEED(records_dev);
+    if (rec_hi > n_in_buffer) return fail(DHSA_EDATA, "record range [%llu, %llu) exceeds the buffer's %llu records",
+                                          (unsigned long long)rec_lo, (unsigned long long)rec_hi,
+                                          (unsigned long long)n_in_buffer);
+    if (window_seconds == 0) return fail(DHSA_ECONFIG, "window_seconds must be positive (got 0)");
+    if (direction < 0 || direction > 2) return fail(DHSA_ECONFIG, "direction must be 0 (src), 1 (dst) or 2 (both)");
+    if ((uintptr_t)records_dev & 3u) return fail(DHSA_ECONFIG, "record buffer must be 4-byte aligned");
+    std::lock_guard<std::mutex> lk(s->mu);
+    if (int rc = use_device(s)) return rc;
+    const uint8_t *rec = static_cast<const uint8_t *>(records_dev);
+    // "both" feeds each record in both orientations (engine.py:191-192): two passes over the segment.
+    // Late records are tallied once, by the first pass.
+    if (direction == 0 || direction == 2)
+        if (int rc = scan_records_locked(s, rec, n_in_buffer, rec_lo, rec_hi, window_seconds, window_id, 0, 1)) return rc;
+    if (direction == 1 || direction == 2)
+        if (int rc = scan_records_locked(s, rec, n_in_buffer, rec_lo, rec_hi, window_seconds, window_id, 1,
+                                         direction == 1)) return rc;
+    return DHSA_OK;
+}
+
+extern "C" int dhsa_record_tally(dhsa_sketch_t *s, uint64_t *records_fed, uint64_t *records_dropped)
+{
+    NEED(s);
+    NEED(records_fed);
+    NEED(records_dropped);
+    std::lock_guard<std::mutex> lk(s->mu);
+    if (int rc = use_device(s)) return rc;
+    unsigned long long v[2];
+    CU(cudaMemcpyAsync(v, s->tally, sizeof v, cudaMemcpyDeviceToHost, s->stream));
+    CU(cudaStreamSynchronize(s->stream));
+    *records_fed = v[0], *records_dropped = v[1];
+    return DHSA_OK;
+}
+
+static int cmp_boundary(const void *a, const void *b)
+{
+    const dhsa_boundary_t *x = static_cast<const dhsa_boundary_t *>(a), *y = static_cast<const dhsa_boundary_t *>(b);
+    return (x->position > y->position) - (x->position < y->position);
+}
+
+extern "C" int dhsa_plan_windows(dhsa_sketch_t *s, const void *records_dev, uint64_t n_records, uint32_t window_seconds,
+                                 int64_t open_window, dhsa_boundary_t *out_host, uint32_t cap, uint32_t *n_out)
+{
+    NEED(s);
+    NEED(n_out);
+    *n_out = 0;
+    if (n_records == 0) return DHSA_OK;
+    NEED(records_dev);
+    NEED(out_host);
+    if (window_seconds == 0) return fail(DHSA_ECONFIG, "window_seconds must be positive (got 0)");
+    if ((uintptr_t)records_dev & 3u) return fail(DHSA_ECONFIG, "record buffer must be 4-byte aligned");
+    if (cap == 0) return fail(DHSA_ECONFIG, "boundary capacity must be positive");
+    std::lock_guard<std::mutex> lk(s->mu);
+    if (int rc = use_device(s)) return rc;
+    const uint64_t nblocks = (n_records + DHSA_PLAN_BLOCK - 1) / DHSA_PLAN_BLOCK;
+    if (nblocks > 0x7FFFFFFFull) return fail(DHSA_EDATA, "record buffer too large for one plan (%llu records)",
+                                             (unsigned long long)n_records);
+    if (nblocks > s->plan_blocks_cap || cap > s->plan_out_cap) {
+        CU(cudaStreamSynchronize(s->stream));
+        const uint64_t nb = nblocks > s->plan_blocks_cap ? nblocks : s->plan_blocks_cap;
+        const uint32_t nc = cap > s->plan_out_cap ? cap : s->plan_out_cap;
+        cudaFree(s->plan_block_max);
+        cudaFree(s->plan_carry);
+        cudaFree(s->plan_out);
+        s->plan_block_max = nullptr, s->plan_carry = nullptr, s->plan_out = nullptr;
+        s->plan_blocks_cap = 0, s->plan_out_cap = 0;
+        CU(cudaMalloc(&s->plan_block_max, nb * sizeof(uint32_t)));
+        CU(cudaMalloc(&s->plan_carry, nb * sizeof(long long)));
+        CU(cudaMalloc(&s->plan_out, (size_t)nc * sizeof(PlanBoundary)));
+        if (!s->plan_count) CU(cudaMalloc(&s->plan_count, sizeof(unsigned int)));
+        s->plan_blocks_cap = nb;
+        s->plan_out_cap = nc;
+    }
+    const uint32_t *rec_words = static_cast<const uint32_t *>(records_dev);
+    CU(cudaMemsetAsync(s->plan_count, 0, sizeof(unsigned int), s->stream));
+    k_plan_blockmax<<<(unsigned)nblocks, 256, 0, s->stream>>>(rec_words, n_records, window_seconds, s->plan_block_max);
+    k_plan_carry<<<1, 1024, 0, s->stream>>>(s->plan_block_max, nblocks, (long long)open_window, s->plan_carry);
+    k_plan_boundaries<<<(unsigned)nblocks, 256, 0, s->stream>>>(rec_words, n_records, window_seconds, s->plan_block_max,
+                                                              s->plan_carry, s->plan_out, cap, s->plan_count);
+    s->launches += 3;
+    CU(cudaGetLastError());
+    unsigned int n = 0;
+    CU(cudaMemcpyAsync(&n, s->plan_count, sizeof n, cudaMemcpyDeviceToHost, s->stream));
+    CU(cudaStreamSynchronize(s->stream));
+    if (n > cap) return fail(DHSA_EDATA, "record stream opens %u windows, more than the plan capacity %u", n, cap);
+    static_assert(sizeof(PlanBoundary) == sizeof(dhsa_boundary_t), "boundary layouts must match");
+    if (n) {
+        CU(cudaMemcpyAsync(out_host, s->plan_out, (size_t)n * sizeof(PlanBoundary), cudaMemcpyDeviceToHost, s->stream));
+        CU(cudaStreamSynchronize(s->stream));
+        qsort(out_host, n, sizeof(dhsa_boundary_t), cmp_boundary);
+    }
+    *n_out = n;
     return DHSA_OK;
 }
 

@@ -203,27 +203,121 @@ __device__ __forceinline__ void packet_slots(const DevParams &p, int wshift, uin
     }
 }
 
-template <int R, int MODE>
-__global__ void __launch_bounds__(256) k_scan_vec4(const uint4 *__restrict__ cand4,
-                                                   const uint4 *__restrict__ opp4, uint64_t nvec,
-                                                   uint32_t *__restrict__ words, DevParams p)
+// ------------------------------------------------------- packet sources --
+// Where a lane's 4 packets per trip come from.  The scan kernels are templated
+// on the source, so decode is fused into the scan instead of being a pass.
+//
+//   SoaSource     the reference's batch form: uint32 cand[], opp[] (8 B per packet),
+//                 Backend.update_batch(cand, opp) -- pkg/src/dhsa/_core.pyx:52-59.
+//   RecordSource  raw 12-byte IPPR trace records -- u32 timestamp little-endian, src
+//                 and dst IPv4 as u32 big-endian (pkg/src/dhsa/ingest.py:20) -- with
+//                 the window engine's per-record work folded in: window id =
+//                 ts // window_seconds (engine.py:140), late-record drop
+//                 (wins == arrival, engine.py:148), direction policy
+//                 (split_pairs, engine.py:179-194; "both" is two launches).
+//                 4 records = 48 B = three 16-byte loads per lane.
+struct SoaSource {
+    const uint4 *cand4, *opp4;
+    uint64_t nvec;
+    static constexpr bool kTally = false;
+    struct Raw {
+        uint4 c, o;
+    };
+    __host__ __device__ __forceinline__ uint64_t vectors() const { return nvec; }
+    __device__ __forceinline__ void load(Raw &r, uint64_t v, uint64_t pol) const
+    {
+        r.c = make_uint4(0, 0, 0, 0), r.o = make_uint4(0, 0, 0, 0);
+        if (v < nvec) {
+            r.c = ld_stream_v4(cand4 + v, pol);
+            r.o = ld_stream_v4(opp4 + v, pol);
+        }
+    }
+    __device__ __forceinline__ void unpack(const Raw &r, uint64_t v, uint32_t (&cs)[4], uint32_t (&os)[4],
+                                           bool (&ok)[4], uint32_t &, uint32_t &) const
+    {
+        cs[0] = r.c.x, cs[1] = r.c.y, cs[2] = r.c.z, cs[3] = r.c.w;
+        os[0] = r.o.x, os[1] = r.o.y, os[2] = r.o.z, os[3] = r.o.w;
+        ok[0] = ok[1] = ok[2] = ok[3] = v < nvec;
+    }
+};
+
+struct RecordSource {
+    const uint4 *rec4;        // quad q (records first_rec + 4q .. + 3) = rec4[3q .. 3q + 2]
+    uint64_t nquads;
+    uint64_t first_rec;       // record index of quad 0 in the caller's stream
+    uint64_t rec_lo, rec_hi;  // records of this launch: one window's contiguous segment
+    uint32_t window_seconds;
+    uint32_t window_id;
+    int cand_is_dst;          // direction policy: 0 "src" (cand = src), 1 "dst" (cand = dst)
+    unsigned long long *tally;  // [0] pairs fed (on-time records), [1] late records dropped
+    int tally_late;             // 0 on the second pass of "both", so a late record is counted once
+    static constexpr bool kTally = true;
+    struct Raw {
+        uint4 a, b, c;
+    };
+    __host__ __device__ __forceinline__ uint64_t vectors() const { return nquads; }
+    __device__ __forceinline__ void load(Raw &r, uint64_t v, uint64_t pol) const
+    {
+        r.a = r.b = r.c = make_uint4(0, 0, 0, 0);
+        if (v < nquads) {
+            r.a = ld_stream_v4(rec4 + 3 * v + 0, pol);
+            r.b = ld_stream_v4(rec4 + 3 * v + 1, pol);
+            r.c = ld_stream_v4(rec4 + 3 * v + 2, pol);
+        }
+    }
+    __device__ __forceinline__ void unpack(const Raw &r, uint64_t v, uint32_t (&cs)[4], uint32_t (&os)[4],
+                                           bool (&ok)[4], uint32_t &on_time, uint32_t &late) const
+    {
+        const uint32_t w[12] = {r.a.x, r.a.y, r.a.z, r.a.w, r.b.x, r.b.y, r.b.z, r.b.w, r.c.x, r.c.y, r.c.z, r.c.w};
+#pragma unroll
+        for (int j = 0; j < 4; j++) {
+            const uint64_t idx = first_rec + 4 * v + (uint64_t)j;
+            const bool mine = v < nquads && idx >= rec_lo && idx < rec_hi;
+            const uint32_t ts = w[3 * j];
+            const uint32_t src = __byte_perm(w[3 * j + 1], 0, 0x0123);  // network order -> host order
+            const uint32_t dst = __byte_perm(w[3 * j + 2], 0, 0x0123);
+            const bool fresh = mine && (ts / window_seconds) == window_id;
+            cs[j] = cand_is_dst ? dst : src;
+            os[j] = cand_is_dst ? src : dst;
+            ok[j] = fresh;
+            on_time += fresh;
+            late += mine && !fresh && tally_late;
+        }
+    }
+};
+
+template <typename SRC>
+__device__ __forceinline__ void flush_tally(const SRC &src, uint32_t on_time, uint32_t late, uint32_t lane)
+{
+    if (!SRC::kTally) return;
+    for (int d = 16; d > 0; d >>= 1) {
+        on_time += __shfl_xor_sync(0xFFFFFFFFu, on_time, d);
+        late += __shfl_xor_sync(0xFFFFFFFFu, late, d);
+    }
+    if (lane == 0) {
+        if (on_time) atomicAdd(((const RecordSource &)src).tally + 0, (unsigned long long)on_time);
+        if (late) atomicAdd(((const RecordSource &)src).tally + 1, (unsigned long long)late);
+    }
+}
+
+template <int R, int MODE, typename SRC>
+__global__ void __launch_bounds__(256) k_scan_vec4(SRC src, uint32_t *__restrict__ words, DevParams p)
 {
     const uint32_t lane = threadIdx.x & 31u;
+    const uint64_t nvec = src.vectors();
     const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
     const uint64_t warp0 = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int wshift = p.log2g - 5;
     const uint64_t pol = policy_evict_first();
+    uint32_t on_time = 0, late = 0;
 
     for (uint64_t base = warp0 * 32; base < nvec; base += nwarps * 32) {
         const uint64_t v = base + lane;
-        const bool valid = v < nvec;
-        uint4 c = make_uint4(0, 0, 0, 0), o = make_uint4(0, 0, 0, 0);
-        if (valid) {
-            c = ld_stream_v4(cand4 + v, pol);
-            o = ld_stream_v4(opp4 + v, pol);
-        }
-        const uint32_t cs[4] = {c.x, c.y, c.z, c.w};
-        const uint32_t os[4] = {o.x, o.y, o.z, o.w};
+        typename SRC::Raw raw;
+        src.load(raw, v, pol);
+        uint32_t cs[4], os[4];
+        bool ok[4];
+        src.unpack(raw, v, cs, os, ok, on_time, late);
 
         uint32_t widx[4][R];
         uint32_t mask[4];
@@ -235,19 +329,19 @@ __global__ void __launch_bounds__(256) k_scan_vec4(const uint4 *__restrict__ can
             packet_slots<R>(p, wshift, cs[j], h, d0, widx[j]);
         }
         if (MODE == 0) {
-            if (valid) {
 #pragma unroll
-                for (int j = 0; j < 4; j++)
+            for (int j = 0; j < 4; j++)
+                if (ok[j]) {
 #pragma unroll
                     for (int i = 0; i < R; i++) red_or(words + widx[j][i], mask[j]);
-            }
+                }
         } else {
             // all 4 * R test loads are issued before the first is consumed
             uint32_t w[4][R];
 #pragma unroll
             for (int j = 0; j < 4; j++)
 #pragma unroll
-                for (int i = 0; i < R; i++) w[j][i] = valid ? ld_sketch(words + widx[j][i]) : 0xFFFFFFFFu;
+                for (int i = 0; i < R; i++) w[j][i] = ok[j] ? ld_sketch(words + widx[j][i]) : 0xFFFFFFFFu;
 #pragma unroll
             for (int j = 0; j < 4; j++) {
 #pragma unroll
@@ -262,6 +356,7 @@ __global__ void __launch_bounds__(256) k_scan_vec4(const uint4 *__restrict__ can
             }
         }
     }
+    flush_tally(src, on_time, late, lane);
 }
 
 // K1, scan mode 3: the scan behind an exact flow cache.
@@ -313,79 +408,53 @@ __device__ __forceinline__ void fc_drain32(uint32_t *__restrict__ words, const D
     if (act) st_fc_way(p.fcache + m.slot, ~(((unsigned long long)m.cand << 32) | (unsigned long long)m.opp));
 }
 
-template <int R, int NV, int MINB, bool EVL>
-__global__ void __launch_bounds__(256, MINB) k_scan_flowcache(const uint4 *__restrict__ cand4,
-                                                              const uint4 *__restrict__ opp4, uint64_t nvec,
-                                                              uint32_t *__restrict__ words, DevParams p)
+template <int R, typename SRC>
+__global__ void __launch_bounds__(256, 3) k_scan_flowcache(SRC src, uint32_t *__restrict__ words, DevParams p)
 {
-    constexpr int NP = 4 * NV;  // packets per lane per trip
-    __shared__ FcMiss queue_s[8][32 + 32 * NP];
+    __shared__ FcMiss queue_s[8][32 + 128];  // < 32 left over + up to 128 pushed per trip
     const uint32_t lane = threadIdx.x & 31u;
     FcMiss *q = queue_s[threadIdx.x >> 5];
     uint32_t qn = 0;  // warp-uniform queue length
+    const uint64_t nvec = src.vectors();
     const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
     const uint64_t warp0 = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    const uint64_t step = nwarps * 32 * NV;
+    const uint64_t step = nwarps * 32;
     const int wshift = p.log2g - 5;
     const uint64_t pol = policy_evict_first();
     const uint32_t lt_mask = (1u << lane) - 1u;
     unsigned long long fc_hits = 0, fc_lookups = 0;
+    uint32_t on_time = 0, late = 0;
 
-    uint64_t base = warp0 * 32 * NV;
-    uint4 c_next[NV], o_next[NV];
-#pragma unroll
-    for (int u = 0; u < NV; u++) {
-        c_next[u] = make_uint4(0, 0, 0, 0), o_next[u] = make_uint4(0, 0, 0, 0);
-        const uint64_t v = base + (uint64_t)u * 32 + lane;
-        if (v < nvec) {
-            c_next[u] = ld_stream_v4(cand4 + v, pol);
-            o_next[u] = ld_stream_v4(opp4 + v, pol);
-        }
-    }
+    uint64_t base = warp0 * 32;
+    typename SRC::Raw next;
+    src.load(next, base + lane, pol);
     for (; base < nvec; base += step) {
-        uint32_t cs[NP], os[NP];
-        bool valid[NV];
-#pragma unroll
-        for (int u = 0; u < NV; u++) {
-            valid[u] = base + (uint64_t)u * 32 + lane < nvec;
-            cs[4 * u + 0] = c_next[u].x, cs[4 * u + 1] = c_next[u].y, cs[4 * u + 2] = c_next[u].z, cs[4 * u + 3] = c_next[u].w;
-            os[4 * u + 0] = o_next[u].x, os[4 * u + 1] = o_next[u].y, os[4 * u + 2] = o_next[u].z, os[4 * u + 3] = o_next[u].w;
-        }
+        uint32_t cs[4], os[4];
+        bool ok[4];
+        src.unpack(next, base + lane, cs, os, ok, on_time, late);
         // request the next trip's packets now; they land while the table sets are in flight
+        src.load(next, base + step + lane, pol);
+
+        unsigned long long e[4][4];
+        uint32_t set_idx[4], way_hint[4];
 #pragma unroll
-        for (int u = 0; u < NV; u++) {
-            const uint64_t vn = base + step + (uint64_t)u * 32 + lane;
-            if (vn < nvec) {
-                c_next[u] = ld_stream_v4(cand4 + vn, pol);
-                o_next[u] = ld_stream_v4(opp4 + vn, pol);
-            }
-        }
-        unsigned long long e[NP][4];
-        uint32_t set_idx[NP], way_hint[NP];
-#pragma unroll
-        for (int j = 0; j < NP; j++) {
+        for (int j = 0; j < 4; j++) {
             const uint64_t hh = mix64(p.state_h1 ^ (uint64_t)os[j]);
             const uint64_t hd = mix64(p.state_dh0 ^ (uint64_t)cs[j]);
             // set index from the high halves of both hashes (their low bits feed h and d0);
             // multiply-shift range reduction, so any set count works, not only powers of two
             set_idx[j] = __umulhi((uint32_t)(hh >> 32) + (uint32_t)(hd >> 32) * 0x9E3779B1u, p.fc_sets);
             way_hint[j] = (uint32_t)(hd >> 30) & 3u;
-            if (valid[j >> 2]) {
-                if (EVL)
-                    ld_fc_set_evict_last(p.fcache + ((size_t)set_idx[j] << 2), e[j]);
-                else
-                    ld_fc_set(p.fcache + ((size_t)set_idx[j] << 2), e[j]);
-            }
+            if (ok[j]) ld_fc_set(p.fcache + ((size_t)set_idx[j] << 2), e[j]);
         }
 #pragma unroll
-        for (int j = 0; j < NP; j++) {
-            const bool ok = valid[j >> 2];
+        for (int j = 0; j < 4; j++) {
             const unsigned long long inv_key = ~(((unsigned long long)cs[j] << 32) | (unsigned long long)os[j]);
-            const bool hit = ok && inv_key != 0ull &&
+            const bool hit = ok[j] && inv_key != 0ull &&
                              (e[j][0] == inv_key || e[j][1] == inv_key || e[j][2] == inv_key || e[j][3] == inv_key);
-            const bool miss = ok && !hit;
+            const bool miss = ok[j] && !hit;
             fc_hits += hit;
-            fc_lookups += ok;
+            fc_lookups += ok[j];
             const unsigned bal = __ballot_sync(0xFFFFFFFFu, miss);
             if (bal == 0) continue;
             if (miss) {
@@ -416,6 +485,7 @@ __global__ void __launch_bounds__(256, MINB) k_scan_flowcache(const uint4 *__res
         atomicAdd(p.fc_stats + 0, fc_lookups);
         atomicAdd(p.fc_stats + 1, fc_hits);
     }
+    flush_tally(src, on_time, late, lane);
 }
 
 // General path: any r <= 64, any g >= 8 (sub-word cells included), 64-bit bit
@@ -437,6 +507,151 @@ __global__ void __launch_bounds__(256) k_scan_generic(const uint32_t *__restrict
             uint32_t *wp = words + (B >> 5);
             const uint32_t m = 1u << (uint32_t)(B & 31);
             if (MODE == 0 || (ld_sketch(wp) & m) == 0) red_or(wp, m);
+        }
+    }
+}
+
+// Records through the general path (any parameters, ragged ends of a segment):
+// one record per lane per trip, 4-byte loads.
+template <int MODE>
+__global__ void __launch_bounds__(256) k_scan_records_generic(const uint32_t *__restrict__ rec_words, uint64_t rec_lo,
+                                                              uint64_t rec_hi, uint32_t window_seconds,
+                                                              uint32_t window_id, int cand_is_dst,
+                                                              unsigned long long *tally, int tally_late,
+                                                              uint32_t *__restrict__ words, DevParams p)
+{
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    const uint64_t pol = policy_evict_first();
+    uint32_t on_time = 0, late = 0;
+    for (uint64_t t = rec_lo + (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; t < rec_hi; t += stride) {
+        const uint32_t ts = ld_stream_u32(rec_words + 3 * t, pol);
+        const uint32_t src = __byte_perm(ld_stream_u32(rec_words + 3 * t + 1, pol), 0, 0x0123);
+        const uint32_t dst = __byte_perm(ld_stream_u32(rec_words + 3 * t + 2, pol), 0, 0x0123);
+        if (ts / window_seconds != window_id) {
+            late += tally_late;
+            continue;
+        }
+        on_time++;
+        const uint64_t a = cand_is_dst ? dst : src;
+        const uint64_t h = mix64(p.state_h1 ^ (uint64_t)(cand_is_dst ? src : dst)) & p.gmask;
+        const uint32_t d0 = (uint32_t)mix64(p.state_dh0 ^ a) & p.kmask;
+        for (int i = 0; i < p.r; i++) {
+            const uint64_t cell = ((uint64_t)i << p.k) | index_of(p, a, d0, i);
+            const uint64_t B = (cell << p.log2g) + h;
+            uint32_t *wp = words + (B >> 5);
+            const uint32_t m = 1u << (uint32_t)(B & 31);
+            if (MODE == 0 || (ld_sketch(wp) & m) == 0) red_or(wp, m);
+        }
+    }
+    if (on_time) atomicAdd(tally + 0, (unsigned long long)on_time);
+    if (late) atomicAdd(tally + 1, (unsigned long long)late);
+}
+
+// Window plan of a record stream (engine.py:140-149): a record arrives during the
+// running maximum of the window ids seen so far, so the stream splits into
+// contiguous segments, one per window, at the records where that running maximum
+// rises.  Pass 1: per-block maximum window id.  Pass 2 (one CTA): exclusive
+// prefix maximum over blocks, seeded with the window already open.  Pass 3:
+// every block replays its records against its carry-in and appends a
+// (position, new window id) boundary wherever the running maximum rises.
+#define DHSA_PLAN_BLOCK 4096  // records per plan block (256 threads x 16)
+
+__global__ void __launch_bounds__(256) k_plan_blockmax(const uint32_t *__restrict__ rec_words, uint64_t n,
+                                                       uint32_t window_seconds, uint32_t *__restrict__ block_max)
+{
+    __shared__ uint32_t warp_max[8];
+    const uint64_t lo = (uint64_t)blockIdx.x * DHSA_PLAN_BLOCK;
+    uint32_t m = 0;
+    for (uint32_t q = threadIdx.x; q < DHSA_PLAN_BLOCK; q += 256) {
+        const uint64_t t = lo + q;
+        if (t < n) m = max(m, rec_words[3 * t] / window_seconds);
+    }
+    for (int d = 16; d > 0; d >>= 1) m = max(m, __shfl_xor_sync(0xFFFFFFFFu, m, d));
+    if ((threadIdx.x & 31) == 0) warp_max[threadIdx.x >> 5] = m;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int w = 1; w < 8; w++) m = max(m, warp_max[w]);
+        block_max[blockIdx.x] = m;
+    }
+}
+
+// carry[b] = max(seed, block_max[0 .. b-1]) as a signed 64-bit value (seed -1 = no window open yet)
+__global__ void __launch_bounds__(1024) k_plan_carry(const uint32_t *__restrict__ block_max, uint64_t nblocks,
+                                                     long long seed, long long *__restrict__ carry)
+{
+    __shared__ long long warp_tot[32];
+    __shared__ long long running_s;
+    const uint32_t lane = threadIdx.x & 31u, wid = threadIdx.x >> 5;
+    if (threadIdx.x == 0) running_s = seed;
+    __syncthreads();
+    for (uint64_t b0 = 0; b0 < nblocks; b0 += 1024) {
+        const uint64_t b = b0 + threadIdx.x;
+        const long long mine = b < nblocks ? (long long)block_max[b] : -1;
+        long long inc = mine;
+        for (int d = 1; d < 32; d <<= 1) {
+            const long long t = __shfl_up_sync(0xFFFFFFFFu, inc, d);
+            if (lane >= (uint32_t)d) inc = max(inc, t);
+        }
+        if (lane == 31) warp_tot[wid] = inc;
+        __syncthreads();
+        long long before = running_s;  // everything before this chunk
+        for (uint32_t w = 0; w < wid; w++) before = max(before, warp_tot[w]);
+        long long excl = __shfl_up_sync(0xFFFFFFFFu, inc, 1);
+        if (lane == 0) excl = -1;
+        if (b < nblocks) carry[b] = max(before, excl);
+        __syncthreads();
+        if (threadIdx.x == 1023) running_s = max(before, inc);
+        __syncthreads();
+    }
+}
+
+struct PlanBoundary {
+    unsigned long long position;  // first record of the segment
+    long long window_id;
+};
+
+__global__ void __launch_bounds__(256) k_plan_boundaries(const uint32_t *__restrict__ rec_words, uint64_t n,
+                                                         uint32_t window_seconds,
+                                                         const uint32_t *__restrict__ block_max,
+                                                         const long long *__restrict__ carry,
+                                                         PlanBoundary *__restrict__ out, unsigned int cap,
+                                                         unsigned int *__restrict__ count)
+{
+    // no record of this block raises the running maximum: nothing to find, nothing to read
+    if ((long long)block_max[blockIdx.x] <= carry[blockIdx.x]) return;
+    // 256 threads x 16 consecutive records: thread-local running max, block scan of the
+    // per-thread maxima, then each thread replays its 16 records against its own carry-in
+    __shared__ long long warp_tot[8];
+    const uint32_t lane = threadIdx.x & 31u, wid = threadIdx.x >> 5;
+    const uint64_t t0 = (uint64_t)blockIdx.x * DHSA_PLAN_BLOCK + (uint64_t)threadIdx.x * 16;
+    long long win[16];
+    long long tmax = -1;
+#pragma unroll
+    for (int q = 0; q < 16; q++) {
+        win[q] = t0 + q < n ? (long long)(rec_words[3 * (t0 + q)] / window_seconds) : -1;
+        tmax = max(tmax, win[q]);
+    }
+    long long inc = tmax;
+    for (int d = 1; d < 32; d <<= 1) {
+        const long long t = __shfl_up_sync(0xFFFFFFFFu, inc, d);
+        if (lane >= (uint32_t)d) inc = max(inc, t);
+    }
+    if (lane == 31) warp_tot[wid] = inc;
+    __syncthreads();
+    long long run = carry[blockIdx.x];
+    for (uint32_t w = 0; w < wid; w++) run = max(run, warp_tot[w]);
+    long long excl = __shfl_up_sync(0xFFFFFFFFu, inc, 1);
+    if (lane == 0) excl = -1;
+    run = max(run, excl);
+#pragma unroll
+    for (int q = 0; q < 16; q++) {
+        if (win[q] > run) {
+            run = win[q];
+            const unsigned int pos = atomicAdd(count, 1u);
+            if (pos < cap) {
+                out[pos].position = t0 + q;
+                out[pos].window_id = run;
+            }
         }
     }
 }

@@ -217,7 +217,9 @@ class ShardedWindow:
                     can = 0
         except Exception:
             can = 0
-        flag = torch.tensor([can], dtype=torch.int32, device=f"cuda:{self.sketch.device}")
+        on_gpu = dist.get_backend(self.group) == "nccl"   # gloo rendezvous (tests) reduces on the host
+        flag = torch.tensor([can], dtype=torch.int32,
+                            device=f"cuda:{self.sketch.device}" if on_gpu else "cpu")
         dist.all_reduce(flag, op=dist.ReduceOp.MIN, group=self.group)
         if int(flag.item()) == 0:
             return False

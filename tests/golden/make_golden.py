@@ -219,6 +219,32 @@ def main():
     rec.update(readout(sk, 1024))
     with open(os.path.join(HERE, "config1_expected.json"), "w") as fh:
         json.dump(rec, fh, indent=1)
+    # snapshots (row N2): the reference's own file bytes for one sketch
+    import io
+    sk = Dhla(P, backend=BACKEND)
+    sk.update_batch(*O.distinct_pairs(50_000, 19))
+    sk.window_id = 77
+    buf = io.BytesIO()
+    dhla.write_snapshot(sk, buf)
+    blob = buf.getvalue()
+    with open(os.path.join(HERE, "snapshot_case.json"), "w") as fh:
+        json.dump(dict(pairs=[50_000, 19], window_id=77, size=len(blob), header_hex=blob[:42].hex(),
+                       file_sha256=hashlib.sha256(blob).hexdigest()), fh, indent=1)
+
+    # window engine (row N1): the reference's DetectionEngine on a multi-window trace with late records
+    from dhsa.engine import DetectionEngine, WindowConfig
+    eng = []
+    for seed in (9, 10):
+        trace = O.engine_trace(seed)
+        for direction in ("src", "dst", "both"):
+            res = DetectionEngine(WindowConfig(direction=direction, batch_pairs=1000), backend=BACKEND).run(trace)
+            eng.append(dict(seed=seed, direction=direction, window_seconds=300, theta=1024,
+                            records=int(len(trace)), trace_sha256=sha(trace),
+                            windows=[dict(window_id=r.window_id, pairs=r.pairs, dropped=r.dropped,
+                                          reports=[[x.host, x.estimate, bool(x.saturated)] for x in r.reports])
+                                     for r in res]))
+    with open(os.path.join(HERE, "engine_cases.json"), "w") as fh:
+        json.dump(eng, fh, indent=1)
     print("wrote", sorted(os.listdir(HERE)))
 
 

@@ -519,3 +519,63 @@ def test_sharded_scan_plus_or_merge_equals_single_scan():
         shards[0].merge_from(sk)
     assert sha(shards[0].bits) == sha(whole.bits)
     assert shards[0].restore_superpoints(1024) == whole.restore_superpoints(1024)
+
+
+# ------------------------------------------ multi-process merge over CUDA IPC --
+
+
+def _ipc_rank(rank, world, port, mode, q):
+    import os
+
+    import torch.distributed as dist
+
+    from paper_1803_11449_b200.multi import ShardedWindow, packet_slice
+
+    os.environ["MASTER_ADDR"], os.environ["MASTER_PORT"] = "127.0.0.1", str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        cand, opp = O.distinct_pairs(300_000, 55)
+        for n, host in enumerate((0x0A0B0C0D, 0x01020304, 0xC63A1B02)):
+            c2, o2 = O.plant_pairs(host, 2048 + 100 * n, 70 + n)
+            cand, opp = np.concatenate([cand, c2]), np.concatenate([opp, o2])
+        order = np.random.default_rng(3).permutation(len(cand))
+        cand, opp = cand[order], opp[order]
+        lo, hi = packet_slice(len(cand), rank, world)
+        win = ShardedWindow(P.DhgParams(), theta=1024, device=0, merge=mode)
+        win.scan(cand[lo:hi], opp[lo:hi])
+        used = win.merge()
+        ora = O.OracleSketch()
+        ora.update_batch(cand, opp, threads=2)
+        want = ora.restore_superpoints(1024)
+        got = win.restore()
+        ok = (np.array_equal(win.sketch.bits, ora.bits)
+              and [(r.host, r.saturated) for r in got] == [(r.host, r.saturated) for r in want]
+              and len(got) == 3)
+        q.put((rank, used, bool(ok)))
+        dist.barrier()
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_sharded_window_merges_over_cuda_ipc_between_processes(world):
+    """The real multi-process path -- one process per rank, sketches exported with
+    cudaIpcGetMemHandle, peers mapped with cudaIpcOpenMemHandle, k_or_merge and
+    k_copy_slice reading the mapped pointers -- with every rank on this one GPU
+    (gloo does the rendezvous because NCCL refuses two ranks on one device)."""
+    import os
+
+    import torch.multiprocessing as mp
+
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = 29700 + os.getpid() % 1000 + world
+    procs = [ctx.Process(target=_ipc_rank, args=(r, world, port, "p2p", q)) for r in range(world)]
+    for p_ in procs:
+        p_.start()
+    results = [q.get(timeout=300) for _ in range(world)]
+    for p_ in procs:
+        p_.join(timeout=60)
+        assert p_.exitcode == 0
+    assert sorted(r[0] for r in results) == list(range(world))
+    assert all(used == "p2p" and ok for _, used, ok in results), results

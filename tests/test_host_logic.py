@@ -120,3 +120,18 @@ def test_product_package_never_imports_the_oracle():
             if f.endswith((".py", ".cu", ".cuh", ".h")):
                 text = open(os.path.join(base, f)).read()
                 assert "oracle" not in text.replace("no CPU oracle", ""), f"{f} mentions the oracle"
+
+
+def test_library_has_no_device_function_host_stubs_on_call_paths():
+    """nvcc compiles a __device__ function that host code calls inside a template into an
+    exit(1) stub instead of an error; make sure none is reachable in the built library."""
+    import shutil
+    import subprocess
+
+    from paper_1803_11449_b200 import _build
+
+    if shutil.which("objdump") is None:
+        pytest.skip("objdump not available")
+    _cabi.lib()
+    asm = subprocess.run(["objdump", "-d", "--no-show-raw-insn", _build.LIB_PATH], capture_output=True, text=True).stdout
+    assert "<exit@plt>" not in asm.replace("<__cxa_atexit@plt>", "")

@@ -206,3 +206,20 @@ def test_oracle_equals_reference_compiled_loops(kw):
     assert np.array_equal(core.zero_counts(ref_bits), sk.zero_counts())
     if not kw:
         assert sha(sk.bits) == "38d4cac25b1922468b09d87d40a536699a03d0a58ac44cdc776a8ed1995dd136"
+
+
+ENGINE_CASES = load_json("engine_cases.json")
+
+
+@pytest.mark.parametrize("case", ENGINE_CASES, ids=[f"{c['seed']}-{c['direction']}" for c in ENGINE_CASES])
+def test_engine_oracle_matches_reference_engine_fixture(case):
+    """oracle.run_windows against what the reference's DetectionEngine produced."""
+    trace = O.engine_trace(case["seed"])
+    assert sha(trace) == case["trace_sha256"]
+    got = O.run_windows(trace, case["window_seconds"], case["theta"], case["direction"])
+    assert [(w, p, d) for w, p, d, _ in got] == \
+        [(w["window_id"], w["pairs"], w["dropped"]) for w in case["windows"]]
+    for (_, _, _, reps), w in zip(got, case["windows"]):
+        assert [(r.host, r.saturated) for r in reps] == [(h, s) for h, _, s in w["reports"]]
+        for r, (_, e, _) in zip(reps, w["reports"]):
+            assert r.estimate == pytest.approx(e, rel=1e-12)
