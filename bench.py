@@ -179,6 +179,14 @@ def run_reference(args, rank: int) -> None:
 
 # ------------------------------------------------------------------- GPU arm --
 
+_T0 = time.perf_counter()
+
+
+def log(msg: str) -> None:
+    """Progress on stderr (stdout carries only the JSON line)."""
+    print(f"[bench +{time.perf_counter() - _T0:6.1f}s] {msg}", file=sys.stderr, flush=True)
+
+
 def run_ours(args, rank: int, local_rank: int, world: int) -> None:
     import torch
     import torch.distributed as dist
@@ -212,6 +220,7 @@ def run_ours(args, rank: int, local_rank: int, world: int) -> None:
     del pick
     torch.cuda.synchronize()
 
+    log(f"window generated: {n} packets over {flows} flows")
     win = ShardedWindow(P.DhgParams(), theta=THETA, device=local_rank, merge=args.merge)
     sk = win.sketch
     sk.set_scan_mode(args.scan_mode)
@@ -260,6 +269,7 @@ def run_ours(args, rank: int, local_rank: int, world: int) -> None:
                   "n_superpoints": len(reports),
                   "scanners_found": int(len(set(scanners.tolist()) & {r.host for r in reports}))}
 
+    log("warm-up and parity done")
     # -- timed: device-resident window
     evs = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(args.steps)]
     t_begin, t_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -277,6 +287,7 @@ def run_ours(args, rank: int, local_rank: int, world: int) -> None:
     scan_ms = float(np.mean([e[0].elapsed_time(e[1]) for e in evs]))
     readout_ms = float(np.mean([e[1].elapsed_time(e[2]) for e in evs]))
 
+    log(f"device-resident timing done: {ms_total / args.steps:.3f} ms per window")
     # -- timed: end to end from pinned host arrays through the public API
     e2e = None
     if not args.no_e2e:
@@ -306,6 +317,68 @@ def run_ours(args, rank: int, local_rank: int, world: int) -> None:
         e2e = (e2e_ms, len(reports_h))
         del cand_h, opp_h
 
+    log("end-to-end timing done")
+    # -- row N1: the same window as raw 12-byte trace records through DetectionEngine (record decode,
+    #    windowing, late drop and direction split fused into the scan).  Two windows, 1% late records.
+    rec_stats = None
+    if world == 1 and not args.no_records:
+        wsec = 300
+        half = n // 2
+        gen2 = torch.Generator(device=dev)
+        gen2.manual_seed(args.seed + 7)
+        ts = torch.randint(7 * wsec, 8 * wsec, (n,), device=dev, generator=gen2, dtype=torch.int32)
+        ts[half:] += wsec
+        late = torch.rand(n - half, device=dev, generator=gen2) < 0.01
+        ts[half:][late] -= wsec                      # stamped in window 7 but arriving during window 8: dropped
+
+        def bswap(x):                                # host order -> network order, as captures deliver addresses
+            x = x.to(torch.int64) & 0xFFFFFFFF
+            y = ((x & 0xFF) << 24) | ((x & 0xFF00) << 8) | ((x >> 8) & 0xFF00) | ((x >> 24) & 0xFF)
+            return (y - ((y >> 31) << 32)).to(torch.int32)
+
+        rec_dev = torch.empty((n, 3), dtype=torch.int32, device=dev)
+        rec_dev[:, 0] = ts
+        rec_dev[:, 1] = bswap(cand_d)
+        rec_dev[:, 2] = bswap(opp_d)
+        n_late = int(late.sum().item())
+        del ts, late
+        raw_dev = rec_dev.view(torch.uint8).reshape(-1)
+        eng = P.DetectionEngine(P.WindowConfig(theta=THETA, window_seconds=wsec), device=local_rank)
+        for _ in range(2):
+            res = eng.run(raw_dev)
+        ok = [r.window_id for r in res] == [7, 8] and res[0].pairs == half and \
+            res[1].pairs == n - half - n_late and res[1].dropped == n_late
+        r0, r1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        r0.record(stream)
+        for _ in range(args.steps):
+            res = eng.run(raw_dev)
+        r1.record(stream)
+        torch.cuda.synchronize()
+        rec_ms = r0.elapsed_time(r1) / args.steps
+        rec_stats = {"device_resident_mpps": n / (rec_ms * 1e-3) / 1e6, "ms_per_step": rec_ms,
+                     "bytes_per_packet": 12, "windows": len(res), "late_dropped": n_late,
+                     "counts_match": bool(ok), "superpoints_per_window": [len(r.reports) for r in res]}
+        if not args.no_e2e:
+            rec_h = torch.empty(n * 12, dtype=torch.uint8, pin_memory=True)
+            rec_h.copy_(raw_dev)
+            torch.cuda.synchronize()
+            rec_np = rec_h.numpy()
+            eng.run(rec_np)
+            torch.cuda.synchronize()
+            r0.record(stream)
+            for _ in range(args.steps):
+                res = eng.run(rec_np)
+            r1.record(stream)
+            torch.cuda.synchronize()
+            ms = r0.elapsed_time(r1) / args.steps
+            rec_stats["e2e_mpps"] = n / (ms * 1e-3) / 1e6
+            rec_stats["e2e_ms_per_step"] = ms
+            rec_stats["e2e_h2d_bytes_per_step"] = 12 * n
+            del rec_h
+        del rec_dev, raw_dev
+
+    log("records path done")
     # -- max over ranks
     stats = torch.tensor([ms_total, scan_ms, readout_ms, e2e[0] if e2e else 0.0], device=dev, dtype=torch.float64)
     if world > 1:
@@ -371,6 +444,8 @@ def run_ours(args, rank: int, local_rank: int, world: int) -> None:
         }
         if parity:
             line["parity"] = parity
+        if rec_stats:
+            line["records_path"] = rec_stats
         if e2e:
             reports_bytes = 24 * e2e[1] + 1608  # dhsa_report_t rows + the 1608-byte control block read back per window
             line["e2e"] = {"value": world * n * args.steps / (e2e_ms * 1e-3) / 1e6, "unit": "Mpps",
@@ -383,6 +458,7 @@ def run_ours(args, rank: int, local_rank: int, world: int) -> None:
             threads = os.cpu_count() or 1
             cpu_reference_window(cand_s[: m // 4], opp_s[: m // 4], threads)  # page in, spin up the pool
             kind, t_scan, t_all, _ = cpu_reference_window(cand_s, opp_s, threads)
+            log("cpu baseline done")
             line["cpu_baseline"] = {
                 "value": m / t_all / 1e6, "unit": "Mpps", "cores": threads, "kind": kind,
                 "scan_only_mpps": m / t_scan / 1e6,
@@ -411,6 +487,7 @@ def main() -> None:
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-parity", action="store_true")
     ap.add_argument("--no-probe", action="store_true")
+    ap.add_argument("--no-records", action="store_true", help="skip the raw-record (DetectionEngine) leg")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
     rank = int(os.environ.get("RANK", "0"))

@@ -194,6 +194,12 @@ int dhsa_update_records_device(dhsa_sketch_t *s, const void *records_dev, uint64
                                uint32_t window_id, int direction);
 int dhsa_record_tally(dhsa_sketch_t *s, uint64_t *records_fed, uint64_t *records_dropped);
 
+/* Host -> device staging copy on a caller-chosen stream (cudaMemcpyAsync): DMA straight from
+ * page-locked host memory, the driver's bounce buffers otherwise.  Lets the Python engine
+ * stage numpy record buffers without routing them through another library. */
+int dhsa_copy_to_device_async(int device, void *dst_dev, const void *src_host, uint64_t nbytes,
+                              void *cuda_stream);
+
 /* ---- merge: dhsa.dhla.merge (pkg/src/dhsa/dhla.py:305-318) ------------------------ */
 
 /* dst |= src; both handles in this process (same or peer device).  Parameter

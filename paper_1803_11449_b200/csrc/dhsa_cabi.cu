@@ -302,7 +302,7 @@ static int ensure_flow_cache_locked(dhsa_sketch *s)
 extern "C" int dhsa_set_flow_cache(dhsa_sketch_t *s, uint64_t n_sets)
 {
     NEED(s);
-    if (n_sets < 1024 || n_sets > (1ull << 27))
+    if (n_sets < 1024 || n_sets > (1ull << 27))  // slot indices carry a flag in bit 31: sets * 4 < 2^31
         return fail(DHSA_ECONFIG, "flow cache size must satisfy 1024 <= n_sets <= 2^27 (got %llu)",
                     (unsigned long long)n_sets);
     std::lock_guard<std::mutex> lk(s->mu);
@@ -425,7 +425,8 @@ static void launch_scan_src(dhsa_sketch *s, int mode, const SRC &src)
     case DHSA_SCAN_TEST_RED: LAUNCH((k_scan_vec4<R, 1, SRC>), 3); break;
     case DHSA_SCAN_TEST_AGG_RED: LAUNCH((k_scan_vec4<R, 2, SRC>), 2); break;
     // flow cache: 4 packets per lane at 3 CTAs/SM measured best on B200 (profiles/r01_flowcache_variants.txt);
-    // 8 packets per lane, 4 CTAs/SM (spills) and L2::evict_last table loads were slower or equal
+    // 8 packets per lane, 4 CTAs/SM (spills) and L2::evict_last table loads were slower or equal; staging the
+    // packet stream by TMA was 2-3% faster than register prefetch and is the only form kept
     default: LAUNCH((k_scan_flowcache<R, SRC>), 3); break;
     }
 #undef LAUNCH
@@ -602,6 +603,17 @@ extern "C" int dhsa_record_tally(dhsa_sketch_t *s, uint64_t *records_fed, uint64
     CU(cudaMemcpyAsync(v, s->tally, sizeof v, cudaMemcpyDeviceToHost, s->stream));
     CU(cudaStreamSynchronize(s->stream));
     *records_fed = v[0], *records_dropped = v[1];
+    return DHSA_OK;
+}
+
+extern "C" int dhsa_copy_to_device_async(int device, void *dst_dev, const void *src_host, uint64_t nbytes,
+                                         void *cuda_stream)
+{
+    if (nbytes == 0) return DHSA_OK;
+    NEED(dst_dev);
+    NEED(src_host);
+    CU(cudaSetDevice(device));
+    CU(cudaMemcpyAsync(dst_dev, src_host, nbytes, cudaMemcpyHostToDevice, (cudaStream_t)cuda_stream));
     return DHSA_OK;
 }
 

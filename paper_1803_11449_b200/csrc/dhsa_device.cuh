@@ -132,14 +132,6 @@ __device__ __forceinline__ void ld_fc_set(const unsigned long long *set, unsigne
                  : "memory");
 }
 
-__device__ __forceinline__ void ld_fc_set_evict_last(const unsigned long long *set, unsigned long long (&e)[4])
-{
-    asm volatile("ld.global.L1::no_allocate.L2::evict_last.v4.b64 {%0,%1,%2,%3}, [%4];"
-                 : "=l"(e[0]), "=l"(e[1]), "=l"(e[2]), "=l"(e[3])
-                 : "l"(set)
-                 : "memory");
-}
-
 __device__ __forceinline__ void st_fc_way(unsigned long long *slot, unsigned long long v)
 {
     asm volatile("st.global.cg.u64 [%0], %1;" ::"l"(slot), "l"(v) : "memory");
@@ -203,6 +195,54 @@ __device__ __forceinline__ void packet_slots(const DevParams &p, int wshift, uin
     }
 }
 
+// ------------------------------------------- TMA bulk copies + mbarriers --
+// cp.async.bulk (SASS UBLKCP): the TMA engine moves a contiguous run of global
+// memory into shared memory and signals an mbarrier with the byte count, so the
+// packet stream neither occupies registers nor competes with the scattered
+// sketch / flow-cache accesses for the SM's L1-miss request port.
+__device__ __forceinline__ uint32_t smem_u32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void mbar_init(uint32_t mbar, uint32_t arrivals)
+{
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(mbar), "r"(arrivals) : "memory");
+}
+
+__device__ __forceinline__ void mbar_expect_tx(uint32_t mbar, uint32_t bytes)
+{
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(mbar), "r"(bytes) : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint32_t mbar, uint32_t parity)
+{
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        "@p bra DONE_%=;\n"
+        "bra WAIT_%=;\n"
+        "DONE_%=:\n"
+        "}\n" ::"r"(mbar),
+        "r"(parity)
+        : "memory");
+}
+
+__device__ __forceinline__ void bulk_g2s(uint32_t smem_dst, const void *gmem_src, uint32_t bytes, uint32_t mbar,
+                                         uint64_t pol)
+{
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+            smem_dst),
+        "l"(gmem_src), "r"(bytes), "r"(mbar), "l"(pol)
+        : "memory");
+}
+
+// order this thread's earlier generic-proxy accesses to shared memory before later async-proxy ones
+__device__ __forceinline__ void fence_proxy_async_smem()
+{
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
 // ------------------------------------------------------- packet sources --
 // Where a lane's 4 packets per trip come from.  The scan kernels are templated
 // on the source, so decode is fused into the scan instead of being a pass.
@@ -231,6 +271,22 @@ struct SoaSource {
             r.c = ld_stream_v4(cand4 + v, pol);
             r.o = ld_stream_v4(opp4 + v, pol);
         }
+    }
+    // staged form: one warp trip = 32 vectors = 512 B of cand then 512 B of opp in shared memory
+    static constexpr int kStageBytes = 1024;
+    static constexpr int kStages = 4;
+    __device__ __forceinline__ void stage_issue(uint32_t smem_dst, uint32_t mbar, uint64_t base, uint32_t count,
+                                                uint64_t pol) const
+    {
+        const uint32_t bytes = count * 16u;
+        mbar_expect_tx(mbar, 2u * bytes);
+        bulk_g2s(smem_dst, cand4 + base, bytes, mbar, pol);
+        bulk_g2s(smem_dst + 512u, opp4 + base, bytes, mbar, pol);
+    }
+    __device__ __forceinline__ void stage_read(Raw &r, const uint8_t *stage, uint32_t lane) const
+    {
+        r.c = *reinterpret_cast<const uint4 *>(stage + lane * 16u);
+        r.o = *reinterpret_cast<const uint4 *>(stage + 512u + lane * 16u);
     }
     __device__ __forceinline__ void unpack(const Raw &r, uint64_t v, uint32_t (&cs)[4], uint32_t (&os)[4],
                                            bool (&ok)[4], uint32_t &, uint32_t &) const
@@ -264,6 +320,21 @@ struct RecordSource {
             r.b = ld_stream_v4(rec4 + 3 * v + 1, pol);
             r.c = ld_stream_v4(rec4 + 3 * v + 2, pol);
         }
+    }
+    // staged form: one warp trip = 32 quads = 1536 contiguous bytes of records
+    static constexpr int kStageBytes = 1536;
+    static constexpr int kStages = 2;  // keeps the kernel inside 48 KB of static shared memory
+    __device__ __forceinline__ void stage_issue(uint32_t smem_dst, uint32_t mbar, uint64_t base, uint32_t count,
+                                                uint64_t pol) const
+    {
+        const uint32_t bytes = count * 48u;
+        mbar_expect_tx(mbar, bytes);
+        bulk_g2s(smem_dst, rec4 + 3 * base, bytes, mbar, pol);
+    }
+    __device__ __forceinline__ void stage_read(Raw &r, const uint8_t *stage, uint32_t lane) const
+    {
+        const uint4 *q = reinterpret_cast<const uint4 *>(stage + lane * 48u);
+        r.a = q[0], r.b = q[1], r.c = q[2];
     }
     __device__ __forceinline__ void unpack(const Raw &r, uint64_t v, uint32_t (&cs)[4], uint32_t (&os)[4],
                                            bool (&ok)[4], uint32_t &on_time, uint32_t &late) const
@@ -388,6 +459,17 @@ struct FcMiss {
     uint32_t cand, opp, slot;  // slot = set * 4 + way to fill
 };
 
+// Set of a pair: from the high halves of the two hashes (their low bits feed h and d0),
+// multiply-shift range reduction so any set count works, not only powers of two.
+// (A second-choice set probed on a miss was tried: hit rate 0.925 -> 0.953 at 64 MiB, but the
+// heavier drain made the scan 20% slower -- profiles/r01_flowcache_variants.txt.)
+__device__ __forceinline__ uint32_t fc_set_of(uint64_t hh, uint64_t hd, uint32_t n_sets)
+{
+    return __umulhi((uint32_t)(hh >> 32) + (uint32_t)(hd >> 32) * 0x9E3779B1u, n_sets);
+}
+
+// Drain up to 32 queued misses, one per lane: the R test loads of a lane are in flight
+// together, REDs are warp-aggregated, then the pair is recorded in the table.
 template <int R>
 __device__ __forceinline__ void fc_drain32(uint32_t *__restrict__ words, const DevParams &p, int wshift,
                                            const FcMiss *q, uint32_t n_active, uint32_t lane)
@@ -408,13 +490,19 @@ __device__ __forceinline__ void fc_drain32(uint32_t *__restrict__ words, const D
     if (act) st_fc_way(p.fcache + m.slot, ~(((unsigned long long)m.cand << 32) | (unsigned long long)m.opp));
 }
 
+// The packet stream is staged by TMA: every warp owns a ring of SRC::kStages
+// shared-memory slots and one mbarrier per slot; lane 0 keeps the ring full with
+// cp.async.bulk copies (one warp trip per slot), all lanes wait on the slot's
+// mbarrier parity and read their 16-byte vectors with LDS.128.
 template <int R, typename SRC>
 __global__ void __launch_bounds__(256, 3) k_scan_flowcache(SRC src, uint32_t *__restrict__ words, DevParams p)
 {
-    __shared__ FcMiss queue_s[8][32 + 128];  // < 32 left over + up to 128 pushed per trip
-    const uint32_t lane = threadIdx.x & 31u;
-    FcMiss *q = queue_s[threadIdx.x >> 5];
-    uint32_t qn = 0;  // warp-uniform queue length
+    __shared__ FcMiss queue_s[8][32 + 128];
+    __shared__ __align__(128) uint8_t stage_s[8][SRC::kStages][SRC::kStageBytes];
+    __shared__ __align__(8) unsigned long long mbar_s[8][SRC::kStages];
+    const uint32_t lane = threadIdx.x & 31u, wib = threadIdx.x >> 5;
+    FcMiss *q = queue_s[wib];
+    uint32_t qn = 0;
     const uint64_t nvec = src.vectors();
     const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
     const uint64_t warp0 = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -425,15 +513,45 @@ __global__ void __launch_bounds__(256, 3) k_scan_flowcache(SRC src, uint32_t *__
     unsigned long long fc_hits = 0, fc_lookups = 0;
     uint32_t on_time = 0, late = 0;
 
-    uint64_t base = warp0 * 32;
-    typename SRC::Raw next;
-    src.load(next, base + lane, pol);
-    for (; base < nvec; base += step) {
+    if (lane == 0) {
+        for (int st = 0; st < SRC::kStages; st++) mbar_init(smem_u32(&mbar_s[wib][st]), 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncwarp();
+    // fill the ring
+    uint64_t issue_base = warp0 * 32;
+    if (lane == 0) {
+        for (int st = 0; st < SRC::kStages; st++) {
+            if (issue_base < nvec) {
+                const uint64_t left = nvec - issue_base;
+                src.stage_issue(smem_u32(stage_s[wib][st]), smem_u32(&mbar_s[wib][st]), issue_base,
+                                (uint32_t)(left < 32 ? left : 32), pol);
+            }
+            issue_base += step;
+        }
+    }
+    uint32_t slot = 0, parity = 0;
+    for (uint64_t base = warp0 * 32; base < nvec; base += step) {
+        mbar_wait(smem_u32(&mbar_s[wib][slot]), parity);
+        typename SRC::Raw raw;
+        src.stage_read(raw, stage_s[wib][slot], lane);
+        __syncwarp();
+        if (lane == 0) {  // the slot is free again: refill it with the trip kStages ahead
+            const uint64_t nb = base + (uint64_t)SRC::kStages * step;
+            if (nb < nvec) {
+                fence_proxy_async_smem();
+                const uint64_t left = nvec - nb;
+                src.stage_issue(smem_u32(stage_s[wib][slot]), smem_u32(&mbar_s[wib][slot]), nb,
+                                (uint32_t)(left < 32 ? left : 32), pol);
+            }
+        }
+        if (++slot == SRC::kStages) {
+            slot = 0;
+            parity ^= 1u;
+        }
         uint32_t cs[4], os[4];
         bool ok[4];
-        src.unpack(next, base + lane, cs, os, ok, on_time, late);
-        // request the next trip's packets now; they land while the table sets are in flight
-        src.load(next, base + step + lane, pol);
+        src.unpack(raw, base + lane, cs, os, ok, on_time, late);
 
         unsigned long long e[4][4];
         uint32_t set_idx[4], way_hint[4];
@@ -441,9 +559,7 @@ __global__ void __launch_bounds__(256, 3) k_scan_flowcache(SRC src, uint32_t *__
         for (int j = 0; j < 4; j++) {
             const uint64_t hh = mix64(p.state_h1 ^ (uint64_t)os[j]);
             const uint64_t hd = mix64(p.state_dh0 ^ (uint64_t)cs[j]);
-            // set index from the high halves of both hashes (their low bits feed h and d0);
-            // multiply-shift range reduction, so any set count works, not only powers of two
-            set_idx[j] = __umulhi((uint32_t)(hh >> 32) + (uint32_t)(hd >> 32) * 0x9E3779B1u, p.fc_sets);
+            set_idx[j] = fc_set_of(hh, hd, p.fc_sets);
             way_hint[j] = (uint32_t)(hd >> 30) & 3u;
             if (ok[j]) ld_fc_set(p.fcache + ((size_t)set_idx[j] << 2), e[j]);
         }

@@ -18,6 +18,7 @@ as (cand, opp) arrays.
 from __future__ import annotations
 
 import ctypes as C
+import sys
 from dataclasses import dataclass, field
 from typing import Callable, Iterable, Iterator, List, Optional
 
@@ -86,9 +87,10 @@ class WindowSession:
     """One open window: accepts batches until sealed, then restores (engine.py:57-103)."""
 
     def __init__(self, cfg: WindowConfig, window_id: int = 0, backend: str = "auto", pool=None,
-                 device: Optional[int] = None):
+                 device: Optional[int] = None, sketch: Optional[Dhla] = None):
         self.cfg = cfg
-        self.sketch = Dhla(cfg.dhg, backend=backend, window_id=window_id, device=device)
+        self.sketch = sketch if sketch is not None else Dhla(cfg.dhg, backend=backend, window_id=window_id,
+                                                             device=device)
         self.sealed = False
         self.pairs = 0
         self.dropped = 0
@@ -165,6 +167,7 @@ class DetectionEngine:
         self.backend = backend
         self.device = device
         self.chunk_records = max(4, (int(chunk_records) + 3) & ~3)
+        self._idle: List[Dhla] = []   # sketches nobody else holds any more, reset for reuse
 
     def run(self, records, on_sealed: Optional[Callable[[Dhla], None]] = None) -> List[WindowResult]:
         """Detect super points per tumbling window.
@@ -197,26 +200,25 @@ class DetectionEngine:
         n = host.size // RECORD_BYTES
         if n == 0:
             return
-        dev = torch.device("cuda", self._device_index())
+        dev_index = self._device_index()
+        dev = torch.device("cuda", dev_index)
         step = min(self.chunk_records, (n + 3) & ~3)
         bufs = [torch.empty(step * RECORD_BYTES, dtype=torch.uint8, device=dev) for _ in range(2 if n > step else 1)]
         copy_stream = torch.cuda.Stream(dev)
         ready = [torch.cuda.Event() for _ in bufs]
         consumed = [torch.cuda.Event() for _ in bufs]
-        import warnings
-
-        with warnings.catch_warnings():  # read-only host buffers (bytes, memmaps) are only ever read
-            warnings.simplefilter("ignore", UserWarning)
-            src = torch.from_numpy(host)
+        lib = _cabi.lib()
+        base = host.ctypes.data
 
         def start_copy(c):
             lo = c * step
             hi = min(n, lo + step)
             b = c % len(bufs)
-            with torch.cuda.stream(copy_stream):
-                copy_stream.wait_event(consumed[b])
-                bufs[b][: (hi - lo) * RECORD_BYTES].copy_(src[lo * RECORD_BYTES: hi * RECORD_BYTES], non_blocking=True)
-                ready[b].record(copy_stream)
+            copy_stream.wait_event(consumed[b])      # the scans of the chunk that used this buffer are done
+            _cabi.check(lib.dhsa_copy_to_device_async(
+                dev_index, C.c_void_p(bufs[b].data_ptr()), C.c_void_p(base + lo * RECORD_BYTES),
+                (hi - lo) * RECORD_BYTES, C.c_void_p(copy_stream.cuda_stream)))
+            ready[b].record(copy_stream)
             return hi - lo
 
         n_chunks = (n + step - 1) // step
@@ -225,7 +227,7 @@ class DetectionEngine:
             if c + 1 < n_chunks:
                 counts[c + 1] = start_copy(c + 1)
             b = c % len(bufs)
-            ready[b].synchronize()
+            torch.cuda.current_stream(dev).wait_event(ready[b])
             yield bufs[b][: counts[c] * RECORD_BYTES], counts[c]
             consumed[b].record(torch.cuda.current_stream(dev))
 
@@ -275,21 +277,35 @@ class DetectionEngine:
                     yield self._finish(session, on_sealed)
                     session = None
                 if session is None:
-                    session = WindowSession(cfg, wid, self.backend, device=self._device_index())
+                    session = WindowSession(cfg, wid, self.backend, device=self._device_index(),
+                                            sketch=self._take_idle(wid))
                     session.sketch.use_stream(torch.cuda.current_stream(session.sketch.device).cuda_stream)
                 session.feed_records(ptr, n, lo, hi)
         if session is not None:
             yield self._finish(session, on_sealed)
 
-    @staticmethod
-    def _finish(session: WindowSession, on_sealed) -> WindowResult:
+    def _take_idle(self, window_id: int) -> Optional[Dhla]:
+        if not self._idle:
+            return None
+        sk = self._idle.pop()
+        sk.reset(window_id=window_id)
+        return sk
+
+    def _finish(self, session: WindowSession, on_sealed) -> WindowResult:
         session.seal()
         if on_sealed is not None:
             on_sealed(session.sketch)
         reports = session.restore()
-        return WindowResult(
+        result = WindowResult(
             window_id=session.sketch.window_id,
             reports=reports,
             pairs=session.pairs,
             dropped=session.dropped,
         )
+        # Every window owns its sketch, as in the reference.  Allocating one costs milliseconds
+        # (cudaMalloc of the bits and the flow cache), so a sketch that nobody else kept a
+        # reference to (on_sealed may have) goes back to the idle list instead of being freed.
+        sk, session.sketch = session.sketch, None
+        if sys.getrefcount(sk) <= 2 and len(self._idle) < 2:
+            self._idle.append(sk)
+        return result

@@ -7,10 +7,10 @@ timeout 300 python __graft_entry__.py smoke > gpurun_out/smoke.log 2>&1; echo "s
 timeout 600 python bench.py --steps 5 --warmup 3 > gpurun_out/bench_${TAG}.json 2> gpurun_out/bench_${TAG}.err
 timeout 600 python bench.py --impl reference --steps 3 --warmup 1 > gpurun_out/bench_${TAG}_reference.json 2>> gpurun_out/bench_${TAG}.err
 for mode in test_agg test red; do
-  timeout 300 python bench.py --steps 5 --warmup 3 --scan-mode $mode --no-e2e --no-cpu-baseline > gpurun_out/bench_${TAG}_$mode.json 2>> gpurun_out/bench_${TAG}.err
+  timeout 300 python bench.py --steps 5 --warmup 3 --scan-mode $mode --no-e2e --no-cpu-baseline --no-records > gpurun_out/bench_${TAG}_$mode.json 2>> gpurun_out/bench_${TAG}.err
 done
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/launches_${TAG}.csv \
-   python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu-baseline --no-parity --no-probe > gpurun_out/ncu_launches.log 2>&1
+   python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu-baseline --no-parity --no-probe --no-records > gpurun_out/ncu_launches.log 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_scan_ -s 3 -c 1 -f -o gpurun_out/prof_scan_${TAG} \
-   python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu-baseline --no-parity --no-probe > gpurun_out/ncu_full.log 2>&1
+   python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu-baseline --no-parity --no-probe --no-records > gpurun_out/ncu_full.log 2>&1
 tail -3 gpurun_out/pytest_gpu.log; tail -2 gpurun_out/smoke.log; cat gpurun_out/bench_${TAG}.json gpurun_out/bench_${TAG}_reference.json; tail -2 gpurun_out/ncu_full.log
