@@ -459,13 +459,22 @@ struct FcMiss {
     uint32_t cand, opp, slot;  // slot = set * 4 + way to fill
 };
 
-// Set of a pair: from the high halves of the two hashes (their low bits feed h and d0),
-// multiply-shift range reduction so any set count works, not only powers of two.
+// Set (and victim way) of a pair from a 32-bit multiply-xorshift of (cand, opp): ~8 integer
+// instructions.  The sketch's own splitmix64 hashes (~90 instructions per packet) are computed
+// only for the packets that miss, in the drain -- ncu showed the front end issue-limited at 520
+// warp-instructions per 128 packets when it derived the set from them.  The table is a cache:
+// the index hash affects the hit rate, never the result.  Multiply-shift range reduction, so
+// any set count works, not only powers of two.
 // (A second-choice set probed on a miss was tried: hit rate 0.925 -> 0.953 at 64 MiB, but the
 // heavier drain made the scan 20% slower -- profiles/r01_flowcache_variants.txt.)
-__device__ __forceinline__ uint32_t fc_set_of(uint64_t hh, uint64_t hd, uint32_t n_sets)
+__device__ __forceinline__ uint32_t fc_hash32(uint32_t cand, uint32_t opp)
 {
-    return __umulhi((uint32_t)(hh >> 32) + (uint32_t)(hd >> 32) * 0x9E3779B1u, n_sets);
+    uint32_t z = (cand ^ 0x7F4A7C15u) * 0x9E3779B1u;
+    z ^= (opp + 0x165667B1u) * 0x85EBCA77u;
+    z ^= z >> 16;
+    z *= 0x7FEB352Du;
+    z ^= z >> 15;
+    return z;
 }
 
 // Drain up to 32 queued misses, one per lane: the R test loads of a lane are in flight
@@ -557,10 +566,9 @@ __global__ void __launch_bounds__(256, 3) k_scan_flowcache(SRC src, uint32_t *__
         uint32_t set_idx[4], way_hint[4];
 #pragma unroll
         for (int j = 0; j < 4; j++) {
-            const uint64_t hh = mix64(p.state_h1 ^ (uint64_t)os[j]);
-            const uint64_t hd = mix64(p.state_dh0 ^ (uint64_t)cs[j]);
-            set_idx[j] = fc_set_of(hh, hd, p.fc_sets);
-            way_hint[j] = (uint32_t)(hd >> 30) & 3u;
+            const uint32_t z = fc_hash32(cs[j], os[j]);
+            set_idx[j] = __umulhi(z, p.fc_sets);
+            way_hint[j] = z & 3u;
             if (ok[j]) ld_fc_set(p.fcache + ((size_t)set_idx[j] << 2), e[j]);
         }
 #pragma unroll
