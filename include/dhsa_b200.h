@@ -194,6 +194,28 @@ int dhsa_update_records_device(dhsa_sketch_t *s, const void *records_dev, uint64
                                uint32_t window_id, int direction);
 int dhsa_record_tally(dhsa_sketch_t *s, uint64_t *records_fed, uint64_t *records_dropped);
 
+/* ---- exact oracle on the GPU: ingest.exact_oracle (pkg/src/dhsa/ingest.py:159-176) -----------
+ * Exact number of distinct opposites per candidate host, by a hash set of whole pairs and
+ * per-host counters in HBM.  Evaluation tooling for windows too large for the reference's
+ * numpy sort/unique; results are exact, not estimates.
+ *   create   tables sized for about expected_pairs distinct pairs (grows by re-creation:
+ *            DHSA_ECAPACITY from add_* / result means "full, create a larger one")
+ *   add_*    insert pairs (device arrays) or raw IPPR records [rec_lo, rec_hi) of window
+ *            `window_id` under a direction policy, as dhsa_update_records_device selects them
+ *            (window_seconds 0 = no windowing: every record of the range)
+ *   result   hosts with count >= min_count, ascending by host */
+typedef struct dhsa_exact dhsa_exact_t;
+int dhsa_exact_create(int device, uint64_t expected_pairs, dhsa_exact_t **out);
+int dhsa_exact_destroy(dhsa_exact_t *e);
+int dhsa_exact_add_pairs(dhsa_exact_t *e, const uint32_t *cand_dev, const uint32_t *opp_dev, uint64_t n,
+                         void *cuda_stream);
+int dhsa_exact_add_records(dhsa_exact_t *e, const void *records_dev, uint64_t n_in_buffer,
+                           uint64_t rec_lo, uint64_t rec_hi, uint32_t window_seconds,
+                           uint32_t window_id, int direction, void *cuda_stream);
+int dhsa_exact_result(dhsa_exact_t *e, uint64_t min_count, uint64_t *hosts_host,
+                      uint64_t *counts_host, uint64_t cap, uint64_t *n_out,
+                      uint64_t *distinct_pairs, uint64_t *distinct_hosts, void *cuda_stream);
+
 /* Host -> device staging copy on a caller-chosen stream (cudaMemcpyAsync): DMA straight from
  * page-locked host memory, the driver's bounce buffers otherwise.  Lets the Python engine
  * stage numpy record buffers without routing them through another library. */

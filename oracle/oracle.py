@@ -338,6 +338,26 @@ def run_windows(records: np.ndarray, window_seconds: int, theta, direction: str 
     return out
 
 
+def exact_counts(records: np.ndarray, direction: str = "src") -> dict:
+    """Exact distinct-opposite count per candidate host (pkg/src/dhsa/ingest.py:159-176):
+    unique 64-bit (cand << 32 | opp) keys, then a count per candidate."""
+    if len(records) == 0:
+        return {}
+    src = records["src"].astype(np.uint64)
+    dst = records["dst"].astype(np.uint64)
+    if direction == "src":
+        cand, opp = src, dst
+    elif direction == "dst":
+        cand, opp = dst, src
+    elif direction == "both":
+        cand, opp = np.concatenate([src, dst]), np.concatenate([dst, src])
+    else:
+        raise ValueError(direction)
+    pairs = np.unique((cand << np.uint64(32)) | opp)
+    hosts, counts = np.unique(pairs >> np.uint64(32), return_counts=True)
+    return {int(h): int(c) for h, c in zip(hosts, counts)}
+
+
 def engine_trace(seed: int, n_noise: int = 90_000, window_seconds: int = 300):
     """A deterministic multi-window trace with late records, built from mix64 only (no
     library RNG): three and a half windows of background pairs in time order, three hosts

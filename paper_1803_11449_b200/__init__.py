@@ -18,6 +18,7 @@ from .dhla import (DEFAULT_MAX_CANDIDATES, Dhla, Estimate, SuperPointReport, hot
                    merge)
 from .engine import (DetectionEngine, TRACE_DTYPE, WindowConfig, WindowResult, WindowSession,
                      split_pairs)
+from .exact import EvalMetrics, ExactCounter, evaluate, exact_oracle
 from .snapshot import read_snapshot, write_snapshot
 from .errors import (CapacityError, ConfigError, CudaError, DataError, DhsaError,
                      SealedWindowError)
@@ -27,6 +28,6 @@ __version__ = "0.1.0"
 __all__ = [
     "DhgParams", "Dhla", "SuperPointReport", "Estimate", "merge", "hot_threshold",
     "DEFAULT_MAX_CANDIDATES", "DetectionEngine", "WindowConfig", "WindowResult", "WindowSession",
-    "split_pairs", "TRACE_DTYPE", "read_snapshot", "write_snapshot", "DhsaError", "ConfigError", "DataError", "CapacityError",
+    "split_pairs", "TRACE_DTYPE", "read_snapshot", "write_snapshot", "exact_oracle", "ExactCounter", "evaluate", "EvalMetrics", "DhsaError", "ConfigError", "DataError", "CapacityError",
     "SealedWindowError", "CudaError",
 ]

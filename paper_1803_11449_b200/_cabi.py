@@ -73,6 +73,11 @@ SIGNATURES = {
     "dhsa_plan_windows": [_vp, _vp, _u64, C.c_uint32, C.c_int64, _vp, C.c_uint32, C.POINTER(C.c_uint32)],
     "dhsa_update_records_device": [_vp, _vp, _u64, _u64, _u64, C.c_uint32, C.c_uint32, C.c_int],
     "dhsa_record_tally": [_vp, C.POINTER(_u64), C.POINTER(_u64)],
+    "dhsa_exact_create": [C.c_int, _u64, C.POINTER(_vp)],
+    "dhsa_exact_destroy": [_vp],
+    "dhsa_exact_add_pairs": [_vp, _vp, _vp, _u64, _vp],
+    "dhsa_exact_add_records": [_vp, _vp, _u64, _u64, _u64, C.c_uint32, C.c_uint32, C.c_int, _vp],
+    "dhsa_exact_result": [_vp, _u64, _vp, _vp, _u64, C.POINTER(_u64), C.POINTER(_u64), C.POINTER(_u64), _vp],
     "dhsa_copy_to_device_async": [C.c_int, _vp, _vp, _u64, _vp],
     "dhsa_or_merge": [_vp, _vp],
     "dhsa_or_merge_peers": [_vp, C.POINTER(_vp), C.c_int, _u64, _u64],

@@ -1220,6 +1220,183 @@ extern "C" int dhsa_ipc_close(int device, void *bits_dev)
     return DHSA_OK;
 }
 
+// ------------------------------------------------------------ exact oracle --
+
+struct dhsa_exact {
+    int device;
+    int sm_count;
+    ExactTables t;
+    uint64_t pair_cap, host_cap;
+    unsigned long long *out;      // collected (host << 32 | count) rows, padded to a power of two
+    uint64_t out_cap;
+    unsigned long long *n_out;    // device counter
+};
+
+static uint64_t pow2_ge(uint64_t v)
+{
+    uint64_t l = 1;
+    while (l < v) l <<= 1;
+    return l;
+}
+
+extern "C" int dhsa_exact_create(int device, uint64_t expected_pairs, dhsa_exact_t **out)
+{
+    NEED(out);
+    *out = nullptr;
+    CU(cudaSetDevice(device));
+    dhsa_exact *e = new (std::nothrow) dhsa_exact();
+    if (!e) return fail(-1, "out of host memory");
+    e->device = device;
+    CU(cudaDeviceGetAttribute(&e->sm_count, cudaDevAttrMultiProcessorCount, device));
+    e->pair_cap = pow2_ge(2 * (expected_pairs < 1024 ? 1024 : expected_pairs));  // load factor <= 0.5
+    e->host_cap = e->pair_cap;
+    cudaError_t err = cudaMalloc(&e->t.pairs, e->pair_cap * 8);
+    if (err == cudaSuccess) err = cudaMalloc(&e->t.hosts, e->host_cap * 8);
+    if (err == cudaSuccess) err = cudaMalloc(&e->t.header, 8 * 8);
+    if (err == cudaSuccess) err = cudaMalloc(&e->n_out, 8);
+    if (err == cudaSuccess) err = cudaMemset(e->t.pairs, 0, e->pair_cap * 8);
+    if (err == cudaSuccess) err = cudaMemset(e->t.hosts, 0, e->host_cap * 8);
+    if (err == cudaSuccess) err = cudaMemset(e->t.header, 0, 8 * 8);
+    if (err != cudaSuccess) {
+        cudaFree(e->t.pairs), cudaFree(e->t.hosts), cudaFree(e->t.header), cudaFree(e->n_out);
+        delete e;
+        return cuda_fail(err, "exact oracle tables");
+    }
+    e->t.pair_mask = e->pair_cap - 1;
+    e->t.host_mask = e->host_cap - 1;
+    *out = e;
+    return DHSA_OK;
+}
+
+extern "C" int dhsa_exact_destroy(dhsa_exact_t *e)
+{
+    if (!e) return DHSA_OK;
+    cudaSetDevice(e->device);
+    cudaDeviceSynchronize();
+    cudaFree(e->t.pairs), cudaFree(e->t.hosts), cudaFree(e->t.header), cudaFree(e->n_out), cudaFree(e->out);
+    delete e;
+    return DHSA_OK;
+}
+
+static int exact_grid(const dhsa_exact *e, uint64_t nvec)
+{
+    uint64_t want = (nvec + 255) / 256, cap = (uint64_t)e->sm_count * 8;
+    if (want < 1) want = 1;
+    return (int)(want < cap ? want : cap);
+}
+
+extern "C" int dhsa_exact_add_pairs(dhsa_exact_t *e, const uint32_t *cand_dev, const uint32_t *opp_dev, uint64_t n,
+                                    void *cuda_stream)
+{
+    NEED(e);
+    if (n == 0) return DHSA_OK;
+    NEED(cand_dev);
+    NEED(opp_dev);
+    if (((uintptr_t)cand_dev | (uintptr_t)opp_dev) & 15u || (n & 3u))
+        return fail(DHSA_ECONFIG, "exact oracle input must be 16-byte aligned arrays of a multiple of 4 pairs");
+    CU(cudaSetDevice(e->device));
+    SoaSource src;
+    src.cand4 = reinterpret_cast<const uint4 *>(cand_dev);
+    src.opp4 = reinterpret_cast<const uint4 *>(opp_dev);
+    src.nvec = n / 4;
+    k_exact_insert<SoaSource><<<exact_grid(e, src.nvec), 256, 0, (cudaStream_t)cuda_stream>>>(src, e->t);
+    CU(cudaGetLastError());
+    return DHSA_OK;
+}
+
+extern "C" int dhsa_exact_add_records(dhsa_exact_t *e, const void *records_dev, uint64_t n_in_buffer, uint64_t rec_lo,
+                                      uint64_t rec_hi, uint32_t window_seconds, uint32_t window_id, int direction,
+                                      void *cuda_stream)
+{
+    NEED(e);
+    if (rec_lo >= rec_hi) return DHSA_OK;
+    NEED(records_dev);
+    if (rec_hi > n_in_buffer) return fail(DHSA_EDATA, "record range exceeds the buffer");
+    if (direction < 0 || direction > 2) return fail(DHSA_ECONFIG, "direction must be 0 (src), 1 (dst) or 2 (both)");
+    if (((uintptr_t)records_dev & 15u) || (n_in_buffer & 3u))
+        return fail(DHSA_ECONFIG, "exact oracle record buffers must be 16-byte aligned and hold a multiple of 4 records");
+    CU(cudaSetDevice(e->device));
+    for (int pass = 0; pass < 2; pass++) {
+        if ((pass == 0 && direction == 1) || (pass == 1 && direction == 0)) continue;
+        RecordSource src;
+        const uint64_t q_lo = rec_lo / 4, q_hi = (rec_hi + 3) / 4;
+        src.rec4 = reinterpret_cast<const uint4 *>(records_dev) + 3 * q_lo;
+        src.nquads = q_hi - q_lo;
+        src.first_rec = 4 * q_lo;
+        src.rec_lo = rec_lo, src.rec_hi = rec_hi;
+        src.window_seconds = window_seconds, src.window_id = window_id;
+        src.cand_is_dst = pass;
+        src.tally = nullptr, src.tally_late = 0;
+        k_exact_insert<RecordSource><<<exact_grid(e, src.nquads), 256, 0, (cudaStream_t)cuda_stream>>>(src, e->t);
+    }
+    CU(cudaGetLastError());
+    return DHSA_OK;
+}
+
+extern "C" int dhsa_exact_result(dhsa_exact_t *e, uint64_t min_count, uint64_t *hosts_host, uint64_t *counts_host,
+                                 uint64_t cap, uint64_t *n_out, uint64_t *distinct_pairs, uint64_t *distinct_hosts,
+                                 void *cuda_stream)
+{
+    NEED(e);
+    NEED(n_out);
+    *n_out = 0;
+    CU(cudaSetDevice(e->device));
+    cudaStream_t st = (cudaStream_t)cuda_stream;
+    unsigned long long header[8];
+    CU(cudaMemcpyAsync(header, e->t.header, sizeof header, cudaMemcpyDeviceToHost, st));
+    CU(cudaStreamSynchronize(st));
+    if (header[2]) return fail(DHSA_ECAPACITY, "exact oracle tables are full (%llu slots); create a larger one",
+                               (unsigned long long)e->pair_cap);
+    if (distinct_pairs) *distinct_pairs = header[0];
+    if (distinct_hosts) *distinct_hosts = header[1];
+    const uint64_t want = pow2_ge(header[1] + 1);
+    if (want > e->out_cap) {
+        cudaFree(e->out);
+        e->out = nullptr, e->out_cap = 0;
+        CU(cudaMalloc(&e->out, want * 8));
+        e->out_cap = want;
+    }
+    CU(cudaMemsetAsync(e->n_out, 0, 8, st));
+    k_exact_collect<<<exact_grid(e, e->host_cap), 256, 0, st>>>(e->t, min_count, e->out, e->out_cap, e->n_out);
+    unsigned long long n = 0;
+    CU(cudaMemcpyAsync(&n, e->n_out, 8, cudaMemcpyDeviceToHost, st));
+    CU(cudaStreamSynchronize(st));
+    *n_out = n;
+    if (n == 0) return DHSA_OK;
+    if (n > cap) return fail(DHSA_EDATA, "%llu hosts exceed the output capacity %llu", n, (unsigned long long)cap);
+    NEED(hosts_host);
+    NEED(counts_host);
+    // ascending by host: the packed rows sort as integers
+    if (n <= DHSA_SORT_SMEM_MAX) {
+        CU(cudaFuncSetAttribute(k_sort_small, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                DHSA_SORT_SMEM_MAX * (int)sizeof(uint64_t)));
+        k_sort_small<<<1, 1024, DHSA_SORT_SMEM_MAX * sizeof(uint64_t), st>>>(
+            reinterpret_cast<uint64_t *>(e->out), e->n_out, nullptr);
+    } else {
+        const uint64_t len = pow2_ge(n);
+        const int grid = exact_grid(e, len);
+        k_sort_pad<<<grid, 256, 0, st>>>(reinterpret_cast<uint64_t *>(e->out), n, len);
+        for (uint64_t kk = 2; kk <= len; kk <<= 1)
+            for (uint64_t j = kk >> 1; j > 0; j >>= 1)
+                k_bitonic_pass<<<grid, 256, 0, st>>>(reinterpret_cast<uint64_t *>(e->out), len, kk, j);
+    }
+    CU(cudaGetLastError());
+    unsigned long long *rows = (unsigned long long *)malloc(n * 8);
+    if (!rows) return fail(-1, "out of host memory");
+    cudaError_t err = cudaMemcpyAsync(rows, e->out, n * 8, cudaMemcpyDeviceToHost, st);
+    if (err == cudaSuccess) err = cudaStreamSynchronize(st);
+    if (err != cudaSuccess) {
+        free(rows);
+        return cuda_fail(err, "exact oracle readback");
+    }
+    for (uint64_t i = 0; i < n; i++) {
+        hosts_host[i] = rows[i] >> 32;
+        counts_host[i] = rows[i] & 0xFFFFFFFFull;
+    }
+    free(rows);
+    return DHSA_OK;
+}
+
 // ----------------------------------------------------------------- probes --
 
 extern "C" int dhsa_probe_l2(int device, int kind, uint64_t buffer_bytes, uint64_t ops, double *ops_per_sec)

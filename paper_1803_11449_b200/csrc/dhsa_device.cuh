@@ -347,7 +347,8 @@ struct RecordSource {
             const uint32_t ts = w[3 * j];
             const uint32_t src = __byte_perm(w[3 * j + 1], 0, 0x0123);  // network order -> host order
             const uint32_t dst = __byte_perm(w[3 * j + 2], 0, 0x0123);
-            const bool fresh = mine && (ts / window_seconds) == window_id;
+            // window_seconds == 0: no windowing, every record of the range is taken (exact oracle over a whole trace)
+            const bool fresh = mine && (window_seconds == 0u || (ts / window_seconds) == window_id);
             cs[j] = cand_is_dst ? dst : src;
             os[j] = cand_is_dst ? src : dst;
             ok[j] = fresh;
@@ -1264,7 +1265,7 @@ __global__ void __launch_bounds__(1024) k_sort_small(uint64_t *__restrict__ data
         }
     }
     for (uint32_t t = threadIdx.x; t < n; t += blockDim.x) data[t] = sm[t];
-    if (threadIdx.x == 0) ctl->sorted = 1;
+    if (threadIdx.x == 0 && ctl) ctl->sorted = 1;
 }
 
 __global__ void __launch_bounds__(256) k_sort_pad(uint64_t *__restrict__ data, uint64_t n, uint64_t len)
@@ -1330,6 +1331,121 @@ __global__ void __launch_bounds__(256) k_copy_slice(uint4 *__restrict__ dst, con
                      : "=r"(x.x), "=r"(x.y), "=r"(x.z), "=r"(x.w)
                      : "l"(src + v));
         dst[v] = x;
+    }
+}
+
+// ------------------------------------------------- exact oracle on the GPU --
+// exact_oracle (pkg/src/dhsa/ingest.py:159-176): the exact number of distinct opposites of
+// every candidate host, the ground truth FPR / FNR are scored against.  The reference sorts
+// and uniques 64-bit (cand << 32 | opp) keys with numpy; at 10^8..10^9 packets that is minutes.
+// Here: an open-addressing hash set of whole pairs (linear probing, 64-bit atomicCAS); the
+// lane that wins a pair's insertion bumps its candidate's counter in a second open-addressing
+// table keyed by the candidate.  Both tables store key + 1 so that 0 means empty (pair
+// 0xFFFFFFFF'FFFFFFFF and host 0xFFFFFFFF are tracked in two dedicated slots of the header).
+struct ExactTables {
+    unsigned long long *pairs;  // pair_cap slots
+    unsigned long long pair_mask;
+    unsigned long long *hosts;  // host_cap slots: (host + 1) << 32 | count
+    unsigned long long host_mask;
+    unsigned long long *header;  // [0] distinct pairs, [1] distinct hosts, [2] overflow flag,
+                                 // [3] all-ones pair seen, [4] count of host 0xFFFFFFFF
+};
+
+__device__ __forceinline__ void exact_bump_host(const ExactTables &t, uint32_t host)
+{
+    if (host == 0xFFFFFFFFu) {
+        if (atomicAdd(t.header + 4, 1ull) == 0ull) atomicAdd(t.header + 1, 1ull);
+        return;
+    }
+    const unsigned long long tag = ((unsigned long long)host + 1ull) << 32;
+    unsigned long long slot = mix64((unsigned long long)host) & t.host_mask;
+    for (unsigned long long probes = 0; probes <= t.host_mask; probes++, slot = (slot + 1) & t.host_mask) {
+        unsigned long long cur = t.hosts[slot];
+        if (cur == 0ull) {
+            const unsigned long long prev = atomicCAS(t.hosts + slot, 0ull, tag | 1ull);
+            if (prev == 0ull) {
+                atomicAdd(t.header + 1, 1ull);
+                return;
+            }
+            cur = prev;
+        }
+        if ((cur >> 32) == (tag >> 32)) {
+            atomicAdd(t.hosts + slot, 1ull);  // count lives in the low 32 bits (< 2^32 distinct opposites)
+            return;
+        }
+    }
+    atomicExch(t.header + 2, 1ull);  // table full
+}
+
+template <typename SRC>
+__global__ void __launch_bounds__(256) k_exact_insert(SRC src, ExactTables t)
+{
+    const uint32_t lane = threadIdx.x & 31u;
+    const uint64_t nvec = src.vectors();
+    const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+    const uint64_t warp0 = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const uint64_t pol = policy_evict_first();
+    uint32_t on_time = 0, late = 0;
+    for (uint64_t base = warp0 * 32; base < nvec; base += nwarps * 32) {
+        const uint64_t v = base + lane;
+        typename SRC::Raw raw;
+        src.load(raw, v, pol);
+        uint32_t cs[4], os[4];
+        bool ok[4];
+        src.unpack(raw, v, cs, os, ok, on_time, late);
+#pragma unroll
+        for (int j = 0; j < 4; j++) {
+            if (!ok[j]) continue;
+            const unsigned long long key = ((unsigned long long)cs[j] << 32) | (unsigned long long)os[j];
+            if (key == ~0ull) {
+                if (atomicExch(t.header + 3, 1ull) == 0ull) {
+                    atomicAdd(t.header + 0, 1ull);
+                    exact_bump_host(t, cs[j]);
+                }
+                continue;
+            }
+            const unsigned long long stored = key + 1ull;
+            unsigned long long slot = mix64(key) & t.pair_mask;
+            bool placed = false;
+            for (unsigned long long probes = 0; probes <= t.pair_mask; probes++, slot = (slot + 1) & t.pair_mask) {
+                unsigned long long cur = t.pairs[slot];
+                if (cur == 0ull) {
+                    cur = atomicCAS(t.pairs + slot, 0ull, stored);
+                    if (cur == 0ull) {  // this lane inserted the pair: one more distinct opposite of cs[j]
+                        atomicAdd(t.header + 0, 1ull);
+                        exact_bump_host(t, cs[j]);
+                        placed = true;
+                        break;
+                    }
+                }
+                if (cur == stored) {
+                    placed = true;
+                    break;
+                }
+            }
+            if (!placed) atomicExch(t.header + 2, 1ull);
+        }
+    }
+}
+
+// Hosts with at least min_count distinct opposites -> (host, count) rows, unordered.
+__global__ void __launch_bounds__(256) k_exact_collect(ExactTables t, unsigned long long min_count,
+                                                       unsigned long long *__restrict__ out, unsigned long long cap,
+                                                       unsigned long long *__restrict__ n_out)
+{
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t slot = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; slot <= t.host_mask; slot += stride) {
+        const unsigned long long cur = t.hosts[slot];
+        if (cur == 0ull) continue;
+        const unsigned long long count = cur & 0xFFFFFFFFull, host = (cur >> 32) - 1ull;
+        if (count >= min_count) {
+            const unsigned long long pos = atomicAdd(n_out, 1ull);
+            if (pos < cap) out[pos] = (host << 32) | count;  // sorts by host
+        }
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0 && t.header[4] >= min_count && t.header[4] > 0) {
+        const unsigned long long pos = atomicAdd(n_out, 1ull);
+        if (pos < cap) out[pos] = (0xFFFFFFFFull << 32) | (t.header[4] & 0xFFFFFFFFull);
     }
 }
 

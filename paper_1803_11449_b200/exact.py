@@ -1,0 +1,165 @@
+"""Exact ground truth and accuracy metrics on the device (evaluation tooling).
+
+``exact_oracle`` is the reference's brute-force counter
+(/root/reference/pkg/src/dhsa/ingest.py:159-176) -- exact distinct-opposite count per
+candidate host -- built as a hash set of whole pairs in HBM (csrc ``k_exact_insert``), so a
+10^8..10^9-packet window can be scored in milliseconds instead of the minutes numpy's
+sort/unique takes.  ``evaluate`` mirrors ``ingest.evaluate`` (ingest.py:179-233); it is a few
+set operations on the report list and stays on the host.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+from typing import Dict, Optional, Sequence
+
+import numpy as np
+
+from . import _cabi
+from .engine import DIRECTIONS, RECORD_BYTES, _as_record_bytes
+from .errors import CapacityError, ConfigError
+
+
+class ExactCounter:
+    """Accumulates pairs on one device; ``result`` returns exact per-host distinct counts."""
+
+    def __init__(self, expected_pairs: int = 1 << 22, device: Optional[int] = None):
+        from .dhla import _default_device
+
+        self.device = _default_device() if device is None else int(device)
+        self.expected_pairs = int(expected_pairs)
+        self._lib = _cabi.lib()
+        self._h = C.c_void_p()
+        _cabi.check(self._lib.dhsa_exact_create(self.device, self.expected_pairs, C.byref(self._h)))
+
+    def __del__(self):
+        h, self._h = getattr(self, "_h", None), None
+        if h:
+            try:
+                self._lib.dhsa_exact_destroy(h)
+            except Exception:
+                pass
+
+    def _stream(self) -> int:
+        import torch
+
+        return torch.cuda.current_stream(self.device).cuda_stream
+
+    def add_pairs(self, cand, opp) -> None:
+        """torch CUDA tensors of 32-bit integers (any length; padded internally to 4)."""
+        import torch
+
+        if cand.numel() != opp.numel():
+            raise ValueError("candidate and opposite arrays differ in length")
+        n = cand.numel()
+        if n == 0:
+            return
+        if n % 4 or cand.data_ptr() % 16 or opp.data_ptr() % 16 or not cand.is_contiguous() or not opp.is_contiguous():
+            pad = (-n) % 4  # repeat the last pair: duplicates do not change a distinct count
+            cand = torch.cat([cand.reshape(-1), cand.reshape(-1)[-1:].expand(pad)]).contiguous()
+            opp = torch.cat([opp.reshape(-1), opp.reshape(-1)[-1:].expand(pad)]).contiguous()
+            n += pad
+        _cabi.check(self._lib.dhsa_exact_add_pairs(self._h, C.c_void_p(cand.data_ptr()), C.c_void_p(opp.data_ptr()),
+                                                   n, C.c_void_p(self._stream())))
+
+    def add_records(self, raw_dev, direction: str = "src", window_seconds: int = 0, window_id: int = 0,
+                    lo: int = 0, hi: Optional[int] = None) -> None:
+        """Raw 12-byte records on the device (uint8 tensor).  window_seconds 0 = whole trace."""
+        import torch
+
+        if direction not in DIRECTIONS:
+            raise ConfigError(f"direction must be src, dst, or both (got {direction!r})")
+        flat = raw_dev.reshape(-1)
+        n = flat.numel() // RECORD_BYTES
+        hi = n if hi is None else hi
+        if n % 4 or flat.data_ptr() % 16:
+            pad = (-n) % 4
+            flat = torch.cat([flat, flat.new_zeros(pad * RECORD_BYTES)]).contiguous()
+        _cabi.check(self._lib.dhsa_exact_add_records(
+            self._h, C.c_void_p(flat.data_ptr()), flat.numel() // RECORD_BYTES, lo, hi, window_seconds, window_id,
+            DIRECTIONS.index(direction), C.c_void_p(self._stream())))
+        torch.cuda.current_stream(self.device).synchronize()  # `flat` may be a temporary
+
+    def result(self, min_count: int = 1):
+        """(hosts uint64 ascending, counts uint64, distinct pairs, distinct hosts)."""
+        n, pairs, hosts_n = C.c_uint64(), C.c_uint64(), C.c_uint64()
+        cap = 1 << 16
+        while True:
+            hosts = np.empty(cap, dtype=np.uint64)
+            counts = np.empty(cap, dtype=np.uint64)
+            rc = self._lib.dhsa_exact_result(self._h, int(min_count), hosts.ctypes.data, counts.ctypes.data, cap,
+                                             C.byref(n), C.byref(pairs), C.byref(hosts_n), C.c_void_p(self._stream()))
+            if rc == 3 and n.value > cap:
+                cap = int(n.value)
+                continue
+            _cabi.check(rc)
+            k = int(n.value)
+            return hosts[:k].copy(), counts[:k].copy(), int(pairs.value), int(hosts_n.value)
+
+
+def exact_oracle(records, direction: str = "src", device: Optional[int] = None, min_count: int = 1) -> Dict[int, int]:
+    """Exact distinct-opposite count per candidate host (ingest.py:159-176).
+
+    ``records``: TRACE_DTYPE array, raw record bytes, or a uint8 torch CUDA tensor of raw records."""
+    import torch
+
+    if direction not in DIRECTIONS:
+        raise ConfigError(f"direction must be src, dst, or both (got {direction!r})")
+    if hasattr(records, "is_cuda") and records.is_cuda:
+        raw = records.reshape(-1)
+        dev_index = raw.device.index
+    else:
+        host = _as_record_bytes(records)
+        if host.size == 0:
+            return {}
+        from .dhla import _default_device
+
+        dev_index = _default_device() if device is None else int(device)
+        raw = torch.from_numpy(np.array(host, copy=True)).to(f"cuda:{dev_index}")
+    n = raw.numel() // RECORD_BYTES
+    if n == 0:
+        return {}
+    expected = max(1 << 16, n * (2 if direction == "both" else 1) // 4)
+    while True:
+        counter = ExactCounter(expected, device=dev_index)
+        counter.add_records(raw, direction)
+        try:
+            hosts, counts, _, _ = counter.result(min_count)
+        except CapacityError:
+            expected *= 4       # more distinct pairs than planned for: rebuild larger
+            continue
+        return {int(h): int(c) for h, c in zip(hosts.tolist(), counts.tolist())}
+
+
+@dataclass
+class EvalMetrics:  # ingest.py:179-213
+    n_true: int
+    n_reported: int
+    n_false_pos: int
+    n_false_neg: int
+    fpr: Optional[float]
+    fnr: Optional[float]
+    tfr: Optional[float]
+    mean_rel_err: Optional[float]
+
+    def as_dict(self) -> dict:
+        return {"N": self.n_true, "N_reported": self.n_reported, "N_false_pos": self.n_false_pos,
+                "N_false_neg": self.n_false_neg, "fpr": self.fpr, "fnr": self.fnr, "tfr": self.tfr,
+                "mean_rel_err": self.mean_rel_err}
+
+
+def evaluate(reports: Sequence, truth: Dict[int, int], theta: int) -> EvalMetrics:
+    """Score a report list against exact per-host counts (ingest.py:216-233)."""
+    true_supers = {h for h, c in truth.items() if c >= theta}
+    reported = {rep.host for rep in reports}
+    n = len(true_supers)
+    n_fp = len(reported - true_supers)
+    n_fn = len(true_supers - reported)
+    rel = [abs(rep.estimate - truth[rep.host]) / truth[rep.host] for rep in reports if rep.host in true_supers]
+    mean_rel = sum(rel) / len(rel) if rel else None
+    if n == 0:
+        return EvalMetrics(0, len(reported), n_fp, 0, None, None, None, mean_rel)
+    fpr = n_fp / n
+    fnr = n_fn / n
+    return EvalMetrics(n, len(reported), n_fp, n_fn, fpr, fnr, fpr + fnr, mean_rel)

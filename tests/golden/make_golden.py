@@ -245,6 +245,22 @@ def main():
                                      for r in res]))
     with open(os.path.join(HERE, "engine_cases.json"), "w") as fh:
         json.dump(eng, fh, indent=1)
+    # exact oracle + metrics (row N3): the reference's ingest.exact_oracle / evaluate on the engine trace
+    from dhsa.ingest import evaluate as ref_evaluate, exact_oracle as ref_exact
+    from dhsa.dhla import SuperPointReport as RefReport
+    ex = []
+    trace = O.engine_trace(9)
+    for direction in ("src", "dst", "both"):
+        truth = ref_exact(trace, direction)
+        top = sorted(truth.items(), key=lambda kv: (-kv[1], kv[0]))[:8]
+        fake = [RefReport(h, c * 1.05, False) for h, c in top[:3]] + [RefReport(12345, 2000.0, False)]
+        ex.append(dict(seed=9, direction=direction, n_hosts=len(truth), n_pairs=int(sum(truth.values())),
+                       hosts_sha256=sha(np.array(sorted(truth), dtype=np.uint64)),
+                       counts_sha256=sha(np.array([truth[h] for h in sorted(truth)], dtype=np.uint64)),
+                       top=[[int(h), int(c)] for h, c in top],
+                       metrics=ref_evaluate(fake, truth, 1024).as_dict()))
+    with open(os.path.join(HERE, "exact_cases.json"), "w") as fh:
+        json.dump(ex, fh, indent=1)
     print("wrote", sorted(os.listdir(HERE)))
 
 

@@ -1,0 +1,84 @@
+"""Row N3: the exact oracle on the GPU and the accuracy metrics, against the reference's
+ingest.exact_oracle / evaluate (tests/golden/exact_cases.json) and the oracle's restatement."""
+import hashlib
+from types import SimpleNamespace
+
+import numpy as np
+import pytest
+
+import paper_1803_11449_b200 as P
+from oracle import oracle as O
+
+from helpers import load_json
+
+pytestmark = pytest.mark.gpu
+EXACT_CASES = load_json("exact_cases.json")
+
+
+def sha(a):
+    return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()
+
+
+@pytest.mark.parametrize("case", EXACT_CASES, ids=[c["direction"] for c in EXACT_CASES])
+def test_exact_oracle_matches_reference(case):
+    trace = O.engine_trace(case["seed"])
+    truth = P.exact_oracle(trace, case["direction"])
+    assert len(truth) == case["n_hosts"] and sum(truth.values()) == case["n_pairs"]
+    assert sha(np.array(sorted(truth), dtype=np.uint64)) == case["hosts_sha256"]
+    assert sha(np.array([truth[h] for h in sorted(truth)], dtype=np.uint64)) == case["counts_sha256"]
+    top = sorted(truth.items(), key=lambda kv: (-kv[1], kv[0]))[:8]
+    assert [[h, c] for h, c in top] == case["top"]
+    fake = [SimpleNamespace(host=h, estimate=c * 1.05, saturated=False) for h, c in top[:3]]
+    fake.append(SimpleNamespace(host=12345, estimate=2000.0, saturated=False))
+    got = P.evaluate(fake, truth, 1024).as_dict()
+    for key, want in case["metrics"].items():
+        assert got[key] == (pytest.approx(want) if isinstance(want, float) else want)
+
+
+def test_exact_counter_edge_cases_and_growth():
+    import torch
+
+    assert P.exact_oracle(np.empty(0, dtype=P.TRACE_DTYPE)) == {}
+    # the all-ones pair and host, duplicates, ragged length, a table that must grow
+    cand = np.array([0xFFFFFFFF, 0xFFFFFFFF, 0xFFFFFFFF, 5, 5, 5, 0], dtype=np.uint32)
+    opp = np.array([0xFFFFFFFF, 0xFFFFFFFF, 1, 9, 9, 10, 0], dtype=np.uint32)
+    c = P.ExactCounter(expected_pairs=4)
+    c.add_pairs(torch.from_numpy(cand.view(np.int32)).cuda(), torch.from_numpy(opp.view(np.int32)).cuda())
+    hosts, counts, pairs, nh = c.result()
+    assert hosts.tolist() == [0, 5, 0xFFFFFFFF] and counts.tolist() == [1, 2, 2] and pairs == 5 and nh == 3
+    assert c.result(min_count=2)[0].tolist() == [5, 0xFFFFFFFF]
+    big_c, big_o = O.distinct_pairs(300_000, 4)
+    rec = np.empty(len(big_c), dtype=P.TRACE_DTYPE)
+    rec["ts"], rec["src"], rec["dst"] = 0, big_c, big_o
+    want = O.exact_counts(rec, "both")
+    got = P.exact_oracle(rec, "both")     # starts with too small a table for 600k pairs, grows
+    assert got == want
+
+
+def test_exact_oracle_scores_a_100m_packet_window():
+    """FPR / FNR of the detector at BASELINE config-2 size, with GPU ground truth."""
+    import torch
+
+    rng = np.random.default_rng(3)
+    hosts = np.unique(rng.integers(0, 2 ** 32, size=120_064, dtype=np.uint64))[:120_050].astype(np.uint32)
+    rng.shuffle(hosts)
+    cards = np.concatenate([np.minimum(rng.zipf(1.5, size=120_000), 256), rng.integers(2048, 8193, size=50)])
+    src = np.repeat(hosts, cards)
+    dst = rng.integers(0, 2 ** 32, size=len(src), dtype=np.uint64).astype(np.uint32)
+    pick = torch.randint(0, len(src), (100_000_000,), device="cuda")
+    pick[: len(src)] = torch.arange(len(src), device="cuda")
+    ct = torch.from_numpy(src.view(np.int32)).cuda()[pick]
+    ot = torch.from_numpy(dst.view(np.int32)).cuda()[pick]
+    counter = P.ExactCounter(expected_pairs=len(src))
+    counter.add_pairs(ct, ot)
+    h, c, n_pairs, n_hosts = counter.result(min_count=1024)
+    # ground truth by construction: distinct (src, dst) pairs per host
+    flows = np.unique((src.astype(np.uint64) << np.uint64(32)) | dst.astype(np.uint64))
+    th, tc = np.unique(flows >> np.uint64(32), return_counts=True)
+    assert n_pairs == len(flows) and n_hosts == len(th)
+    keep = tc >= 1024
+    assert h.tolist() == th[keep].tolist() and c.tolist() == tc[keep].tolist()
+    sk = P.Dhla(P.DhgParams())
+    sk.update_batch(ct, ot)
+    m = P.evaluate(sk.restore_superpoints(1024), dict(zip(h.tolist(), c.tolist())), 1024)
+    assert m.n_true == 50 and m.fnr == 0.0 and m.fpr <= 0.05 and m.mean_rel_err <= 0.10   # SPEC C5 bounds

@@ -223,3 +223,14 @@ def test_engine_oracle_matches_reference_engine_fixture(case):
         assert [(r.host, r.saturated) for r in reps] == [(h, s) for h, _, s in w["reports"]]
         for r, (_, e, _) in zip(reps, w["reports"]):
             assert r.estimate == pytest.approx(e, rel=1e-12)
+
+
+EXACT_CASES = load_json("exact_cases.json")
+
+
+@pytest.mark.parametrize("case", EXACT_CASES, ids=[c["direction"] for c in EXACT_CASES])
+def test_exact_counts_oracle_matches_reference_fixture(case):
+    truth = O.exact_counts(O.engine_trace(case["seed"]), case["direction"])
+    assert len(truth) == case["n_hosts"] and sum(truth.values()) == case["n_pairs"]
+    assert sha(np.array(sorted(truth), dtype=np.uint64)) == case["hosts_sha256"]
+    assert sha(np.array([truth[h] for h in sorted(truth)], dtype=np.uint64)) == case["counts_sha256"]
