@@ -216,6 +216,19 @@ int dhsa_exact_result(dhsa_exact_t *e, uint64_t min_count, uint64_t *hosts_host,
                       uint64_t *counts_host, uint64_t cap, uint64_t *n_out,
                       uint64_t *distinct_pairs, uint64_t *distinct_hosts, void *cuda_stream);
 
+/* ---- synthetic trace generator on the device: ingest.generate_trace's per-record half
+ * (pkg/src/dhsa/ingest.py:128-151).  hosts / prefix / bases describe the flow population
+ * (n_hosts distinct addresses, exclusive prefix sums of their cardinalities with
+ * prefix[n_hosts] = flows, first destination of each host's ramp); the call writes output
+ * positions [p_lo, p_hi) of the shuffled, time-ordered stream of flows * dup packets as 12-byte
+ * IPPR records and/or (cand, opp) uint32 arrays (null = not wanted).  A rank of a multi-GPU
+ * window generates only its own slice. */
+int dhsa_generate_trace(int device, const uint32_t *hosts_dev, const uint64_t *prefix_dev,
+                        const uint32_t *bases_dev, uint32_t n_hosts, uint64_t flows, uint64_t dup,
+                        uint64_t seed, uint32_t start_ts, uint32_t window_seconds, uint64_t p_lo,
+                        uint64_t p_hi, void *records_out_dev, uint32_t *cand_out_dev,
+                        uint32_t *opp_out_dev, void *cuda_stream);
+
 /* Host -> device staging copy on a caller-chosen stream (cudaMemcpyAsync): DMA straight from
  * page-locked host memory, the driver's bounce buffers otherwise.  Lets the Python engine
  * stage numpy record buffers without routing them through another library. */

@@ -358,6 +358,88 @@ def exact_counts(records: np.ndarray, direction: str = "src") -> dict:
     return {int(h): int(c) for h, c in zip(hosts, counts)}
 
 
+def _fmix32_many(x):
+    x = x.astype(np.uint32, copy=True)
+    with np.errstate(over="ignore"):
+        x ^= x >> np.uint32(16)
+        x *= np.uint32(0x85EBCA6B)
+        x ^= x >> np.uint32(13)
+        x *= np.uint32(0xC2B2AE35)
+        x ^= x >> np.uint32(16)
+    return x
+
+
+def generate_trace_spec(background_hosts=0, background_max_cardinality=256, background_zipf=1.5, superpoints=0,
+                        super_cardinality=(2048, 8192), duplicate_factor=1, start_ts=0, window_seconds=300, seed=0):
+    """numpy restatement of the device generator's definition (paper_1803_11449_b200/traces.py,
+    csrc k_generate_trace), which follows the reference generator's semantics
+    (pkg/src/dhsa/ingest.py:109-153) over a counter-based random source:
+
+      hosts[i]   fmix32(i ^ low32(mix64(seed ^ TAG_HOST)))            distinct (bijection)   ingest.py:121
+      cards[i]   background: 1 + #{k : floor(2^53 P(zipf<=k)) <= u_i >> 11}, capped          ingest.py:123-126
+                 super: lo + u_i mod (hi - lo + 1), u_i = mix64(i + (seed ^ TAG_CARD))       ingest.py:127-129
+      dst        bases[h] + offset within the host (mod 2^32): distinct per host             ingest.py:131-137
+      position p record perm(p) mod flows, perm = 4-round Feistel with cycle walking; each
+                 flow exactly duplicate_factor times, shuffled                                ingest.py:139-147
+      ts         start_ts + floor(p * window_seconds / total): time-ordered                   ingest.py:143-148
+
+    Returns (records TRACE_DTYPE, truth dict)."""
+    M64 = (1 << 64) - 1
+    n_hosts = background_hosts + superpoints
+    if n_hosts == 0:
+        return np.empty(0, dtype=TRACE_DTYPE), {}
+    seed64 = seed & M64
+    idx = np.arange(n_hosts, dtype=np.uint64)
+    host_key = mix64(seed64 ^ 0x1F83D9ABFB41BD6B) & 0xFFFFFFFF
+    hosts = _fmix32_many(idx.astype(np.uint32) ^ np.uint32(host_key))
+    with np.errstate(over="ignore"):
+        u = mix64_many(idx + np.uint64(seed64 ^ 0x5BE0CD19137E2179))
+        bases = mix64_many(idx + np.uint64(seed64 ^ 0xCBBB9D5DC1059ED8)) & np.uint64(0xFFFFFFFF)
+    cards = np.empty(n_hosts, dtype=np.int64)
+    if background_hosts:
+        kmax, a = background_max_cardinality, background_zipf
+        if kmax > 1:
+            big = 1_000_000
+            zeta = float(np.sum(np.arange(1, big + 1, dtype=np.float64) ** -a)) + (big + 0.5) ** (1.0 - a) / (a - 1.0)
+            cdf = np.cumsum(np.arange(1, kmax, dtype=np.float64) ** -a) / zeta
+            thr = np.floor(np.minimum(cdf, 1.0) * float(1 << 53)).astype(np.uint64)
+        else:
+            thr = np.empty(0, dtype=np.uint64)
+        cards[:background_hosts] = 1 + np.searchsorted(thr, u[:background_hosts] >> np.uint64(11), side="right")
+    if superpoints:
+        lo, hi = super_cardinality
+        cards[background_hosts:] = lo + (u[background_hosts:] % np.uint64(hi - lo + 1)).astype(np.int64)
+    prefix = np.concatenate([[0], np.cumsum(cards)]).astype(np.uint64)
+    flows = int(prefix[-1])
+    total = flows * duplicate_factor
+    bits = 2
+    while (1 << bits) < total:
+        bits += 1
+    hb = (bits + 1) // 2
+    mask = np.uint64((1 << hb) - 1)
+    key = mix64(seed64 ^ 0x629A292A367CD507)
+    x = np.arange(total, dtype=np.uint64)
+    todo = np.ones(total, dtype=bool)
+    while todo.any():
+        cur = x[todo]
+        l, r = (cur >> np.uint64(hb)) & mask, cur & mask
+        for rnd in range(4):
+            k = np.uint64(((key + rnd) * 0x9E3779B97F4A7C15) & M64)
+            f = mix64_many(r ^ k) & mask
+            l, r = r, l ^ f
+        cur = (l << np.uint64(hb)) | r
+        x[todo] = cur
+        todo[todo] = cur >= np.uint64(total)
+    f_idx = x % np.uint64(flows)
+    h = np.searchsorted(prefix, f_idx, side="right") - 1
+    rec = np.empty(total, dtype=TRACE_DTYPE)
+    rec["src"] = hosts[h]
+    rec["dst"] = ((bases[h] + (f_idx - prefix[h])) & np.uint64(0xFFFFFFFF)).astype(np.uint32)
+    p = np.arange(total, dtype=object) if total * window_seconds >= (1 << 63) else np.arange(total, dtype=np.uint64)
+    rec["ts"] = (start_ts + (p * window_seconds) // total).astype(np.uint32)
+    return rec, {int(a_): int(c) for a_, c in zip(hosts.tolist(), cards.tolist())}
+
+
 def engine_trace(seed: int, n_noise: int = 90_000, window_seconds: int = 300):
     """A deterministic multi-window trace with late records, built from mix64 only (no
     library RNG): three and a half windows of background pairs in time order, three hosts

@@ -19,6 +19,7 @@ from .dhla import (DEFAULT_MAX_CANDIDATES, Dhla, Estimate, SuperPointReport, hot
 from .engine import (DetectionEngine, TRACE_DTYPE, WindowConfig, WindowResult, WindowSession,
                      split_pairs)
 from .exact import EvalMetrics, ExactCounter, evaluate, exact_oracle
+from .traces import GeneratorConfig, generate_trace, generate_trace_device
 from .snapshot import read_snapshot, write_snapshot
 from .errors import (CapacityError, ConfigError, CudaError, DataError, DhsaError,
                      SealedWindowError)
@@ -28,6 +29,6 @@ __version__ = "0.1.0"
 __all__ = [
     "DhgParams", "Dhla", "SuperPointReport", "Estimate", "merge", "hot_threshold",
     "DEFAULT_MAX_CANDIDATES", "DetectionEngine", "WindowConfig", "WindowResult", "WindowSession",
-    "split_pairs", "TRACE_DTYPE", "read_snapshot", "write_snapshot", "exact_oracle", "ExactCounter", "evaluate", "EvalMetrics", "DhsaError", "ConfigError", "DataError", "CapacityError",
+    "split_pairs", "TRACE_DTYPE", "read_snapshot", "write_snapshot", "GeneratorConfig", "generate_trace", "generate_trace_device", "exact_oracle", "ExactCounter", "evaluate", "EvalMetrics", "DhsaError", "ConfigError", "DataError", "CapacityError",
     "SealedWindowError", "CudaError",
 ]

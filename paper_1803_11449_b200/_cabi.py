@@ -78,6 +78,8 @@ SIGNATURES = {
     "dhsa_exact_add_pairs": [_vp, _vp, _vp, _u64, _vp],
     "dhsa_exact_add_records": [_vp, _vp, _u64, _u64, _u64, C.c_uint32, C.c_uint32, C.c_int, _vp],
     "dhsa_exact_result": [_vp, _u64, _vp, _vp, _u64, C.POINTER(_u64), C.POINTER(_u64), C.POINTER(_u64), _vp],
+    "dhsa_generate_trace": [C.c_int, _vp, _vp, _vp, C.c_uint32, _u64, _u64, _u64, C.c_uint32, C.c_uint32, _u64, _u64,
+                            _vp, _vp, _vp, _vp],
     "dhsa_copy_to_device_async": [C.c_int, _vp, _vp, _u64, _vp],
     "dhsa_or_merge": [_vp, _vp],
     "dhsa_or_merge_peers": [_vp, C.POINTER(_vp), C.c_int, _u64, _u64],

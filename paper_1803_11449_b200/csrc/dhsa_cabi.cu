@@ -1397,6 +1397,43 @@ extern "C" int dhsa_exact_result(dhsa_exact_t *e, uint64_t min_count, uint64_t *
     return DHSA_OK;
 }
 
+// --------------------------------------------------------- trace generator --
+
+extern "C" int dhsa_generate_trace(int device, const uint32_t *hosts_dev, const uint64_t *prefix_dev,
+                                   const uint32_t *bases_dev, uint32_t n_hosts, uint64_t flows, uint64_t dup,
+                                   uint64_t seed, uint32_t start_ts, uint32_t window_seconds, uint64_t p_lo,
+                                   uint64_t p_hi, void *records_out_dev, uint32_t *cand_out_dev,
+                                   uint32_t *opp_out_dev, void *cuda_stream)
+{
+    if (p_lo >= p_hi) return DHSA_OK;
+    NEED(hosts_dev);
+    NEED(prefix_dev);
+    NEED(bases_dev);
+    if (n_hosts == 0 || flows == 0 || dup == 0) return fail(DHSA_ECONFIG, "trace population must be non-empty");
+    if (window_seconds == 0) return fail(DHSA_ECONFIG, "window_seconds must be positive (got 0)");
+    if (flows > (1ull << 62) / dup) return fail(DHSA_ECONFIG, "flows * duplicate_factor must stay below 2^62");
+    const uint64_t total = flows * dup;
+    if (p_hi > total) return fail(DHSA_EDATA, "positions [%llu, %llu) exceed the trace's %llu packets",
+                                  (unsigned long long)p_lo, (unsigned long long)p_hi, (unsigned long long)total);
+    CU(cudaSetDevice(device));
+    TraceSpec t;
+    t.hosts = hosts_dev, t.prefix = prefix_dev, t.bases = bases_dev;
+    t.n_hosts = n_hosts, t.flows = flows, t.total = total;
+    t.perm_key = seed;
+    uint32_t bits = 2;
+    while (bits < 64 && (1ull << bits) < total) bits++;
+    t.half_bits = (bits + 1) / 2;
+    t.start_ts = start_ts, t.window_seconds = window_seconds;
+    int sms = 0;
+    CU(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
+    uint64_t want = (p_hi - p_lo + 255) / 256, cap = (uint64_t)sms * 8;
+    const int grid = (int)(want < cap ? want : cap);
+    k_generate_trace<<<grid, 256, 0, (cudaStream_t)cuda_stream>>>(t, p_lo, p_hi, static_cast<uint32_t *>(records_out_dev),
+                                                                 cand_out_dev, opp_out_dev);
+    CU(cudaGetLastError());
+    return DHSA_OK;
+}
+
 // ----------------------------------------------------------------- probes --
 
 extern "C" int dhsa_probe_l2(int device, int kind, uint64_t buffer_bytes, uint64_t ops, double *ops_per_sec)

@@ -1449,6 +1449,83 @@ __global__ void __launch_bounds__(256) k_exact_collect(ExactTables t, unsigned l
     }
 }
 
+// ---------------------------------------------- synthetic trace generator --
+// generate_trace's per-record half (pkg/src/dhsa/ingest.py:128-151) on the device: flows are
+// laid out host-major (host h owns flow indices [prefix[h], prefix[h+1]), its destinations a
+// ramp from bases[h], so they are distinct by construction, ingest.py:129-133), every flow is
+// repeated `dup` times (duplicate_factor, :135-137), the stream is shuffled and time-ordered
+// (:143-148).  Output position p takes record perm(p): a 4-round Feistel network over the
+// smallest even-width bit field covering M = flows * dup, cycle-walked into [0, M) -- a
+// bijection, so each flow appears exactly `dup` times with no sort and no 8 GB permutation
+// array; timestamps rise linearly with p (sorted by construction).  Pure integer arithmetic
+// on counters: the numpy restatement in oracle/ reproduces every byte.
+struct TraceSpec {
+    const uint32_t *hosts;        // n_hosts distinct addresses
+    const uint64_t *prefix;       // n_hosts + 1 exclusive prefix sums of the cardinalities
+    const uint32_t *bases;        // first destination of each host's ramp
+    uint32_t n_hosts;
+    uint64_t flows;               // prefix[n_hosts]
+    uint64_t total;               // flows * dup
+    uint64_t perm_key;
+    uint32_t half_bits;           // Feistel half width
+    uint32_t start_ts, window_seconds;
+};
+
+__device__ __forceinline__ uint64_t trace_permute(uint64_t p, const TraceSpec &t)
+{
+    const uint64_t mask = (1ull << t.half_bits) - 1ull;
+    uint64_t x = p;
+    do {
+        uint64_t l = (x >> t.half_bits) & mask, r = x & mask;
+#pragma unroll
+        for (int rnd = 0; rnd < 4; rnd++) {
+            const uint64_t f = mix64(r ^ ((t.perm_key + (uint64_t)rnd) * 0x9E3779B97F4A7C15ULL)) & mask;
+            const uint64_t nl = r;
+            r = l ^ f;
+            l = nl;
+        }
+        x = (l << t.half_bits) | r;
+    } while (x >= t.total);
+    return x;
+}
+
+// records_out (12-byte IPPR records) and/or cand_out / opp_out (host-order uint32) for output
+// positions [p_lo, p_hi); any of the three outputs may be null.
+__global__ void __launch_bounds__(256) k_generate_trace(TraceSpec t, uint64_t p_lo, uint64_t p_hi,
+                                                        uint32_t *__restrict__ records_out,
+                                                        uint32_t *__restrict__ cand_out,
+                                                        uint32_t *__restrict__ opp_out)
+{
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t p = p_lo + (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; p < p_hi; p += stride) {
+        const uint64_t f = trace_permute(p, t) % t.flows;
+        uint32_t lo = 0, hi = t.n_hosts;  // largest h with prefix[h] <= f
+        while (hi - lo > 1) {
+            const uint32_t mid = (lo + hi) >> 1;
+            if (t.prefix[mid] <= f) lo = mid; else hi = mid;
+        }
+        const uint32_t src = t.hosts[lo];
+        const uint32_t dst = t.bases[lo] + (uint32_t)(f - t.prefix[lo]);
+        const uint64_t q = p - p_lo;
+        if (records_out) {
+            // ts = start + floor(p * window / total), exact in 128-bit arithmetic
+            const uint64_t hi64 = __umul64hi(p, (uint64_t)t.window_seconds), lo64 = p * (uint64_t)t.window_seconds;
+            uint64_t ts;
+            if (hi64 == 0) {
+                ts = lo64 / t.total;
+            } else {  // p * window >= 2^64: split the division (total < 2^63 here)
+                const unsigned __int128 num = ((unsigned __int128)hi64 << 64) | lo64;
+                ts = (uint64_t)(num / t.total);
+            }
+            records_out[3 * q + 0] = t.start_ts + (uint32_t)ts;
+            records_out[3 * q + 1] = __byte_perm(src, 0, 0x0123);  // network byte order on the wire
+            records_out[3 * q + 2] = __byte_perm(dst, 0, 0x0123);
+        }
+        if (cand_out) cand_out[q] = src;
+        if (opp_out) opp_out[q] = dst;
+    }
+}
+
 // ------------------------------------------------------------ L2 probes --
 // Random-address 32-bit operations into a buffer that fits L2: the ceiling the
 // scan's sketch traffic runs against.  Addresses come from a multiply-xorshift
