@@ -52,6 +52,7 @@ static int cuda_fail(cudaError_t e, const char *what)
 
 // ------------------------------------------------------------------ handle --
 
+static const uint64_t kPinnedReports = 256;  // report rows copied back inside the read-out graph
 static const int kStageBufs = 3;            // staging buffers of the host-input pipeline
 static const uint64_t kStagePackets = 1ull << 22;  // packets per staged chunk (16 MiB per array)
 
@@ -96,6 +97,15 @@ struct dhsa_sketch {
     uint64_t *hosts_in;     // shared_zero_counts input
     int32_t *sz_out;
     uint64_t hosts_in_cap;
+
+    // the read-out chain as a CUDA graph (captured once per theta / max_candidates / workspace)
+    cudaGraphExec_t restore_graph;
+    double graph_theta;
+    uint64_t graph_max_candidates;
+    uint64_t graph_cand_cap;
+    uint64_t graph_kernels;
+    bool graph_disabled;
+    ReportOut *reports_pinned;      // the first kPinnedReports rows land here with the control block
 
     // record streams
     unsigned long long *tally;      // device: records fed, records dropped
@@ -223,6 +233,8 @@ extern "C" int dhsa_create(const dhsa_params_t *params, int device, dhsa_sketch_
     CU(cudaMalloc(&s->tally, 2 * sizeof(unsigned long long)));
     CU(cudaMemsetAsync(s->tally, 0, 2 * sizeof(unsigned long long), s->stream));
     CU(cudaMallocHost(&s->ctl_host, sizeof(Control)));
+    CU(cudaMallocHost(&s->reports_pinned, kPinnedReports * sizeof(ReportOut)));
+    s->graph_disabled = getenv("DHSA_NO_GRAPH") != nullptr;
     CU(cudaMemsetAsync(s->bits, 0, s->alloc_bytes, s->stream));
     CU(cudaMemsetAsync(s->ctl, 0, sizeof(Control), s->stream));
     CU(cudaStreamSynchronize(s->stream));
@@ -261,6 +273,8 @@ extern "C" int dhsa_destroy(dhsa_sketch_t *s)
     }
     cudaFree(s->ctl);
     cudaFreeHost(s->ctl_host);
+    cudaFreeHost(s->reports_pinned);
+    if (s->restore_graph) cudaGraphExecDestroy(s->restore_graph);
     cudaStreamDestroy(s->own_stream);
     cudaStreamDestroy(s->copy_stream);
     delete s;
@@ -1049,12 +1063,11 @@ extern "C" int dhsa_shared_zero_counts(dhsa_sketch_t *s, const uint64_t *hosts_h
     return DHSA_OK;
 }
 
-extern "C" int dhsa_restore(dhsa_sketch_t *s, double theta, uint64_t max_candidates, dhsa_report_t *reports_host,
-                            uint64_t reports_cap, dhsa_restore_info_t *info)
+// The whole read-out -- zero counts, hot sets + scalars, stage chain, verify, re-estimate, sort,
+// emit, and the copy-back of the control block and the first kPinnedReports rows -- enqueued on
+// s->stream.  Called directly, or once under stream capture to build the graph.
+static int enqueue_restore(dhsa_sketch *s, double theta, uint64_t max_candidates)
 {
-    NEED(s);
-    std::lock_guard<std::mutex> lk(s->mu);
-    if (int rc = use_device(s)) return rc;
     if (int rc = launch_estimate(s, theta)) return rc;
     if (int rc = launch_restore_stages(s, max_candidates)) return rc;
     const int grid = s->sm_count * 4;
@@ -1063,17 +1076,81 @@ extern "C" int dhsa_restore(dhsa_sketch_t *s, double theta, uint64_t max_candida
     k_emit_reports<<<grid, 256, 0, s->stream>>>(s->packed, s->params.g, s->reports, s->ctl);
     s->launches += 3;
     CU(cudaGetLastError());
-    if (int rc = read_control(s)) return rc;
+    CU(cudaMemcpyAsync(s->ctl_host, s->ctl, sizeof(Control), cudaMemcpyDeviceToHost, s->stream));
+    const uint64_t rows = s->cand_cap < kPinnedReports ? s->cand_cap : kPinnedReports;
+    CU(cudaMemcpyAsync(s->reports_pinned, s->reports, rows * sizeof(ReportOut), cudaMemcpyDeviceToHost, s->stream));
+    return DHSA_OK;
+}
+
+// One graph launch instead of eight kernel launches and two copies: the chain is latency-bound
+// (every kernel is microseconds), so launch gaps are a third of its time.  Falls back to direct
+// launches if capture is not possible on the current stream (same kernels either way).
+static int run_restore(dhsa_sketch *s, double theta, uint64_t max_candidates)
+{
+    if (int rc = ensure_readout(s)) return rc;
+    if (int rc = ensure_candidates(s, max_candidates)) return rc;
+    if (!s->graph_disabled) {
+        const bool fresh = s->restore_graph && s->graph_theta == theta &&
+                           s->graph_max_candidates == max_candidates && s->graph_cand_cap == s->cand_cap;
+        if (!fresh) {
+            if (s->restore_graph) {
+                cudaGraphExecDestroy(s->restore_graph);
+                s->restore_graph = nullptr;
+            }
+            const uint64_t before = s->launches;
+            cudaGraph_t graph = nullptr;
+            cudaError_t e = cudaStreamBeginCapture(s->stream, cudaStreamCaptureModeThreadLocal);
+            if (e == cudaSuccess) {
+                const int rc = enqueue_restore(s, theta, max_candidates);
+                e = cudaStreamEndCapture(s->stream, &graph);
+                if (rc != DHSA_OK && e == cudaSuccess) e = cudaErrorUnknown;
+            }
+            if (e == cudaSuccess) e = cudaGraphInstantiate(&s->restore_graph, graph, 0);
+            if (graph) cudaGraphDestroy(graph);
+            s->graph_kernels = s->launches - before;
+            s->launches = before;
+            if (e != cudaSuccess) {
+                (void)cudaGetLastError();
+                s->restore_graph = nullptr;
+                s->graph_disabled = true;  // e.g. the caller's stream is itself being captured
+            } else {
+                s->graph_theta = theta;
+                s->graph_max_candidates = max_candidates;
+                s->graph_cand_cap = s->cand_cap;
+            }
+        }
+        if (s->restore_graph) {
+            CU(cudaGraphLaunch(s->restore_graph, s->stream));
+            s->launches += s->graph_kernels;
+            CU(cudaStreamSynchronize(s->stream));
+            return DHSA_OK;
+        }
+    }
+    if (int rc = enqueue_restore(s, theta, max_candidates)) return rc;
+    CU(cudaStreamSynchronize(s->stream));
+    return DHSA_OK;
+}
+
+extern "C" int dhsa_restore(dhsa_sketch_t *s, double theta, uint64_t max_candidates, dhsa_report_t *reports_host,
+                            uint64_t reports_cap, dhsa_restore_info_t *info)
+{
+    NEED(s);
+    std::lock_guard<std::mutex> lk(s->mu);
+    if (int rc = use_device(s)) return rc;
+    if (int rc = run_restore(s, theta, max_candidates)) return rc;
     if (s->ctl_host->fail_stage) {
         fill_info(s, info);
         return capacity_error(s, max_candidates);
     }
+    const int grid = s->sm_count * 4;
     const uint64_t n = s->ctl_host->n_reports;
+    bool in_pinned = n <= kPinnedReports;
     if (n > DHSA_SORT_SMEM_MAX) {  // rare: the single-CTA sorter declined, sort with global passes and re-emit
         if (int rc = sort_large(s, s->packed, n)) return rc;
         k_emit_reports<<<grid, 256, 0, s->stream>>>(s->packed, s->params.g, s->reports, s->ctl);
         s->launches++;
         CU(cudaGetLastError());
+        in_pinned = false;
     }
     fill_info(s, info);
     if (n > reports_cap) return fail(DHSA_EDATA, "%llu reports exceed the output capacity %llu",
@@ -1081,8 +1158,12 @@ extern "C" int dhsa_restore(dhsa_sketch_t *s, double theta, uint64_t max_candida
     if (n) {
         NEED(reports_host);
         static_assert(sizeof(ReportOut) == sizeof(dhsa_report_t), "report layouts must match");
-        CU(cudaMemcpyAsync(reports_host, s->reports, n * sizeof(ReportOut), cudaMemcpyDeviceToHost, s->stream));
-        CU(cudaStreamSynchronize(s->stream));
+        if (in_pinned) {
+            memcpy(reports_host, s->reports_pinned, n * sizeof(ReportOut));
+        } else {
+            CU(cudaMemcpyAsync(reports_host, s->reports, n * sizeof(ReportOut), cudaMemcpyDeviceToHost, s->stream));
+            CU(cudaStreamSynchronize(s->stream));
+        }
     }
     return DHSA_OK;
 }

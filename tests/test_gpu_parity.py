@@ -403,6 +403,62 @@ def test_many_reports_sorted_like_the_reference():
     assert [(r.host, r.saturated) for r in got] == [(r.host, r.saturated) for r in want]
 
 
+def _random_param_sets(n, seed):
+    """Valid DhgParams drawn at random (pkg/src/dhsa/dhg.py:78-105 rules), small enough for the
+    oracle's literal enumeration."""
+    rng = np.random.default_rng(seed)
+    out = []
+    while len(out) < n:
+        r = int(rng.integers(3, 9))
+        k = int(rng.integers(4, 13))
+        alpha = int(rng.integers(1, k + 1))
+        w = int(rng.integers(max(8, k), 33))
+        g = int(2 ** rng.integers(3, 10))
+        if (r - 2) * alpha + k < w or (r - 2) * alpha + k > 64:
+            continue
+        out.append(dict(r=r, g=g, k=k, alpha=alpha, key_width=w,
+                        seed_dh0=int(rng.integers(0, 2 ** 63)), seed_h1=int(rng.integers(0, 2 ** 63))))
+    return out
+
+
+@pytest.mark.parametrize("kw", _random_param_sets(24, 2024), ids=lambda kw: "r{r}g{g}k{k}a{alpha}w{key_width}".format(**kw))
+def test_random_parameter_sets_match_oracle(kw):
+    """Scan, zero counts, hot sets, candidates, per-stage counts, reports (or the CapacityError
+    text) for parameter sets nobody hand-picked: every path choice (vector / general kernel,
+    bitmap / list stage expansion, word / sub-word cells) gets exercised."""
+    rng = np.random.default_rng(kw["seed_dh0"] & 0xFFFF)
+    wmask = np.uint32((1 << kw["key_width"]) - 1) if kw["key_width"] < 32 else np.uint32(0xFFFFFFFF)
+    cells = 1 << kw["k"]
+    cand, opp = O.distinct_pairs(int(cells * kw["g"] * 0.02) + 200, int(rng.integers(1, 1000)))
+    cand = cand & wmask
+    theta = max(4, kw["g"] // 2)
+    for n in range(3):
+        c2, o2 = O.plant_pairs(int(rng.integers(0, 2 ** 32)) & int(wmask), int(theta * (1.5 + n)), 900 + n)
+        cand, opp = np.concatenate([cand, c2]), np.concatenate([opp, o2])
+    ora = O.OracleSketch(**kw)
+    ora.update_batch(cand, opp)
+    sk = P.Dhla(P.DhgParams(**kw))
+    sk.update_batch(cand, opp)
+    assert np.array_equal(sk.bits, ora.bits)
+    assert np.array_equal(sk.zero_counts(), ora.zero_counts())
+    for a, b in zip(sk.hot_sets(theta), ora.hot_sets(theta)):
+        assert a.tolist() == b.tolist()
+    mc = 1 << 18
+    try:
+        hosts, stages = ora.candidate_hosts(theta, mc, return_stage_counts=True)
+    except O.OracleCapacityError as exc:
+        with pytest.raises(P.CapacityError) as err:
+            sk.restore_superpoints(theta, max_candidates=mc)
+        assert str(err.value) == str(exc)
+        return
+    assert sk._candidate_hosts(theta, mc).tolist() == hosts.tolist()
+    assert sk.last_info["stage_counts"] == stages
+    got, want = sk.restore_superpoints(theta, max_candidates=mc), ora.restore_superpoints(theta, mc)
+    assert [(r.host, r.saturated) for r in got] == [(r.host, r.saturated) for r in want]
+    for a, b in zip(got, want):
+        assert a.estimate == pytest.approx(b.estimate, rel=REL_TOL)
+
+
 # ----------------------------------------------------------------------- merge --
 
 

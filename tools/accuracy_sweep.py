@@ -1,0 +1,75 @@
+"""BASELINE config 5: threshold / DDH-size sweep, accuracy vs throughput, all on the device.
+
+For every (theta, g, k, alpha) point: generate a window on the GPU (N4), scan + restore it
+(the hot path), get exact ground truth on the GPU (N3) and score FPR / FNR / mean relative
+error (ingest.evaluate semantics).  g grows with theta (at g = 1024 the largest representable
+estimate is g ln g ~ 7098, SURVEY 7 hard part 4) and alpha is chosen so that
+(r - 2) alpha + k >= 32.  Prints one JSON document; committed under profiles/.
+"""
+import json
+import sys
+import time
+
+import torch
+
+sys.path.insert(0, ".")
+import paper_1803_11449_b200 as P  # noqa: E402
+
+POINTS = [
+    # theta, g, k, alpha
+    (256, 1024, 14, 6), (1024, 1024, 14, 6), (4096, 4096, 14, 6), (16384, 16384, 14, 6),
+    (1024, 1024, 12, 7), (1024, 1024, 16, 6), (1024, 1024, 18, 5),
+]
+
+
+def main():
+    out = []
+    for theta, g, k, alpha in POINTS:
+        lo = max(2 * theta, 512)
+        # the background shrinks with theta: at theta 256 a g=1024 cell is hot above 227 set bits, and
+        # 150k hosts would make half of all cells hot (the restore then overflows max_candidates, as
+        # the reference's does -- BASELINE.md section 2)
+        cfg = P.GeneratorConfig(background_hosts=min(150_000, 150 * theta), background_max_cardinality=max(16, theta // 4),
+                                superpoints=50, super_cardinality=(lo, 4 * lo), duplicate_factor=8)
+        tr = P.generate_trace_device(cfg, seed=100, fmt="pairs")
+        params = P.DhgParams(g=g, k=k, alpha=alpha)
+        sk = P.Dhla(params)
+        stream = torch.cuda.Stream()
+        with torch.cuda.stream(stream):
+            sk.use_stream(stream.cuda_stream)
+            try:
+                for _ in range(2):
+                    sk.reset()
+                    sk.update_batch(tr["cand"], tr["opp"])
+                    reports = sk.restore_superpoints(theta, max_candidates=1 << 22)
+            except P.CapacityError as exc:
+                out.append(dict(theta=theta, g=g, k=k, alpha=alpha, packets=tr["total"], capacity_error=str(exc)))
+                print(json.dumps(out[-1]), file=sys.stderr, flush=True)
+                continue
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            for _ in range(3):
+                sk.reset()
+                sk.update_batch(tr["cand"], tr["opp"])
+                reports = sk.restore_superpoints(theta, max_candidates=1 << 22)
+            e1.record(stream)
+            torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1) / 3
+        counter = P.ExactCounter(expected_pairs=tr["flows"])
+        counter.add_pairs(tr["cand"], tr["opp"])
+        hosts, counts, n_pairs, _ = counter.result(min_count=1)
+        truth = dict(zip(hosts.tolist(), counts.tolist()))
+        assert truth == tr["truth"], "GPU exact oracle disagrees with the generator's ground truth"
+        m = P.evaluate(reports, truth, theta)
+        out.append(dict(theta=theta, g=g, k=k, alpha=alpha, r=params.r, sketch_mib=params.sketch_bytes / 2 ** 20,
+                        packets=tr["total"], distinct_flows=n_pairs, ms_per_window=ms,
+                        gpps=tr["total"] / (ms * 1e-3) / 1e9, flow_cache_hit_rate=(lambda a, b: b / a if a else None)(*sk.flow_cache_stats()),
+                        **m.as_dict()))
+        print(json.dumps(out[-1]), file=sys.stderr, flush=True)
+        del sk, tr, counter
+        torch.cuda.empty_cache()
+    print(json.dumps({"when": time.strftime("%Y-%m-%d"), "points": out}, indent=1))
+
+
+if __name__ == "__main__":
+    main()
