@@ -191,7 +191,9 @@ class DetectionEngine:
             if flat.dtype != torch.uint8 or flat.numel() % RECORD_BYTES:
                 raise ValueError("device records must be a uint8 tensor of whole 12-byte records")
             n = flat.numel() // RECORD_BYTES
-            step = self.chunk_records
+            # already on the device: nothing to stage, so plan and scan it whole (chunk_records only
+            # bounds staging buffers); a caller-chosen smaller chunk is still honoured for tests
+            step = max(self.chunk_records, n) if self.chunk_records >= DEFAULT_CHUNK_RECORDS else self.chunk_records
             for lo in range(0, n, step):
                 hi = min(n, lo + step)
                 yield flat[lo * RECORD_BYTES: hi * RECORD_BYTES], hi - lo

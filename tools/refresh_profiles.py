@@ -1,0 +1,76 @@
+"""Summarise the artefacts of tools/gpu_profile_pass.sh (gpurun_out/) into profiles/ (tracked)."""
+import collections
+import csv
+import json
+import shutil
+import subprocess
+import sys
+
+TAG = sys.argv[1] if len(sys.argv) > 1 else "r01"
+OUT = "profiles"
+
+
+def ncu(page):
+    return subprocess.run(["ncu", "-i", f"gpurun_out/prof_scan_{TAG}.ncu-rep", "--page", page, "--csv"],
+                          capture_output=True, text=True).stdout
+
+
+raw = ncu("raw")
+open(f"{OUT}/{TAG}_k_scan_flowcache_raw.csv", "w").write(raw)
+open(f"{OUT}/{TAG}_k_scan_flowcache_details.csv", "w").write(ncu("details"))
+KEYS = ['gpu__time_duration.sum', 'dram__bytes_read.sum', 'dram__bytes_write.sum',
+        'gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed',
+        'l1tex__m_l1tex2xbar_req_cycles_active.avg.pct_of_peak_sustained_elapsed',
+        'l1tex__throughput.avg.pct_of_peak_sustained_elapsed', 'lts__throughput.avg.pct_of_peak_sustained_elapsed',
+        'lts__t_sector_hit_rate.pct', 'l1tex__t_sector_hit_rate.pct', 'l1tex__t_sectors_pipe_lsu_mem_global_op_ld.sum',
+        'l1tex__t_sectors_pipe_lsu_mem_global_op_red.sum', 'l1tex__t_sectors_pipe_lsu_mem_global_op_st.sum',
+        'l1tex__m_xbar2l1tex_read_sectors_mem_global_op_tma_ld.sum', 'lts__t_sectors.sum',
+        'lts__t_sectors_srcunit_tex_op_read.sum', 'lts__t_sectors_srcunit_tex_op_red.sum',
+        'sm__throughput.avg.pct_of_peak_sustained_elapsed', 'sm__warps_active.avg.pct_of_peak_sustained_active',
+        'smsp__issue_active.avg.pct_of_peak_sustained_active', 'launch__registers_per_thread', 'launch__grid_size',
+        'launch__block_size', 'sm__cycles_elapsed.avg', 'smsp__inst_executed.sum']
+
+
+def pick(text):
+    rows = list(csv.reader(text.splitlines()))
+    d, u = dict(zip(rows[0], rows[2])), dict(zip(rows[0], rows[1]))
+    return {k: (float(d[k].replace(',', '')) if d.get(k) not in (None, '') else None, u.get(k)) for k in KEYS}
+
+
+summary = {
+    "k_scan_vec4<5,2> (scan mode test_agg, no flow cache; first capture of the round)":
+        pick(open(f"{OUT}/{TAG}_k_scan_vec4_mode2_raw.csv").read()),
+    "k_scan_flowcache<5,SoaSource> (scan mode auto/flow_cache, 64 MiB table, TMA-staged packet stream)": pick(raw),
+}
+json.dump(summary, open(f"{OUT}/{TAG}_scan_kernels_ncu_summary.json", "w"), indent=1)
+fc = list(summary.values())[1]
+conv = {'Mbyte': 1e6, 'Gbyte': 1e9, 'Kbyte': 1e3, 'byte': 1}
+traffic = sum(fc[k][0] * conv[fc[k][1]] for k in ('dram__bytes_read.sum', 'dram__bytes_write.sum'))
+t = json.load(open(f"{OUT}/{TAG}_traffic.json"))
+t['k_scan_flowcache<5>']['dram_bytes_per_launch'] = traffic
+json.dump(t, open(f"{OUT}/{TAG}_traffic.json", "w"), indent=1)
+for k, v in fc.items():
+    print(k, v)
+print("traffic", traffic)
+
+shutil.copy(f"gpurun_out/launches_{TAG}.csv", f"{OUT}/{TAG}_launch_list_bench_steps2.csv")
+for name in ("", "_reference", "_test_agg", "_test", "_red"):
+    shutil.copy(f"gpurun_out/bench_{TAG}{name}.json", f"{OUT}/{TAG}_bench{name}.json")
+rows = [r for r in csv.reader(open(f"{OUT}/{TAG}_launch_list_bench_steps2.csv")) if len(r) > 10]
+hdr = rows[0]
+ki, vi = hdr.index('Kernel Name'), hdr.index('Metric Value')
+agg = collections.OrderedDict()
+for r in rows[1:]:
+    if 'dhsa::' not in r[ki]:
+        continue
+    a = agg.setdefault(r[ki].split('(')[0][:62], [0, 0.0])
+    a[0] += 1
+    a[1] += float(r[vi].replace(',', ''))
+tot = sum(a[1] for a in agg.values())
+lines = ["# ncu --metrics gpu__time_duration.sum --clock-control none; python bench.py --steps 2 --warmup 3 (5 windows of 100M packets)",
+         "# our kernels only (torch's data-generation kernels omitted); per-launch times are cold-cache and serialised",
+         f"{'kernel':64s} {'launches':>8s} {'avg_us':>10s} {'share_of_our_gpu_time':>22s}"]
+for k, (n, tt) in sorted(agg.items(), key=lambda x: -x[1][1]):
+    lines.append(f"{k:64s} {n:8d} {tt / n / 1e3:10.2f} {tt / tot:22.4f}")
+open(f"{OUT}/{TAG}_launch_shares.txt", "w").write("\n".join(lines) + "\n")
+print("\n".join(lines))
