@@ -37,6 +37,17 @@ def stale() -> bool:
     return any(os.path.exists(d) and os.path.getmtime(d) > built for d in deps)
 
 
+def build_variant(out: str, defs) -> str:
+    """A tuning variant of the library (extra -D definitions) for A/B runs: tools/ builds them
+    under build/variants/ and selects one with DHSA_LIB=<path>."""
+    os.makedirs(os.path.dirname(out), exist_ok=True)
+    cmd = [_nvcc(), *NVCC_FLAGS, *[f"-D{d}" for d in defs], "-o", out, *[os.path.join(CSRC, f) for f in SOURCES]]
+    proc = subprocess.run(cmd, capture_output=True, text=True)
+    if proc.returncode != 0:
+        raise RuntimeError("nvcc failed:\n" + proc.stdout + proc.stderr)
+    return out
+
+
 def build(force: bool = False, verbose: bool = False) -> str:
     if not force and not stale():
         return LIB_PATH

@@ -104,7 +104,9 @@ def lib() -> C.CDLL:
         with _lock:
             if _lib is None:
                 path = _build.LIB_PATH
-                if _build.stale():
+                if os.environ.get("DHSA_LIB"):      # a tuning variant built by _build.build_variant
+                    path = os.environ["DHSA_LIB"]
+                elif _build.stale():
                     if os.environ.get("DHSA_NO_BUILD") and os.path.exists(path):
                         pass
                     else:

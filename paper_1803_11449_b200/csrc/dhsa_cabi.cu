@@ -476,20 +476,13 @@ static int partition_buckets(const dhsa_sketch *s)
     return nb < 1 ? 1 : nb;
 }
 
-// the table's 32-bit entries hold (tag << 1 | choice) + 1 with tag = rem >> 13, rem < 2^bits / nb + 1
+// the table's 32-bit entries hold (tag << 1 | choice) + 1 with tag = rem >> 13 and
+// rem < (2^32 / nb + 1) << log2(g)
 static bool partition_supported(const dhsa_sketch *s)
 {
-    const int bits = 32 + s->dp.log2g;
-    if (bits > 50) return false;
-    const uint64_t rem_max = ((1ull << bits) + (uint64_t)partition_buckets(s) - 1) / (uint64_t)partition_buckets(s) + 1;
+    if (s->dp.log2g > 20) return false;
+    const uint64_t rem_max = ((1ull << 32) / (uint64_t)partition_buckets(s) + 2) << s->dp.log2g;
     return (rem_max >> DHSA_PT_LOG2_SETS) < (1ull << 30);
-}
-
-static uint64_t inverse_mod_2_64(uint64_t odd)
-{
-    uint64_t inv = odd;  // correct to 3 bits; each Newton step doubles that
-    for (int it = 0; it < 6; it++) inv *= 2 - odd * inv;
-    return inv;
 }
 
 static int ensure_partition_locked(dhsa_sketch *s)
@@ -501,11 +494,6 @@ static int ensure_partition_locked(dhsa_sketch *s)
         CU(cudaMalloc(&pt.sync, 8 * sizeof(unsigned int)));
         CU(cudaMalloc(&pt.stats, 4 * sizeof(unsigned long long)));
         CU(cudaMemsetAsync(pt.stats, 0, 4 * sizeof(unsigned long long), s->stream));
-        pt.key_bits = 32 + s->dp.log2g;
-        pt.xs = (pt.key_bits + 1) / 2;
-        pt.key_mask = (1ull << pt.key_bits) - 1;
-        pt.c1 = 0x9E3779B1u, pt.c2 = 0x85EBCA77u;
-        pt.c1_inv = inverse_mod_2_64(pt.c1), pt.c2_inv = inverse_mod_2_64(pt.c2);
     }
     if (s->pt_ring_bytes < need) {
         CU(cudaStreamSynchronize(s->stream));

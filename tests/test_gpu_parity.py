@@ -208,7 +208,7 @@ def test_flow_cache_is_exact_across_batches_resets_and_uploads(n_sets):
 @pytest.mark.parametrize("grid,tiles_per_cta", [(0, 2), (0, 1), (148, 3), (37, 2), (8, 1), (1, 2)])
 def test_partition_scan_is_exact_for_every_grid_and_skew(grid, tiles_per_cta):
     """Scan mode 5 routes keys to per-CTA shared-memory tables.  Small grids overflow
-    their 63-entry bins constantly (the producer's direct update), a few hot keys
+    their 31-entry bins constantly (the producers' overflow list and direct update), a few hot keys
     skew the buckets, the tables fill up; several launches per window; bits stay exact."""
     rng = np.random.default_rng(17)
     base_c, base_o = O.distinct_pairs(300_000, 77)
