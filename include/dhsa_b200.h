@@ -116,10 +116,11 @@ int dhsa_set_stream(dhsa_sketch_t *s, void *cuda_stream);
 int dhsa_set_own_stream(dhsa_sketch_t *s);
 int dhsa_get_stream(dhsa_sketch_t *s, void **cuda_stream);
 int dhsa_set_scan_mode(dhsa_sketch_t *s, int mode);
-/* Flow cache of DHSA_SCAN_FLOW_CACHE: n_sets sets x 32 bytes (default 2^21 -> 64 MiB,
- * allocated on first use; 1024 <= n_sets <= 2^27).  The cache only ever skips a packet whose
- * exact (cand, opp) pair was already scanned into this sketch since its last reset, so the
- * bits are identical with or without it.  stats: pairs looked up / found since the reset. */
+/* Flow cache of DHSA_SCAN_FLOW_CACHE: sets of 8 keys x 4 bytes = 32 bytes.  n_sets is rounded
+ * down to a power of two and up to 2g (default 2^20 -> 32 MiB, allocated on first use;
+ * 1024 <= n_sets <= 2^27).  The cache only ever skips a packet whose exact key (cand, h1(opp))
+ * -- all its bits depend on -- was already scanned into this sketch since its last reset, so
+ * the bits are identical with or without it.  stats: keys looked up / found since the reset. */
 int dhsa_set_flow_cache(dhsa_sketch_t *s, uint64_t n_sets);
 int dhsa_flow_cache_stats(dhsa_sketch_t *s, uint64_t *lookups, uint64_t *hits);
 /* DHSA_SCAN_PARTITION tuning and counters.  grid: CTAs = key buckets (0 = one per SM);

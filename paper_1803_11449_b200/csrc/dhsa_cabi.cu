@@ -216,7 +216,7 @@ extern "C" int dhsa_create(const dhsa_params_t *params, int device, dhsa_sketch_
     s->device = device;
     CU(cudaDeviceGetAttribute(&s->sm_count, cudaDevAttrMultiProcessorCount, device));
     s->scan_mode = DHSA_SCAN_AUTO;
-    s->fc_sets = 1u << 21;
+    s->fc_sets = 1u << 20;
     s->pt_tiles_per_cta = 2;
     const uint64_t m = 1ull << params->k;
     s->nbytes = (uint64_t)params->r * m * ((uint64_t)params->g / 8);
@@ -305,9 +305,23 @@ static int clear_flow_cache_locked(dhsa_sketch *s)
     return DHSA_OK;
 }
 
+// Sets actually allocated for a requested size: the largest power of two not above it, and at
+// least 2g sets -- a 32-bit entry holds the 32 - log2(sets) key bits the set index leaves plus
+// log2(g) bits of h1(opp), and one value is reserved for "empty".
+static int flow_cache_log2_sets(const dhsa_sketch *s)
+{
+    int l = 0;
+    while ((2ull << l) <= (uint64_t)s->fc_sets) l++;
+    if (l < s->dp.log2g + 1) l = s->dp.log2g + 1;
+    return l;
+}
+
+static bool flow_cache_supported(const dhsa_sketch *s) { return s->dp.log2g + 1 <= 27; }
+
 static int ensure_flow_cache_locked(dhsa_sketch *s)
 {
-    if (s->fcache && s->dp.fc_sets == s->fc_sets) return DHSA_OK;
+    const uint32_t sets = 1u << flow_cache_log2_sets(s);
+    if (s->fcache && s->dp.fc_sets == sets) return DHSA_OK;
     CU(cudaStreamSynchronize(s->stream));
     cudaFree(s->fcache);
     s->fcache = nullptr;
@@ -317,8 +331,9 @@ static int ensure_flow_cache_locked(dhsa_sketch *s)
         CU(cudaEventCreateWithFlags(&s->fc_stats_ev, cudaEventDisableTiming));
         s->fc_stats_host[0] = s->fc_stats_host[1] = 0;
     }
-    CU(cudaMalloc(&s->fcache, (size_t)32 * s->fc_sets));
-    s->dp.fc_sets = s->fc_sets;
+    CU(cudaMalloc(&s->fcache, (size_t)32 * sets));
+    s->dp.fc_sets = sets;
+    s->dp.fc_shift = 32 - flow_cache_log2_sets(s);
     s->dp.fcache = s->fcache;
     s->dp.fc_stats = s->fc_stats;
     s->fc_dirty = true;
@@ -328,7 +343,7 @@ static int ensure_flow_cache_locked(dhsa_sketch *s)
 extern "C" int dhsa_set_flow_cache(dhsa_sketch_t *s, uint64_t n_sets)
 {
     NEED(s);
-    if (n_sets < 1024 || n_sets > (1ull << 27))  // slot indices are 32-bit with 0xFFFFFFFF reserved: sets * 4 < 2^32
+    if (n_sets < 1024 || n_sets > (1ull << 27))  // slot indices are 32-bit with 0xFFFFFFFF reserved: sets * 8 < 2^32
         return fail(DHSA_ECONFIG, "flow cache size must satisfy 1024 <= n_sets <= 2^27 (got %llu)",
                     (unsigned long long)n_sets);
     std::lock_guard<std::mutex> lk(s->mu);
@@ -583,6 +598,7 @@ static int pick_scan_mode_locked(dhsa_sketch *s)
         mode = s->auto_fell_back ? DHSA_SCAN_TEST_AGG_RED : DHSA_SCAN_FLOW_CACHE;
     }
     if (mode == DHSA_SCAN_PARTITION && !partition_supported(s)) mode = DHSA_SCAN_FLOW_CACHE;
+    if (mode == DHSA_SCAN_FLOW_CACHE && !flow_cache_supported(s)) mode = DHSA_SCAN_TEST_AGG_RED;
     return mode;
 }
 

@@ -25,9 +25,10 @@ struct DevParams {
     uint64_t state_dh0, state_h1;
     uint64_t ncell;   // r * 2^k
     uint64_t nwords;  // 32-bit words backing the bit array (allocation is padded to 16 B)
-    // flow cache (scan mode 3): fc_sets sets of 4 ways x 8 B, one 32-byte sector per set
+    // flow cache (scan mode 3): fc_sets (a power of two) sets of 8 ways x 4 B, one 32-byte sector per set
     unsigned long long *fcache;
     uint32_t fc_sets;
+    int fc_shift;                  // 32 - log2(fc_sets): set = a >> fc_shift
     unsigned long long *fc_stats;  // [0] lookups, [1] hits
 };
 
@@ -72,6 +73,61 @@ __device__ __forceinline__ uint32_t dh0_of(const DevParams &p, uint64_t a)
 __device__ __forceinline__ uint32_t index_of(const DevParams &p, uint64_t a, uint32_t d0, int i)
 {
     return i == 0 ? d0 : (((uint32_t)(a >> ((i - 1) * p.alpha)) & p.kmask) ^ d0);
+}
+
+// The dedup key of a packet.  Its R bits depend on (cand, h1(opp)) only (_core.pyx:78-86), so
+// both "seen before" tables key on that pair -- 32 + log2(g) bits, 42 at the defaults -- not on
+// the 64-bit (cand, opp), and a scanner's thousands of flows collapse to at most g keys.
+// a = fmix32(cand ^ h * C) is a bijection of cand for every h (murmur3's 32-bit finaliser), so
+// (a, h) still identifies the key: a table indexed by some bits of a only has to store the rest.
+#define DHSA_KEY_MUL 0x9E3779B1u
+
+__device__ __forceinline__ uint32_t fmix32(uint32_t a)
+{
+    a ^= a >> 16;
+    a *= 0x85EBCA6Bu;
+    a ^= a >> 13;
+    a *= 0xC2B2AE35u;
+    a ^= a >> 16;
+    return a;
+}
+
+__device__ __forceinline__ uint32_t unfmix32(uint32_t a)
+{
+    a ^= a >> 16;
+    a *= 0x7ED1B41Du;  // inverse of 0xC2B2AE35 modulo 2^32
+    a ^= a >> 13;
+    a ^= a >> 26;
+    a *= 0xA5CB9243u;  // inverse of 0x85EBCA6B modulo 2^32
+    a ^= a >> 16;
+    return a;
+}
+
+// h1(opp) = mix64(state_h1 ^ opp) & (g - 1) (dhg.py:141-143) with the high word of the first
+// two steps folded into per-thread constants: opp only reaches the low word of state_h1 ^ opp.
+struct H1Consts {
+    uint32_t s_lo, k_shift, m1_hi_term;
+};
+
+__device__ __forceinline__ H1Consts h1_consts(uint64_t state_h1)
+{
+    const uint32_t s_hi = (uint32_t)(state_h1 >> 32);
+    H1Consts c;
+    c.s_lo = (uint32_t)state_h1;
+    c.k_shift = s_hi << 2;                               // bits the first xorshift moves into the low word
+    c.m1_hi_term = (s_hi ^ (s_hi >> 30)) * 0x1CE4E5B9u;  // (high word after the xorshift) * low(M1)
+    return c;
+}
+
+__device__ __forceinline__ uint32_t h1_fast(const H1Consts &c, uint32_t opp, uint32_t gmask)
+{
+    uint32_t xl = c.s_lo ^ opp;
+    xl ^= (xl >> 30) | c.k_shift;                        // z ^= z >> 30, low word
+    uint64_t z = (uint64_t)xl * 0x1CE4E5B9u;             // z *= 0xBF58476D1CE4E5B9
+    z += (uint64_t)(xl * 0xBF58476Du + c.m1_hi_term) << 32;
+    z ^= z >> 27;
+    z *= 0x94D049BB133111EBULL;
+    return ((uint32_t)z ^ (uint32_t)(z >> 31)) & gmask;
 }
 
 // ---------------------------------------------------------- memory helpers --
@@ -122,7 +178,7 @@ __device__ __forceinline__ uint32_t ld_sketch(const uint32_t *ptr)
     return v;
 }
 
-// One flow-cache set: 4 ways x 8 B = one 32-byte sector, fetched with a single
+// One flow-cache set: 8 ways x 4 B = one 32-byte sector, fetched with a single
 // 256-bit load (sm_100a).  Served from L2 only: the table is far larger than L1.
 __device__ __forceinline__ void ld_fc_set(const unsigned long long *set, unsigned long long (&e)[4])
 {
@@ -132,9 +188,9 @@ __device__ __forceinline__ void ld_fc_set(const unsigned long long *set, unsigne
                  : "memory");
 }
 
-__device__ __forceinline__ void st_fc_way(unsigned long long *slot, unsigned long long v)
+__device__ __forceinline__ void st_fc_way(uint32_t *slot, uint32_t v)
 {
-    asm volatile("st.global.cg.u64 [%0], %1;" ::"l"(slot), "l"(v) : "memory");
+    asm volatile("st.global.cg.u32 [%0], %1;" ::"l"(slot), "r"(v) : "memory");
 }
 
 // Fire-and-forget atomic OR (SASS: RED.E.OR), resolved in the L2 slice that owns the word.
@@ -436,54 +492,47 @@ __global__ void __launch_bounds__(256) k_scan_vec4(SRC src, uint32_t *__restrict
 // ncu shows k_scan_vec4 pinned at one L1-miss request per clock per SM
 // (l1tex__m_l1tex2xbar_req_cycles_active 92%) with 5 sketch sectors per packet,
 // so the lever is fewer scattered accesses per packet.  Real windows carry many
-// packets per flow (BASELINE config 2: ~26), and a repeated (cand, opp) pair
-// changes nothing in the sketch.  The cache is a 4-way set-associative table of
-// whole pairs in L2, one 32-byte sector per set, read with a single 256-bit load:
-// a packet whose pair is present was scanned earlier in this window and is
-// dropped after ONE scattered access instead of five.
+// packets per flow (BASELINE config 2: ~26), and a repeated key changes nothing
+// in the sketch.  The cache is an 8-way set-associative table of keys in L2, one
+// 32-byte sector per set, read with a single 256-bit load: a packet whose key is
+// present was scanned earlier in this window and is dropped after ONE scattered
+// access instead of five.
 //
+//   key        (cand, h = h1(opp)), see fmix32 above.  set = top bits of
+//              a = fmix32(cand ^ h * C); the entry is the rest of (a, h) plus one
+//              (0 = empty): 32 bits instead of the 64-bit pair, so the same number of
+//              keys needs half the L2 -- ncu showed a third of the lookups of a 64 MiB
+//              pair table served from HBM -- and a set holds 8 ways instead of 4.
+//              (set, entry) determines (a, h), hence (cand, h): a hit is never another key.
 //   exactness  an entry is written only by a lane that has just issued the
-//              pair's own test+RED, the table is cleared whenever bits can
+//              key's own test+RED, the table is cleared whenever bits can
 //              disappear (reset, upload), and nothing reads bits before the
 //              kernel ends -- so "present => bits set at kernel end" always holds
-//              and a missing / evicted / racing entry only costs a rescan.
-//   encoding   entries hold ~pair, 0 = empty; the all-ones pair therefore never
-//              hits and is always rescanned.
+//              and a missing / racing entry only costs a rescan.
 //   misses     are compacted by ballot into a per-warp shared-memory queue and
 //              drained 32 at a time, one missed packet per lane with its R test
 //              loads in flight together, so a miss costs one more L2 round trip
 //              per 32 misses, not per packet slot.
-//   pipeline   the next trip's packets are requested before this trip's table
-//              sets are consumed.
+//   pipeline   the packet stream is staged by TMA, several trips ahead.
 
 #define DHSA_FC_NO_SLOT 0xFFFFFFFFu
 #ifndef DHSA_FC_SKIP_TEST
 #define DHSA_FC_SKIP_TEST 1
 #endif
 struct FcMiss {
-    uint32_t cand, opp, slot;  // slot = set * 4 + way to fill, or DHSA_FC_NO_SLOT when the set was full
+    uint32_t cand, h, slot;  // slot = set * 8 + way to fill, or DHSA_FC_NO_SLOT when the set was full
 };
 
-// Set (and victim way) of a pair from a 32-bit multiply-xorshift of (cand, opp): ~8 integer
-// instructions.  The sketch's own splitmix64 hashes (~90 instructions per packet) are computed
-// only for the packets that miss, in the drain -- ncu showed the front end issue-limited at 520
-// warp-instructions per 128 packets when it derived the set from them.  The table is a cache:
-// the index hash affects the hit rate, never the result.  Multiply-shift range reduction, so
-// any set count works, not only powers of two.
-// (A second-choice set probed on a miss was tried: hit rate 0.925 -> 0.953 at 64 MiB, but the
-// heavier drain made the scan 20% slower -- profiles/r01_flowcache_variants.txt.)
-__device__ __forceinline__ uint32_t fc_hash32(uint32_t cand, uint32_t opp)
+// (set, entry) of a key in a table of 2^(32 - shift) sets
+__device__ __forceinline__ void fc_locate(const DevParams &p, uint32_t cand, uint32_t h, uint32_t &set, uint32_t &entry)
 {
-    uint32_t z = (cand ^ 0x7F4A7C15u) * 0x9E3779B1u;
-    z ^= (opp + 0x165667B1u) * 0x85EBCA77u;
-    z ^= z >> 16;
-    z *= 0x7FEB352Du;
-    z ^= z >> 15;
-    return z;
+    const uint32_t a = fmix32(cand ^ (h * DHSA_KEY_MUL));
+    set = a >> p.fc_shift;
+    entry = (((a & ((1u << p.fc_shift) - 1u)) << p.log2g) | h) + 1u;  // fc_shift + log2(g) <= 31
 }
 
 // Drain up to 32 queued misses, one per lane: the R test loads of a lane are in flight
-// together, REDs are warp-aggregated, then the pair is recorded in the table.
+// together, REDs are warp-aggregated, then the key is recorded in the table.
 template <int R>
 __device__ __forceinline__ void fc_drain32(uint32_t *__restrict__ words, const DevParams &p, int wshift,
                                            const FcMiss *q, uint32_t n_active, uint32_t lane)
@@ -491,23 +540,25 @@ __device__ __forceinline__ void fc_drain32(uint32_t *__restrict__ words, const D
     const bool act = lane < n_active;
     FcMiss m = {0u, 0u, 0u};
     if (act) m = q[lane];
-    const uint32_t h = (uint32_t)mix64(p.state_h1 ^ (uint64_t)m.opp) & p.gmask;
     const uint32_t d0 = (uint32_t)mix64(p.state_dh0 ^ (uint64_t)m.cand) & p.kmask;
-    const uint32_t mask = 1u << (h & 31u);
+    const uint32_t mask = 1u << (m.h & 31u);
     uint32_t widx[R], w[R];
-    packet_slots<R>(p, wshift, m.cand, h, d0, widx);
-    // A pair that found an empty way in its set was never recorded in this window (sets are never
-    // evicted), so it is almost surely a new flow whose bits are still clear: skip the test loads and
-    // RED unconditionally (a RED costs ~1.5 loads in L2, a test that finds the bit clear costs both).
-    // Pairs from full sets are usually repeats whose bits are set: those test first.
+    packet_slots<R>(p, wshift, m.cand, m.h, d0, widx);
+    // A key that found an empty way in its set was never recorded in this window (sets are never
+    // evicted), so it is almost surely new and its bits still clear: skip the test loads and RED
+    // unconditionally (a RED costs ~1.5 loads in L2, a test that finds the bit clear costs both).
+    // Keys from full sets are usually repeats whose bits are set: those test first.
     const bool fresh = DHSA_FC_SKIP_TEST && m.slot != DHSA_FC_NO_SLOT;
 #pragma unroll
     for (int i = 0; i < R; i++) w[i] = act ? (fresh ? 0u : ld_sketch(words + widx[i])) : 0xFFFFFFFFu;
 #pragma unroll
     for (int i = 0; i < R; i++) red_or_aggregated(words, widx[i], mask, (w[i] & mask) == 0, lane);
-    // the pair now counts as scanned: its tests/REDs above are issued before this store
-    if (act && m.slot != DHSA_FC_NO_SLOT)
-        st_fc_way(p.fcache + m.slot, ~(((unsigned long long)m.cand << 32) | (unsigned long long)m.opp));
+    // the key now counts as scanned: its tests/REDs above are issued before this store
+    if (act && m.slot != DHSA_FC_NO_SLOT) {
+        uint32_t set, entry;
+        fc_locate(p, m.cand, m.h, set, entry);
+        st_fc_way(reinterpret_cast<uint32_t *>(p.fcache) + m.slot, entry);
+    }
 }
 
 // The packet stream is staged by TMA: every warp owns a ring of SRC::kStages
@@ -530,7 +581,8 @@ __global__ void __launch_bounds__(256, 3) k_scan_flowcache(SRC src, uint32_t *__
     const int wshift = p.log2g - 5;
     const uint64_t pol = policy_evict_first();
     const uint32_t lt_mask = (1u << lane) - 1u;
-    unsigned long long fc_hits = 0, fc_lookups = 0;
+    const H1Consts hc = h1_consts(p.state_h1);
+    uint32_t fc_hits = 0, fc_lookups = 0;  // per thread and launch: far below 2^32
     uint32_t on_time = 0, late = 0;
 
     if (lane == 0) {
@@ -574,34 +626,36 @@ __global__ void __launch_bounds__(256, 3) k_scan_flowcache(SRC src, uint32_t *__
         src.unpack(raw, base + lane, cs, os, ok, on_time, late);
 
         unsigned long long e[4][4];
-        uint32_t set_idx[4];
+        uint32_t set_idx[4], entry[4], hs[4];
 #pragma unroll
         for (int j = 0; j < 4; j++) {
-            const uint32_t z = fc_hash32(cs[j], os[j]);
-            set_idx[j] = __umulhi(z, p.fc_sets);
+            hs[j] = h1_fast(hc, os[j], p.gmask);
+            fc_locate(p, cs[j], hs[j], set_idx[j], entry[j]);
             if (ok[j]) ld_fc_set(p.fcache + ((size_t)set_idx[j] << 2), e[j]);
         }
 #pragma unroll
         for (int j = 0; j < 4; j++) {
-            const unsigned long long inv_key = ~(((unsigned long long)cs[j] << 32) | (unsigned long long)os[j]);
-            const bool hit = ok[j] && inv_key != 0ull &&
-                             (e[j][0] == inv_key || e[j][1] == inv_key || e[j][2] == inv_key || e[j][3] == inv_key);
+            uint32_t way[8];
+#pragma unroll
+            for (int t = 0; t < 4; t++) way[2 * t] = (uint32_t)e[j][t], way[2 * t + 1] = (uint32_t)(e[j][t] >> 32);
+            bool hit = false;
+#pragma unroll
+            for (int t = 0; t < 8; t++) hit |= way[t] == entry[j];
+            hit = hit && ok[j];
             const bool miss = ok[j] && !hit;
             fc_hits += hit;
             fc_lookups += ok[j];
             const unsigned bal = __ballot_sync(0xFFFFFFFFu, miss);
             if (bal == 0) continue;
             if (miss) {
-                // first empty way of the set as loaded, else a hashed victim (a race only loses an entry)
-                // record the pair in the first empty way of its set as loaded; a full set keeps its
-                // entries (no eviction: measured 7% faster than a hashed victim -- evicting a live flow
-                // only moves the miss to another flow and costs a store; the table empties with every window)
-                uint32_t slot = DHSA_FC_NO_SLOT;
-                if (e[j][3] == 0ull) slot = (set_idx[j] << 2) | 3u;
-                if (e[j][2] == 0ull) slot = (set_idx[j] << 2) | 2u;
-                if (e[j][1] == 0ull) slot = (set_idx[j] << 2) | 1u;
-                if (e[j][0] == 0ull) slot = (set_idx[j] << 2) | 0u;
-                FcMiss m = {cs[j], os[j], slot};
+                // record the key in the first empty way of its set as loaded; a full set keeps its
+                // entries (no eviction: evicting a live key only moves the miss to another key and
+                // costs a store; the table empties with every window).  A race only loses an entry.
+                uint32_t fill = DHSA_FC_NO_SLOT;
+#pragma unroll
+                for (int t = 7; t >= 0; t--)
+                    if (way[t] == 0u) fill = (set_idx[j] << 3) | (uint32_t)t;
+                FcMiss m = {cs[j], hs[j], fill};
                 q[qn + __popc(bal & lt_mask)] = m;
             }
             qn += __popc(bal);
@@ -614,13 +668,14 @@ __global__ void __launch_bounds__(256, 3) k_scan_flowcache(SRC src, uint32_t *__
         __syncwarp();
     }
     if (qn) fc_drain32<R>(words, p, wshift, q, qn, lane);
+    unsigned long long hits64 = fc_hits, lookups64 = fc_lookups;
     for (int d = 16; d > 0; d >>= 1) {
-        fc_hits += __shfl_xor_sync(0xFFFFFFFFu, fc_hits, d);
-        fc_lookups += __shfl_xor_sync(0xFFFFFFFFu, fc_lookups, d);
+        hits64 += __shfl_xor_sync(0xFFFFFFFFu, hits64, d);
+        lookups64 += __shfl_xor_sync(0xFFFFFFFFu, lookups64, d);
     }
-    if (lane == 0 && fc_lookups) {
-        atomicAdd(p.fc_stats + 0, fc_lookups);
-        atomicAdd(p.fc_stats + 1, fc_hits);
+    if (lane == 0 && lookups64) {
+        atomicAdd(p.fc_stats + 0, lookups64);
+        atomicAdd(p.fc_stats + 1, hits64);
     }
     flush_tally(src, on_time, late, lane);
 }

@@ -77,57 +77,6 @@ struct PartParams {
     uint32_t tiles_per_cta;     // tiles every CTA produces per chunk
 };
 
-// murmur3's 32-bit finaliser and its inverse: a bijection on 32-bit words
-__device__ __forceinline__ uint32_t pt_fmix32(uint32_t a)
-{
-    a ^= a >> 16;
-    a *= 0x85EBCA6Bu;
-    a ^= a >> 13;
-    a *= 0xC2B2AE35u;
-    a ^= a >> 16;
-    return a;
-}
-
-__device__ __forceinline__ uint32_t pt_unfmix32(uint32_t a)
-{
-    a ^= a >> 16;
-    a *= 0x7ED1B41Du;  // inverse of 0xC2B2AE35 modulo 2^32
-    a ^= a >> 13;
-    a ^= a >> 26;
-    a *= 0xA5CB9243u;  // inverse of 0x85EBCA6B modulo 2^32
-    a ^= a >> 16;
-    return a;
-}
-
-#define DHSA_PT_KEY_MUL 0x9E3779B1u
-
-// h1(opp) = mix64(state_h1 ^ opp) & (g - 1) (dhg.py:141-143) with the high word of the first
-// two steps folded into per-thread constants: opp only reaches the low word of state_h1 ^ opp.
-struct H1Consts {
-    uint32_t s_lo, k_shift, m1_hi_term;
-};
-
-__device__ __forceinline__ H1Consts pt_h1_consts(uint64_t state_h1)
-{
-    const uint32_t s_hi = (uint32_t)(state_h1 >> 32);
-    H1Consts c;
-    c.s_lo = (uint32_t)state_h1;
-    c.k_shift = s_hi << 2;                                  // bits the first xorshift moves into the low word
-    c.m1_hi_term = (s_hi ^ (s_hi >> 30)) * 0x1CE4E5B9u;     // (high word after the xorshift) * low(M1)
-    return c;
-}
-
-__device__ __forceinline__ uint32_t pt_h1(const H1Consts &c, uint32_t opp, uint32_t gmask)
-{
-    uint32_t xl = c.s_lo ^ opp;
-    xl ^= (xl >> 30) | c.k_shift;                                           // z ^= z >> 30, low word
-    uint64_t z = (uint64_t)xl * 0x1CE4E5B9u;                                // z *= 0xBF58476D1CE4E5B9
-    z += (uint64_t)(xl * 0xBF58476Du + c.m1_hi_term) << 32;
-    z ^= z >> 27;
-    z *= 0x94D049BB133111EBULL;
-    return ((uint32_t)z ^ (uint32_t)(z >> 31)) & gmask;
-}
-
 __device__ __forceinline__ void bar_sync_named(int id, int count)
 {
     asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory");
@@ -211,7 +160,7 @@ __device__ __forceinline__ void pt_drain32(uint32_t *__restrict__ words, const D
     // invert the bijection
     const uint32_t a = (uint32_t)(rem >> p.log2g) + lo32;
     const uint32_t h = ((uint32_t)rem ^ (a >> 11)) & p.gmask;
-    const uint32_t cand = pt_unfmix32(a) ^ (h * DHSA_PT_KEY_MUL);
+    const uint32_t cand = unfmix32(a) ^ (h * DHSA_KEY_MUL);
     const uint32_t d0 = (uint32_t)mix64(p.state_dh0 ^ (uint64_t)cand) & p.kmask;
     const uint32_t mask = 1u << (h & 31u);
     uint32_t widx[R], w[R];
@@ -255,7 +204,7 @@ __global__ void __launch_bounds__((DHSA_PT_PWARPS + DHSA_PT_CWARPS) * 32, 1)
         // ------------------------------------------------------------ producers --
         constexpr int NPT = DHSA_PT_PWARPS * 32;
         const uint64_t pol = policy_evict_first();
-        const H1Consts hc = pt_h1_consts(p.state_h1);
+        const H1Consts hc = h1_consts(p.state_h1);
         uint32_t on_time = 0, late = 0;
         unsigned long long direct = 0;
         typename SRC::Raw raw[DHSA_PT_VECS];
@@ -287,8 +236,8 @@ __global__ void __launch_bounds__((DHSA_PT_PWARPS + DHSA_PT_CWARPS) * 32, 1)
                     src.unpack(cur[v], g * DHSA_PT_TILE_VEC + (uint64_t)v * NPT + tid, cs, os, ok, on_time, late);
 #pragma unroll
                     for (int q = 0; q < 4; q++) {
-                        const uint32_t h = pt_h1(hc, os[q], p.gmask);
-                        const uint32_t a = pt_fmix32(cs[q] ^ (h * DHSA_PT_KEY_MUL));
+                        const uint32_t h = h1_fast(hc, os[q], p.gmask);
+                        const uint32_t a = fmix32(cs[q] ^ (h * DHSA_KEY_MUL));
                         const uint32_t b = __umulhi(a, nb);
                         const uint32_t bl = (h ^ (a >> 11)) & p.gmask;
                         const unsigned long long rem = ((unsigned long long)(a - lo_s[b]) << p.log2g) | bl;
