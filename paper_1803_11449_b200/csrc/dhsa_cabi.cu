@@ -298,7 +298,14 @@ extern "C" int dhsa_destroy(dhsa_sketch_t *s)
 static int clear_flow_cache_locked(dhsa_sketch *s)
 {
     if (!s->fcache || !s->fc_dirty) return DHSA_OK;
-    CU(cudaMemsetAsync(s->fcache, 0, (size_t)32 * s->dp.fc_sets, s->stream));
+    // entries carry the epoch they were written in: bumping it empties the table without touching it
+    const uint32_t epoch_max = (uint32_t)((1ull << (32 - s->dp.fc_tag_bits)) - 1);
+    if (s->dp.fc_epoch >= epoch_max) {
+        CU(cudaMemsetAsync(s->fcache, 0, (size_t)32 * s->dp.fc_sets, s->stream));
+        s->dp.fc_epoch = 1;
+    } else {
+        s->dp.fc_epoch++;
+    }
     CU(cudaMemsetAsync(s->fc_stats, 0, 2 * sizeof(unsigned long long), s->stream));
     s->fc_dirty = false;
     s->auto_fell_back = false;  // a new window may repeat flows again
@@ -307,7 +314,7 @@ static int clear_flow_cache_locked(dhsa_sketch *s)
 
 // Sets actually allocated for a requested size: the largest power of two not above it, and at
 // least 2g sets -- a 32-bit entry holds the 32 - log2(sets) key bits the set index leaves plus
-// log2(g) bits of h1(opp), and one value is reserved for "empty".
+// log2(g) bits of h1(opp), and needs at least one bit for the epoch.
 static int flow_cache_log2_sets(const dhsa_sketch *s)
 {
     int l = 0;
@@ -334,6 +341,8 @@ static int ensure_flow_cache_locked(dhsa_sketch *s)
     CU(cudaMalloc(&s->fcache, (size_t)32 * sets));
     s->dp.fc_sets = sets;
     s->dp.fc_shift = 32 - flow_cache_log2_sets(s);
+    s->dp.fc_tag_bits = s->dp.fc_shift + s->dp.log2g;  // <= 31: the table has at least 2g sets
+    s->dp.fc_epoch = (uint32_t)((1ull << (32 - s->dp.fc_tag_bits)) - 1);  // = epoch_max: the clear below zeroes the table
     s->dp.fcache = s->fcache;
     s->dp.fc_stats = s->fc_stats;
     s->fc_dirty = true;

@@ -29,6 +29,8 @@ struct DevParams {
     unsigned long long *fcache;
     uint32_t fc_sets;
     int fc_shift;                  // 32 - log2(fc_sets): set = a >> fc_shift
+    int fc_tag_bits;               // fc_shift + log2(g): key bits an entry stores
+    uint32_t fc_epoch;             // entries of other epochs count as empty: a window reset is epoch + 1
     unsigned long long *fc_stats;  // [0] lookups, [1] hits
 };
 
@@ -330,7 +332,10 @@ struct SoaSource {
     }
     // staged form: one warp trip = 32 vectors = 512 B of cand then 512 B of opp in shared memory
     static constexpr int kStageBytes = 1024;
-    static constexpr int kStages = 4;
+#ifndef DHSA_FC_SOA_STAGES
+#define DHSA_FC_SOA_STAGES 4
+#endif
+    static constexpr int kStages = DHSA_FC_SOA_STAGES;
     __device__ __forceinline__ void stage_issue(uint32_t smem_dst, uint32_t mbar, uint64_t base, uint32_t count,
                                                 uint64_t pol) const
     {
@@ -499,8 +504,9 @@ __global__ void __launch_bounds__(256) k_scan_vec4(SRC src, uint32_t *__restrict
 // access instead of five.
 //
 //   key        (cand, h = h1(opp)), see fmix32 above.  set = top bits of
-//              a = fmix32(cand ^ h * C); the entry is the rest of (a, h) plus one
-//              (0 = empty): 32 bits instead of the 64-bit pair, so the same number of
+//              a = fmix32(cand ^ h * C); the entry is the rest of (a, h) under the
+//              table's current epoch (>= 1; entries of other epochs are empty ways, so
+//              a window reset is epoch + 1, not a memset): 32 bits instead of the 64-bit pair, so the same number of
 //              keys needs half the L2 -- ncu showed a third of the lookups of a 64 MiB
 //              pair table served from HBM -- and a set holds 8 ways instead of 4.
 //              (set, entry) determines (a, h), hence (cand, h): a hit is never another key.
@@ -519,6 +525,9 @@ __global__ void __launch_bounds__(256) k_scan_vec4(SRC src, uint32_t *__restrict
 #ifndef DHSA_FC_SKIP_TEST
 #define DHSA_FC_SKIP_TEST 1
 #endif
+#ifndef DHSA_FC_CTAS_PER_SM
+#define DHSA_FC_CTAS_PER_SM 3
+#endif
 struct FcMiss {
     uint32_t cand, h, slot;  // slot = set * 8 + way to fill, or DHSA_FC_NO_SLOT when the set was full
 };
@@ -528,7 +537,7 @@ __device__ __forceinline__ void fc_locate(const DevParams &p, uint32_t cand, uin
 {
     const uint32_t a = fmix32(cand ^ (h * DHSA_KEY_MUL));
     set = a >> p.fc_shift;
-    entry = (((a & ((1u << p.fc_shift) - 1u)) << p.log2g) | h) + 1u;  // fc_shift + log2(g) <= 31
+    entry = (p.fc_epoch << p.fc_tag_bits) | ((a & ((1u << p.fc_shift) - 1u)) << p.log2g) | h;  // epoch >= 1
 }
 
 // Drain up to 32 queued misses, one per lane: the R test loads of a lane are in flight
@@ -566,7 +575,7 @@ __device__ __forceinline__ void fc_drain32(uint32_t *__restrict__ words, const D
 // cp.async.bulk copies (one warp trip per slot), all lanes wait on the slot's
 // mbarrier parity and read their 16-byte vectors with LDS.128.
 template <int R, typename SRC>
-__global__ void __launch_bounds__(256, 3) k_scan_flowcache(SRC src, uint32_t *__restrict__ words, DevParams p)
+__global__ void __launch_bounds__(256, DHSA_FC_CTAS_PER_SM) k_scan_flowcache(SRC src, uint32_t *__restrict__ words, DevParams p)
 {
     __shared__ FcMiss queue_s[8][32 + 128];
     __shared__ __align__(128) uint8_t stage_s[8][SRC::kStages][SRC::kStageBytes];
@@ -651,10 +660,15 @@ __global__ void __launch_bounds__(256, 3) k_scan_flowcache(SRC src, uint32_t *__
                 // record the key in the first empty way of its set as loaded; a full set keeps its
                 // entries (no eviction: evicting a live key only moves the miss to another key and
                 // costs a store; the table empties with every window).  A race only loses an entry.
-                uint32_t fill = DHSA_FC_NO_SLOT;
+                // Lanes that loaded the same (still empty) set at the same time would all pick its
+                // first empty way and overwrite each other: start the search at a key-dependent way.
+                uint32_t empty = 0;
 #pragma unroll
-                for (int t = 7; t >= 0; t--)
-                    if (way[t] == 0u) fill = (set_idx[j] << 3) | (uint32_t)t;
+                for (int t = 0; t < 8; t++) empty |= (uint32_t)((way[t] >> p.fc_tag_bits) != p.fc_epoch) << t;
+                const uint32_t rot = entry[j] & 7u;
+                const uint32_t turned = ((empty >> rot) | (empty << (8u - rot))) & 0xFFu;
+                const uint32_t fill =
+                    turned ? ((set_idx[j] << 3) | ((uint32_t)(__ffs(turned) - 1) + rot) & 7u) : DHSA_FC_NO_SLOT;
                 FcMiss m = {cs[j], hs[j], fill};
                 q[qn + __popc(bal & lt_mask)] = m;
             }

@@ -203,6 +203,18 @@ def test_flow_cache_is_exact_across_batches_resets_and_uploads(n_sets):
     sk.update_batch(base_c[pick], base_o[pick])
     fresh.update_batch(oc, oo)
     assert np.array_equal(sk.bits, fresh.bits)
+    # a reset bumps the table's epoch instead of clearing it; go around the epoch counter
+    # (31 epochs at 32768 sets, 1 at 2048) so stale entries of a recycled epoch would show
+    small_c, small_o = base_c[:5000], base_o[:5000]
+    want = O.OracleSketch()
+    want.update_batch(small_c, small_o)
+    for _ in range(40):
+        sk.reset()
+        sk.update_batch(small_c, small_o)
+        sk.update_batch(small_c, small_o)
+    assert np.array_equal(sk.bits, want.bits)
+    lookups, hits = sk.flow_cache_stats()
+    assert lookups == 10_000 and 2_500 <= hits <= 5_100       # the second pass of the last window hits (lost insert races aside)
 
 
 @pytest.mark.parametrize("grid,tiles_per_cta", [(0, 2), (0, 1), (148, 3), (37, 2), (8, 1), (1, 2)])
