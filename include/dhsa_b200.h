@@ -175,6 +175,16 @@ int dhsa_shared_zero_counts(dhsa_sketch_t *s, const uint64_t *hosts_host, uint64
  * the true count (DHSA_EDATA if it exceeds reports_cap). */
 int dhsa_restore(dhsa_sketch_t *s, double theta, uint64_t max_candidates,
                  dhsa_report_t *reports_host, uint64_t reports_cap, dhsa_restore_info_t *info);
+/* The same read-out in two halves, for callers that keep the GPU busy: _begin enqueues the
+ * whole chain and returns at once; the caller may queue the next window's reset and scan on
+ * this sketch (stream order keeps them behind the read-out) and then collect the reports with
+ * _end, which waits only for the read-out.  WindowSession.restore (pkg/src/dhsa/engine.py:96-103)
+ * of window k then overlaps the feed of window k + 1.  One read-out may be pending per sketch;
+ * other read-out calls fail with DHSA_ECONFIG until it is collected.  _end with too small a
+ * buffer returns DHSA_EDATA and leaves the read-out collectable. */
+int dhsa_restore_begin(dhsa_sketch_t *s, double theta, uint64_t max_candidates);
+int dhsa_restore_end(dhsa_sketch_t *s, dhsa_report_t *reports_host, uint64_t reports_cap,
+                     dhsa_restore_info_t *info);
 
 /* ---- record streams: the window engine's per-record work, fused into the scan --------
  * Records are the reference's 12-byte IPPR trace records (pkg/src/dhsa/ingest.py:20): u32

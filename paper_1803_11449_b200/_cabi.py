@@ -72,6 +72,8 @@ SIGNATURES = {
     "dhsa_candidate_hosts": [_vp, C.c_double, _u64, _vp, _u64, C.POINTER(RestoreInfo)],
     "dhsa_shared_zero_counts": [_vp, _vp, _u64, _vp],
     "dhsa_restore": [_vp, C.c_double, _u64, _vp, _u64, C.POINTER(RestoreInfo)],
+    "dhsa_restore_begin": [_vp, C.c_double, _u64],
+    "dhsa_restore_end": [_vp, _vp, _u64, C.POINTER(RestoreInfo)],
     "dhsa_plan_windows": [_vp, _vp, _u64, C.c_uint32, C.c_int64, _vp, C.c_uint32, C.POINTER(C.c_uint32)],
     "dhsa_update_records_device": [_vp, _vp, _u64, _u64, _u64, C.c_uint32, C.c_uint32, C.c_int],
     "dhsa_record_tally": [_vp, C.POINTER(_u64), C.POINTER(_u64)],

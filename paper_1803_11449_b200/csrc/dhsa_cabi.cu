@@ -114,6 +114,9 @@ struct dhsa_sketch {
     uint64_t graph_kernels;
     bool graph_disabled;
     ReportOut *reports_pinned;      // the first kPinnedReports rows land here with the control block
+    cudaEvent_t restore_ev;         // read-out enqueued by dhsa_restore_begin has landed in the pinned mirrors
+    bool restore_pending;
+    uint64_t restore_max_candidates;
 
     // record streams
     unsigned long long *tally;      // device: records fed, records dropped
@@ -243,6 +246,7 @@ extern "C" int dhsa_create(const dhsa_params_t *params, int device, dhsa_sketch_
     CU(cudaMemsetAsync(s->tally, 0, 2 * sizeof(unsigned long long), s->stream));
     CU(cudaMallocHost(&s->ctl_host, sizeof(Control)));
     CU(cudaMallocHost(&s->reports_pinned, kPinnedReports * sizeof(ReportOut)));
+    CU(cudaEventCreateWithFlags(&s->restore_ev, cudaEventDisableTiming));
     s->graph_disabled = getenv("DHSA_NO_GRAPH") != nullptr;
     CU(cudaMemsetAsync(s->bits, 0, s->alloc_bytes, s->stream));
     CU(cudaMemsetAsync(s->ctl, 0, sizeof(Control), s->stream));
@@ -286,6 +290,7 @@ extern "C" int dhsa_destroy(dhsa_sketch_t *s)
     cudaFree(s->ctl);
     cudaFreeHost(s->ctl_host);
     cudaFreeHost(s->reports_pinned);
+    cudaEventDestroy(s->restore_ev);
     if (s->restore_graph) cudaGraphExecDestroy(s->restore_graph);
     cudaStreamDestroy(s->own_stream);
     cudaStreamDestroy(s->copy_stream);
@@ -988,6 +993,8 @@ static int launch_zero_counts(dhsa_sketch *s)
     return DHSA_OK;
 }
 
+static int refuse_if_restore_pending(const dhsa_sketch *s);
+
 // K2 + hot sets + scalars, stream-ordered.
 static int launch_estimate(dhsa_sketch *s, double theta)
 {
@@ -1071,6 +1078,7 @@ extern "C" int dhsa_zero_counts(dhsa_sketch_t *s, int64_t *zc_host, int64_t *zr_
     NEED(zc_host);
     std::lock_guard<std::mutex> lk(s->mu);
     if (int rc = use_device(s)) return rc;
+    if (int rc = refuse_if_restore_pending(s)) return rc;
     if (int rc = launch_estimate(s, 0.0)) return rc;
     // widen on the host side of the copy: device keeps int32, the reference API is int64
     int32_t *tmp = nullptr;
@@ -1096,6 +1104,7 @@ extern "C" int dhsa_hot_sets(dhsa_sketch_t *s, double theta, uint64_t *lists_hos
     NEED(counts_host);
     std::lock_guard<std::mutex> lk(s->mu);
     if (int rc = use_device(s)) return rc;
+    if (int rc = refuse_if_restore_pending(s)) return rc;
     if (int rc = launch_estimate(s, theta)) return rc;
     if (int rc = read_control(s)) return rc;
     const uint64_t m = 1ull << s->params.k;
@@ -1125,6 +1134,7 @@ extern "C" int dhsa_estimate(dhsa_sketch_t *s, double theta, dhsa_restore_info_t
     NEED(info);
     std::lock_guard<std::mutex> lk(s->mu);
     if (int rc = use_device(s)) return rc;
+    if (int rc = refuse_if_restore_pending(s)) return rc;
     if (int rc = launch_estimate(s, theta)) return rc;
     if (int rc = read_control(s)) return rc;
     fill_info(s, info);
@@ -1145,6 +1155,7 @@ extern "C" int dhsa_candidate_hosts(dhsa_sketch_t *s, double theta, uint64_t max
     NEED(s);
     std::lock_guard<std::mutex> lk(s->mu);
     if (int rc = use_device(s)) return rc;
+    if (int rc = refuse_if_restore_pending(s)) return rc;
     if (int rc = launch_estimate(s, theta)) return rc;
     if (int rc = launch_restore_stages(s, max_candidates)) return rc;
     k_sort_small<<<1, 1024, DHSA_SORT_SMEM_MAX * sizeof(uint64_t), s->stream>>>(s->keys, &s->ctl->n_candidates, s->ctl);
@@ -1260,28 +1271,48 @@ static int run_restore(dhsa_sketch *s, double theta, uint64_t max_candidates)
         if (s->restore_graph) {
             CU(cudaGraphLaunch(s->restore_graph, s->stream));
             s->launches += s->graph_kernels;
-            CU(cudaStreamSynchronize(s->stream));
             return DHSA_OK;
         }
     }
-    if (int rc = enqueue_restore(s, theta, max_candidates)) return rc;
-    CU(cudaStreamSynchronize(s->stream));
+    return enqueue_restore(s, theta, max_candidates);
+}
+
+// A read-out call that uses the pinned mirrors while a begun restore has not been collected
+static int refuse_if_restore_pending(const dhsa_sketch *s)
+{
+    if (s->restore_pending)
+        return fail(DHSA_ECONFIG, "a restore begun with dhsa_restore_begin has not been collected with dhsa_restore_end");
     return DHSA_OK;
 }
 
-extern "C" int dhsa_restore(dhsa_sketch_t *s, double theta, uint64_t max_candidates, dhsa_report_t *reports_host,
-                            uint64_t reports_cap, dhsa_restore_info_t *info)
+static int restore_begin_locked(dhsa_sketch *s, double theta, uint64_t max_candidates)
 {
-    NEED(s);
-    std::lock_guard<std::mutex> lk(s->mu);
-    if (int rc = use_device(s)) return rc;
+    if (int rc = refuse_if_restore_pending(s)) return rc;
     if (int rc = run_restore(s, theta, max_candidates)) return rc;
+    CU(cudaEventRecord(s->restore_ev, s->stream));
+    s->restore_pending = true;
+    s->restore_max_candidates = max_candidates;
+    return DHSA_OK;
+}
+
+static int restore_end_locked(dhsa_sketch *s, dhsa_report_t *reports_host, uint64_t reports_cap,
+                              dhsa_restore_info_t *info)
+{
+    if (!s->restore_pending) return fail(DHSA_ECONFIG, "dhsa_restore_end without dhsa_restore_begin");
+    CU(cudaEventSynchronize(s->restore_ev));
+    const uint64_t max_candidates = s->restore_max_candidates;
     if (s->ctl_host->fail_stage) {
+        s->restore_pending = false;
         fill_info(s, info);
         return capacity_error(s, max_candidates);
     }
     const int grid = s->sm_count * 4;
     const uint64_t n = s->ctl_host->n_reports;
+    fill_info(s, info);
+    // too small an output buffer: the read-out stays collectable, the caller retries with n_reports rows
+    if (n > reports_cap) return fail(DHSA_EDATA, "%llu reports exceed the output capacity %llu",
+                                     (unsigned long long)n, (unsigned long long)reports_cap);
+    s->restore_pending = false;
     bool in_pinned = n <= kPinnedReports;
     if (n > DHSA_SORT_SMEM_MAX) {  // rare: the single-CTA sorter declined, sort with global passes and re-emit
         if (int rc = sort_large(s, s->packed, n)) return rc;
@@ -1290,9 +1321,6 @@ extern "C" int dhsa_restore(dhsa_sketch_t *s, double theta, uint64_t max_candida
         CU(cudaGetLastError());
         in_pinned = false;
     }
-    fill_info(s, info);
-    if (n > reports_cap) return fail(DHSA_EDATA, "%llu reports exceed the output capacity %llu",
-                                     (unsigned long long)n, (unsigned long long)reports_cap);
     if (n) {
         NEED(reports_host);
         static_assert(sizeof(ReportOut) == sizeof(dhsa_report_t), "report layouts must match");
@@ -1304,6 +1332,35 @@ extern "C" int dhsa_restore(dhsa_sketch_t *s, double theta, uint64_t max_candida
         }
     }
     return DHSA_OK;
+}
+
+extern "C" int dhsa_restore(dhsa_sketch_t *s, double theta, uint64_t max_candidates, dhsa_report_t *reports_host,
+                            uint64_t reports_cap, dhsa_restore_info_t *info)
+{
+    NEED(s);
+    std::lock_guard<std::mutex> lk(s->mu);
+    if (int rc = use_device(s)) return rc;
+    if (int rc = restore_begin_locked(s, theta, max_candidates)) return rc;
+    const int rc = restore_end_locked(s, reports_host, reports_cap, info);
+    s->restore_pending = false;  // one call: a too-small buffer is reported, not kept pending
+    return rc;
+}
+
+extern "C" int dhsa_restore_begin(dhsa_sketch_t *s, double theta, uint64_t max_candidates)
+{
+    NEED(s);
+    std::lock_guard<std::mutex> lk(s->mu);
+    if (int rc = use_device(s)) return rc;
+    return restore_begin_locked(s, theta, max_candidates);
+}
+
+extern "C" int dhsa_restore_end(dhsa_sketch_t *s, dhsa_report_t *reports_host, uint64_t reports_cap,
+                                dhsa_restore_info_t *info)
+{
+    NEED(s);
+    std::lock_guard<std::mutex> lk(s->mu);
+    if (int rc = use_device(s)) return rc;
+    return restore_end_locked(s, reports_host, reports_cap, info);
 }
 
 // ------------------------------------------------------------------- merge --

@@ -309,6 +309,30 @@ class Dhla:
                     for h, e, s in zip(rows["host"][:n].tolist(), rows["estimate"][:n].tolist(),
                                        rows["saturated"][:n].tolist())]
 
+    def restore_superpoints_begin(self, theta, max_candidates: int = DEFAULT_MAX_CANDIDATES) -> None:
+        """Enqueue the read-out of restore_superpoints and return at once.  The next window's
+        reset() and update_batch() may be queued on this sketch before the reports are
+        collected with restore_superpoints_end(): stream order keeps them behind the read-out,
+        and the device never waits for the host."""
+        _cabi.check(self._lib.dhsa_restore_begin(self._h, float(theta), int(max_candidates)))
+
+    def restore_superpoints_end(self) -> list:
+        """Reports of the read-out begun with restore_superpoints_begin."""
+        info = _cabi.RestoreInfo()
+        cap = 1024
+        while True:
+            rows = np.empty(cap, dtype=_REPORT_DTYPE)
+            rc = self._lib.dhsa_restore_end(self._h, rows.ctypes.data, cap, C.byref(info))
+            self.last_info = self._info_dict(info)
+            if rc == 3 and info.n_reports > cap:
+                cap = int(info.n_reports)
+                continue
+            _cabi.check(rc)
+            n = int(info.n_reports)
+            return [SuperPointReport(int(h), float(e), bool(s))
+                    for h, e, s in zip(rows["host"][:n].tolist(), rows["estimate"][:n].tolist(),
+                                       rows["saturated"][:n].tolist())]
+
     # --- merge -------------------------------------------------------------------------
 
     def merge_from(self, other: "Dhla") -> None:

@@ -228,3 +228,10 @@ class ShardedWindow:
 
     def restore(self):
         return self.sketch.restore_superpoints(self.theta, max_candidates=self.max_candidates)
+
+    def restore_begin(self) -> None:
+        """Enqueue the read-out; the next window's reset() + scan() may follow before restore_end()."""
+        self.sketch.restore_superpoints_begin(self.theta, max_candidates=self.max_candidates)
+
+    def restore_end(self):
+        return self.sketch.restore_superpoints_end()

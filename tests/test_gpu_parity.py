@@ -258,6 +258,41 @@ def test_partition_scan_survives_more_keys_than_table_entries():
     assert sk.partition_stats()["unstored"] > 0
 
 
+def test_restore_begin_end_overlaps_the_next_window():
+    """dhsa_restore_begin/_end: window k's read-out is enqueued, window k + 1 is reset and fed on
+    the same sketch, and only then are window k's reports collected -- they must be window k's."""
+    windows = []
+    for w in range(3):
+        cand, opp = O.distinct_pairs(100_000, 200 + w)
+        for host, fan, seed in [(3_000_000 + 11 * w + n, 2048 + 100 * n, 700 + 10 * w + n) for n in range(4 + w)]:
+            c, o = O.plant_pairs(host, fan, seed)
+            cand, opp = np.concatenate([cand, c]), np.concatenate([opp, o])
+        ora = O.OracleSketch()
+        ora.update_batch(cand, opp, threads=4)
+        windows.append((cand, opp, ora.restore_superpoints(1024)))
+    sk = P.Dhla(P.DhgParams())
+    with pytest.raises(P.ConfigError):
+        sk.restore_superpoints_end()                       # nothing begun
+    got = []
+    for w, (cand, opp, _) in enumerate(windows):
+        sk.reset()
+        sk.update_batch(cand, opp)
+        if w:
+            got.append(sk.restore_superpoints_end())       # window w - 1, collected after window w was fed
+        sk.restore_superpoints_begin(1024)
+        with pytest.raises(P.ConfigError):
+            sk.estimate(1024)                              # the pinned mirrors belong to the pending read-out
+        with pytest.raises(P.ConfigError):
+            sk.restore_superpoints_begin(1024)
+    got.append(sk.restore_superpoints_end())
+    for reports, (_, _, want) in zip(got, windows):
+        assert [(r.host, r.saturated) for r in reports] == [(r.host, r.saturated) for r in want]
+        assert len(reports) >= 4
+        for a, b in zip(reports, want):
+            assert a.estimate == pytest.approx(b.estimate, rel=REL_TOL)
+    assert sk.estimate(1024)["flow_count"] > 0              # collected: read-out calls work again
+
+
 def test_auto_mode_falls_back_when_flows_do_not_repeat():
     """All-distinct pairs: the hit rate stays ~0, auto switches kernels mid-window; bits stay exact."""
     cand, opp = O.distinct_pairs(12_000_000, 90)
