@@ -225,8 +225,6 @@ def run_ours(args, rank: int, local_rank: int, world: int) -> None:
     sk = win.sketch
     sk.set_scan_mode(args.scan_mode)
     sk.set_flow_cache((args.flow_cache_mib << 20) // 32)
-    if os.environ.get("DHSA_PT_TPC") or os.environ.get("DHSA_PT_GRID"):
-        sk.set_partition(int(os.environ.get("DHSA_PT_GRID", "0")), int(os.environ.get("DHSA_PT_TPC", "2")))
     stream = torch.cuda.Stream(dev)   # one stream for torch ops, the sketch's kernels and the timing events
     torch.cuda.set_stream(stream)
     sk.use_stream(stream.cuda_stream)
@@ -308,7 +306,6 @@ def run_ours(args, rank: int, local_rank: int, world: int) -> None:
         parity["timed_windows_equal_warmup_reports"] = bool(same and len(collected) == args.steps)
     launches = sk.launch_count - launches0
     fc_lookups, fc_hits = sk.flow_cache_stats()
-    pt_stats = sk.partition_stats()
     ms_total = t_begin.elapsed_time(t_end)
     scan_ms = float(np.mean([e[3].elapsed_time(e[1]) for e in evs]))      # the scan kernel's launch alone
     reset_ms = float(np.mean([e[0].elapsed_time(e[3]) for e in evs]))     # window reset: sketch + flow cache cleared
@@ -463,7 +460,6 @@ def run_ours(args, rank: int, local_rank: int, world: int) -> None:
                        "scan_mode": args.scan_mode, "merge": win.merged_with,
                        "pipeline": "reports of window k collected after window k+1's reset+scan are queued "
                                    "(restore_begin/_end); every window's reports are read back",
-                       "partition": (pt_stats if pt_stats["lookups"] else None),
                        "flow_cache": ({"mib": args.flow_cache_mib,
                                        "hit_rate": (fc_hits / fc_lookups) if fc_lookups else None}
                                       if args.scan_mode in ("flow_cache", "auto") else None),
@@ -508,7 +504,7 @@ def main() -> None:
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--packets", type=int, default=100_000_000, help="packets per GPU per window")
     ap.add_argument("--seed", type=int, default=100)
-    ap.add_argument("--scan-mode", default="auto", choices=["red", "test", "test_agg", "flow_cache", "auto", "partition"])
+    ap.add_argument("--scan-mode", default="auto", choices=["red", "test", "test_agg", "flow_cache", "auto"])
     ap.add_argument("--flow-cache-mib", type=int, default=32, help="flow cache size; flow_cache mode only")
     ap.add_argument("--merge", default="auto", choices=["auto", "p2p", "allgather"])
     ap.add_argument("--cpu-sample", type=int, default=50_000_000)

@@ -48,8 +48,6 @@ extern "C" {
 #define DHSA_SCAN_TEST_RED 1      /* load the word, atomic only if the bit is still clear      */
 #define DHSA_SCAN_TEST_AGG_RED 2  /* as 1, and lanes of a warp hitting one word merge first    */
 #define DHSA_SCAN_FLOW_CACHE 3    /* as 2 behind an exact L2-resident cache of scanned pairs   */
-#define DHSA_SCAN_PARTITION 5     /* packets routed to the SM owning their (cand, h1(opp)) key and
-                                     dropped against an exact shared-memory key table there    */
 #define DHSA_SCAN_AUTO 4          /* default: 3, falling back to 2 for the rest of a window whose
                                      flows do not repeat (cache hit rate below ~1/3)            */
 
@@ -123,13 +121,6 @@ int dhsa_set_scan_mode(dhsa_sketch_t *s, int mode);
  * the bits are identical with or without it.  stats: keys looked up / found since the reset. */
 int dhsa_set_flow_cache(dhsa_sketch_t *s, uint64_t n_sets);
 int dhsa_flow_cache_stats(dhsa_sketch_t *s, uint64_t *lookups, uint64_t *hits);
-/* DHSA_SCAN_PARTITION tuning and counters.  grid: CTAs = key buckets (0 = one per SM);
- * tiles_per_cta: 4096-packet tiles every CTA bins per chunk (default 2).  stats since the
- * last reset: keys looked up in the shared-memory tables, table hits, packets a producer
- * updated itself (bin overflow), keys that found both candidate sets full. */
-int dhsa_set_partition(dhsa_sketch_t *s, int grid, int tiles_per_cta);
-int dhsa_partition_stats(dhsa_sketch_t *s, uint64_t *lookups, uint64_t *hits, uint64_t *direct,
-                         uint64_t *unstored);
 /* Kernel launches issued through this handle so far (bench.py's gpu_launches). */
 int dhsa_launch_count(const dhsa_sketch_t *s, uint64_t *n);
 

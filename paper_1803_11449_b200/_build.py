@@ -11,7 +11,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(_HERE, "csrc")
 LIB_PATH = os.path.join(_HERE, "libdhsa_b200.so")
 SOURCES = ["dhsa_cabi.cu"]
-HEADERS = ["dhsa_device.cuh", "dhsa_partition.cuh", os.path.join("..", "..", "include", "dhsa_b200.h")]
+HEADERS = ["dhsa_device.cuh", os.path.join("..", "..", "include", "dhsa_b200.h")]
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",

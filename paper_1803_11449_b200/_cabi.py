@@ -58,8 +58,6 @@ SIGNATURES = {
     "dhsa_set_scan_mode": [_vp, C.c_int],
     "dhsa_set_flow_cache": [_vp, _u64],
     "dhsa_flow_cache_stats": [_vp, C.POINTER(_u64), C.POINTER(_u64)],
-    "dhsa_set_partition": [_vp, C.c_int, C.c_int],
-    "dhsa_partition_stats": [_vp, C.POINTER(_u64), C.POINTER(_u64), C.POINTER(_u64), C.POINTER(_u64)],
     "dhsa_launch_count": [_vp, C.POINTER(_u64)],
     "dhsa_update_device": [_vp, _vp, _vp, _u64],
     "dhsa_update_host": [_vp, _vp, _vp, _u64],

@@ -8,7 +8,6 @@
 // CUDA is unavailable every call fails with a negative code.
 #include "../../include/dhsa_b200.h"
 #include "dhsa_device.cuh"
-#include "dhsa_partition.cuh"
 
 #include <math.h>
 #include <stdarg.h>
@@ -53,6 +52,7 @@ static int cuda_fail(cudaError_t e, const char *what)
 
 // ------------------------------------------------------------------ handle --
 
+static const uint64_t kCounterBytes = 256;   // device counters kept behind the bit array
 static const uint64_t kPinnedReports = 256;  // report rows copied back inside the read-out graph
 static const int kStageBufs = 3;            // staging buffers of the host-input pipeline
 static const uint64_t kStagePackets = 1ull << 22;  // packets per staged chunk (16 MiB per array)
@@ -70,7 +70,6 @@ struct dhsa_sketch {
     cudaStream_t copy_stream;
     std::mutex mu;
     uint64_t launches;
-    bool launch_failed;     // a scan launch helper failed; dhsa_last_error() holds the reason
 
     // flow cache of scan mode 3
     unsigned long long *fcache;
@@ -81,12 +80,6 @@ struct dhsa_sketch {
     cudaEvent_t fc_stats_ev;
     bool fc_stats_pending;
     bool auto_fell_back;           // auto mode: this window's flows do not repeat, use the 5-access kernel
-
-    // scan mode 5: packets routed to per-SM shared-memory key tables (dhsa_partition.cuh)
-    PartParams pt;
-    uint64_t pt_ring_bytes;
-    int pt_grid;                   // CTAs = buckets (0: one per SM, at most DHSA_PT_MAX_BUCKETS)
-    int pt_tiles_per_cta;
 
     // read-out workspaces
     Control *ctl;           // device
@@ -220,7 +213,6 @@ extern "C" int dhsa_create(const dhsa_params_t *params, int device, dhsa_sketch_
     CU(cudaDeviceGetAttribute(&s->sm_count, cudaDevAttrMultiProcessorCount, device));
     s->scan_mode = DHSA_SCAN_AUTO;
     s->fc_sets = 1u << 20;
-    s->pt_tiles_per_cta = 2;
     const uint64_t m = 1ull << params->k;
     s->nbytes = (uint64_t)params->r * m * ((uint64_t)params->g / 8);
     s->alloc_bytes = (s->nbytes + 15) & ~15ull;
@@ -233,7 +225,9 @@ extern "C" int dhsa_create(const dhsa_params_t *params, int device, dhsa_sketch_
     d.ncell = (uint64_t)params->r * m;
     d.nwords = s->alloc_bytes / 4;
     s->bitmap_words = m >= 32 ? m / 32 : 1;
-    cudaError_t e = cudaMalloc(&s->bits, s->alloc_bytes);
+    // the window's counters (record tally, flow-cache statistics) sit right behind the
+    // bit array, so a window reset is ONE memset
+    cudaError_t e = cudaMalloc(&s->bits, s->alloc_bytes + kCounterBytes);
     if (e != cudaSuccess) {
         delete s;
         return cuda_fail(e, "cudaMalloc(bits)");
@@ -242,13 +236,13 @@ extern "C" int dhsa_create(const dhsa_params_t *params, int device, dhsa_sketch_
     CU(cudaStreamCreateWithFlags(&s->copy_stream, cudaStreamNonBlocking));
     s->stream = s->own_stream;
     CU(cudaMalloc(&s->ctl, sizeof(Control)));
-    CU(cudaMalloc(&s->tally, 2 * sizeof(unsigned long long)));
-    CU(cudaMemsetAsync(s->tally, 0, 2 * sizeof(unsigned long long), s->stream));
+    s->tally = reinterpret_cast<unsigned long long *>(s->bits + s->alloc_bytes);
+    s->fc_stats = s->tally + 2;
     CU(cudaMallocHost(&s->ctl_host, sizeof(Control)));
     CU(cudaMallocHost(&s->reports_pinned, kPinnedReports * sizeof(ReportOut)));
     CU(cudaEventCreateWithFlags(&s->restore_ev, cudaEventDisableTiming));
     s->graph_disabled = getenv("DHSA_NO_GRAPH") != nullptr;
-    CU(cudaMemsetAsync(s->bits, 0, s->alloc_bytes, s->stream));
+    CU(cudaMemsetAsync(s->bits, 0, s->alloc_bytes + kCounterBytes, s->stream));
     CU(cudaMemsetAsync(s->ctl, 0, sizeof(Control), s->stream));
     CU(cudaStreamSynchronize(s->stream));
     CU(cudaFuncSetAttribute(k_sort_small, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -273,16 +267,11 @@ extern "C" int dhsa_destroy(dhsa_sketch_t *s)
         }
     }
     cudaFree(s->bits);
-    cudaFree(s->tally);
     cudaFree(s->plan_block_max);
     cudaFree(s->plan_carry);
     cudaFree(s->plan_out);
     cudaFree(s->plan_count);
     cudaFree(s->fcache);
-    cudaFree(s->fc_stats);
-    cudaFree(s->pt.ring);
-    cudaFree(s->pt.sync);
-    cudaFree(s->pt.stats);
     if (s->fc_stats_host) {
         cudaFreeHost(s->fc_stats_host);
         cudaEventDestroy(s->fc_stats_ev);
@@ -300,7 +289,7 @@ extern "C" int dhsa_destroy(dhsa_sketch_t *s)
 
 // The flow cache asserts "this pair's bits are in the sketch": it must be emptied
 // whenever bits can disappear (reset, upload).  Stream-ordered with the scans.
-static int clear_flow_cache_locked(dhsa_sketch *s)
+static int clear_flow_cache_locked(dhsa_sketch *s, bool clear_stats = true)
 {
     if (!s->fcache || !s->fc_dirty) return DHSA_OK;
     // entries carry the epoch they were written in: bumping it empties the table without touching it
@@ -311,7 +300,7 @@ static int clear_flow_cache_locked(dhsa_sketch *s)
     } else {
         s->dp.fc_epoch++;
     }
-    CU(cudaMemsetAsync(s->fc_stats, 0, 2 * sizeof(unsigned long long), s->stream));
+    if (clear_stats) CU(cudaMemsetAsync(s->fc_stats, 0, 2 * sizeof(unsigned long long), s->stream));
     s->fc_dirty = false;
     s->auto_fell_back = false;  // a new window may repeat flows again
     return DHSA_OK;
@@ -337,8 +326,7 @@ static int ensure_flow_cache_locked(dhsa_sketch *s)
     CU(cudaStreamSynchronize(s->stream));
     cudaFree(s->fcache);
     s->fcache = nullptr;
-    if (!s->fc_stats) {
-        CU(cudaMalloc(&s->fc_stats, 2 * sizeof(unsigned long long)));
+    if (!s->fc_stats_host) {
         CU(cudaMallocHost(&s->fc_stats_host, 2 * sizeof(unsigned long long)));
         CU(cudaEventCreateWithFlags(&s->fc_stats_ev, cudaEventDisableTiming));
         s->fc_stats_host[0] = s->fc_stats_host[1] = 0;
@@ -372,7 +360,6 @@ extern "C" int dhsa_flow_cache_stats(dhsa_sketch_t *s, uint64_t *lookups, uint64
     NEED(hits);
     *lookups = *hits = 0;
     std::lock_guard<std::mutex> lk(s->mu);
-    if (!s->fc_stats) return DHSA_OK;
     if (int rc = use_device(s)) return rc;
     unsigned long long v[2];
     CU(cudaMemcpyAsync(v, s->fc_stats, sizeof v, cudaMemcpyDeviceToHost, s->stream));
@@ -386,10 +373,8 @@ extern "C" int dhsa_reset(dhsa_sketch_t *s)
     NEED(s);
     std::lock_guard<std::mutex> lk(s->mu);
     if (int rc = use_device(s)) return rc;
-    CU(cudaMemsetAsync(s->bits, 0, s->alloc_bytes, s->stream));
-    CU(cudaMemsetAsync(s->tally, 0, 2 * sizeof(unsigned long long), s->stream));
-    if (s->pt.stats) CU(cudaMemsetAsync(s->pt.stats, 0, 4 * sizeof(unsigned long long), s->stream));
-    return clear_flow_cache_locked(s);
+    CU(cudaMemsetAsync(s->bits, 0, s->alloc_bytes + kCounterBytes, s->stream));  // bits and every counter
+    return clear_flow_cache_locked(s, false);
 }
 
 extern "C" int dhsa_sketch_bytes(const dhsa_sketch_t *s, uint64_t *nbytes)
@@ -448,40 +433,8 @@ extern "C" int dhsa_get_stream(dhsa_sketch_t *s, void **cuda_stream)
 extern "C" int dhsa_set_scan_mode(dhsa_sketch_t *s, int mode)
 {
     NEED(s);
-    if (mode < 0 || mode > 5) return fail(DHSA_ECONFIG, "scan mode must be 0..5 (got %d)", mode);
+    if (mode < 0 || mode > 4) return fail(DHSA_ECONFIG, "scan mode must be 0..4 (got %d)", mode);
     s->scan_mode = mode;
-    return DHSA_OK;
-}
-
-extern "C" int dhsa_set_partition(dhsa_sketch_t *s, int grid, int tiles_per_cta)
-{
-    NEED(s);
-    if (grid < 0 || grid > (int)DHSA_PT_MAX_BUCKETS)
-        return fail(DHSA_ECONFIG, "partition grid must satisfy 0 <= grid <= %d (got %d)", (int)DHSA_PT_MAX_BUCKETS, grid);
-    if (tiles_per_cta < 1 || tiles_per_cta > 16)
-        return fail(DHSA_ECONFIG, "partition tiles_per_cta must satisfy 1 <= tiles_per_cta <= 16 (got %d)", tiles_per_cta);
-    std::lock_guard<std::mutex> lk(s->mu);
-    s->pt_grid = grid;
-    s->pt_tiles_per_cta = tiles_per_cta;
-    return DHSA_OK;
-}
-
-extern "C" int dhsa_partition_stats(dhsa_sketch_t *s, uint64_t *lookups, uint64_t *hits, uint64_t *direct,
-                                    uint64_t *unstored)
-{
-    NEED(s);
-    NEED(lookups);
-    NEED(hits);
-    NEED(direct);
-    NEED(unstored);
-    *lookups = *hits = *direct = *unstored = 0;
-    std::lock_guard<std::mutex> lk(s->mu);
-    if (!s->pt.stats) return DHSA_OK;
-    if (int rc = use_device(s)) return rc;
-    unsigned long long v[4];
-    CU(cudaMemcpyAsync(v, s->pt.stats, sizeof v, cudaMemcpyDeviceToHost, s->stream));
-    CU(cudaStreamSynchronize(s->stream));
-    *lookups = v[0], *hits = v[1], *direct = v[2], *unstored = v[3];
     return DHSA_OK;
 }
 
@@ -494,66 +447,6 @@ extern "C" int dhsa_launch_count(const dhsa_sketch_t *s, uint64_t *n)
 }
 
 // -------------------------------------------------------------------- scan --
-
-// Scan mode 5 (dhsa_partition.cuh).  Buckets = CTAs, one per SM, all resident at once
-// (cooperative launch): producers and consumers of different CTAs wait on each other.
-static int partition_buckets(const dhsa_sketch *s)
-{
-    int nb = s->pt_grid > 0 ? s->pt_grid : s->sm_count;
-    if (nb > s->sm_count) nb = s->sm_count;
-    if (nb > (int)DHSA_PT_MAX_BUCKETS) nb = (int)DHSA_PT_MAX_BUCKETS;
-    return nb < 1 ? 1 : nb;
-}
-
-// the table's 32-bit entries hold (tag << 1 | choice) + 1 with tag = rem >> 13 and
-// rem < (2^32 / nb + 1) << log2(g)
-static bool partition_supported(const dhsa_sketch *s)
-{
-    if (s->dp.log2g > 20) return false;
-    const uint64_t rem_max = ((1ull << 32) / (uint64_t)partition_buckets(s) + 2) << s->dp.log2g;
-    return (rem_max >> DHSA_PT_LOG2_SETS) < (1ull << 30);
-}
-
-static int ensure_partition_locked(dhsa_sketch *s)
-{
-    const uint64_t nb = (uint64_t)partition_buckets(s);
-    const uint64_t need = (uint64_t)DHSA_PT_RING * (uint64_t)s->pt_tiles_per_cta * nb * nb * DHSA_PT_SLOT_WORDS * 8ull;
-    PartParams &pt = s->pt;
-    if (!pt.sync) {
-        CU(cudaMalloc(&pt.sync, 8 * sizeof(unsigned int)));
-        CU(cudaMalloc(&pt.stats, 4 * sizeof(unsigned long long)));
-        CU(cudaMemsetAsync(pt.stats, 0, 4 * sizeof(unsigned long long), s->stream));
-    }
-    if (s->pt_ring_bytes < need) {
-        CU(cudaStreamSynchronize(s->stream));
-        cudaFree(pt.ring);
-        pt.ring = nullptr, s->pt_ring_bytes = 0;
-        CU(cudaMalloc(&pt.ring, need));
-        s->pt_ring_bytes = need;
-    }
-    pt.tiles_per_cta = (uint32_t)s->pt_tiles_per_cta;
-    return DHSA_OK;
-}
-
-template <int R, typename SRC>
-static int launch_partition(dhsa_sketch *s, const SRC &src)
-{
-    static bool attr_set = false;
-    auto kernel = k_scan_partition<R, SRC>;
-    if (!attr_set) {
-        CU(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)DHSA_PT_SMEM_BYTES));
-        attr_set = true;
-    }
-    CU(cudaMemsetAsync(s->pt.sync, 0, 8 * sizeof(unsigned int), s->stream));
-    uint32_t *w = reinterpret_cast<uint32_t *>(s->bits);
-    SRC src_copy = src;
-    void *args[] = {(void *)&src_copy, (void *)&w, (void *)&s->dp, (void *)&s->pt};
-    CU(cudaLaunchCooperativeKernel((const void *)kernel, dim3((unsigned)partition_buckets(s)),
-                                   dim3((DHSA_PT_PWARPS + DHSA_PT_CWARPS) * 32), args, (size_t)DHSA_PT_SMEM_BYTES,
-                                   s->stream));
-    s->launches++;
-    return DHSA_OK;
-}
 
 template <int R, typename SRC>
 static void launch_scan_src(dhsa_sketch *s, int mode, const SRC &src)
@@ -569,9 +462,6 @@ static void launch_scan_src(dhsa_sketch *s, int mode, const SRC &src)
         KERNEL<<<grid_for(s, nvec, 256, occ), 256, 0, s->stream>>>(src, w, s->dp);                         \
     } while (0)
     switch (mode) {
-    case DHSA_SCAN_PARTITION:
-        if (launch_partition<R, SRC>(s, src) != DHSA_OK) s->launch_failed = true;
-        return;
     case DHSA_SCAN_RED_ONLY: LAUNCH((k_scan_vec4<R, 0, SRC>), 8); break;
     case DHSA_SCAN_TEST_RED: LAUNCH((k_scan_vec4<R, 1, SRC>), 3); break;
     case DHSA_SCAN_TEST_AGG_RED: LAUNCH((k_scan_vec4<R, 2, SRC>), 2); break;
@@ -611,7 +501,6 @@ static int pick_scan_mode_locked(dhsa_sketch *s)
         (void)cudaGetLastError();
         mode = s->auto_fell_back ? DHSA_SCAN_TEST_AGG_RED : DHSA_SCAN_FLOW_CACHE;
     }
-    if (mode == DHSA_SCAN_PARTITION && !partition_supported(s)) mode = DHSA_SCAN_FLOW_CACHE;
     if (mode == DHSA_SCAN_FLOW_CACHE && !flow_cache_supported(s)) mode = DHSA_SCAN_TEST_AGG_RED;
     return mode;
 }
@@ -622,15 +511,11 @@ static int before_fast_scan_locked(dhsa_sketch *s, int mode)
         if (int rc = ensure_flow_cache_locked(s)) return rc;
         s->fc_dirty = true;
     }
-    if (mode == DHSA_SCAN_PARTITION)
-        if (int rc = ensure_partition_locked(s)) return rc;
-    s->launch_failed = false;
     return DHSA_OK;
 }
 
 static int after_fast_scan_locked(dhsa_sketch *s, int mode)
 {
-    if (s->launch_failed) return -1;  // message already recorded by the helper
     if (s->scan_mode == DHSA_SCAN_AUTO && mode == DHSA_SCAN_FLOW_CACHE && !s->fc_stats_pending) {
         CU(cudaMemcpyAsync(s->fc_stats_host, s->fc_stats, 2 * sizeof(unsigned long long), cudaMemcpyDeviceToHost,
                            s->stream));

@@ -31,7 +31,7 @@ from .errors import ConfigError
 
 DEFAULT_MAX_CANDIDATES = 1 << 20  # pkg/src/dhsa/dhla.py:34
 
-SCAN_MODES = {"red": 0, "test": 1, "test_agg": 2, "flow_cache": 3, "auto": 4, "partition": 5}
+SCAN_MODES = {"red": 0, "test": 1, "test_agg": 2, "flow_cache": 3, "auto": 4}
 
 _REPORT_DTYPE = np.dtype([("host", "<u8"), ("estimate", "<f8"), ("saturated", "<i4"), ("sz", "<i4")])
 assert _REPORT_DTYPE.itemsize == C.sizeof(_cabi.Report)
@@ -134,17 +134,6 @@ class Dhla:
         a, b = C.c_uint64(), C.c_uint64()
         _cabi.check(self._lib.dhsa_flow_cache_stats(self._h, C.byref(a), C.byref(b)))
         return int(a.value), int(b.value)
-
-    def set_partition(self, grid: int = 0, tiles_per_cta: int = 2) -> None:
-        """Scan mode "partition": CTAs (= key buckets, 0 -> one per SM) and 4096-packet
-        tiles each CTA bins per chunk."""
-        _cabi.check(self._lib.dhsa_set_partition(self._h, int(grid), int(tiles_per_cta)))
-
-    def partition_stats(self) -> dict:
-        """Counters of scan mode "partition" since the last reset."""
-        v = [C.c_uint64() for _ in range(4)]
-        _cabi.check(self._lib.dhsa_partition_stats(self._h, *[C.byref(x) for x in v]))
-        return dict(zip(("lookups", "hits", "direct", "unstored"), (int(x.value) for x in v)))
 
     # --- the bits attribute ----------------------------------------------------
 

@@ -54,7 +54,7 @@ def gpu_for_case(case, mode="test_agg"):
 # ------------------------------------------------------------------------ scan --
 
 
-MODES = ["red", "test", "test_agg", "flow_cache", "auto", "partition"]
+MODES = ["red", "test", "test_agg", "flow_cache", "auto"]
 
 
 @pytest.mark.parametrize("mode", MODES)
@@ -215,47 +215,6 @@ def test_flow_cache_is_exact_across_batches_resets_and_uploads(n_sets):
     assert np.array_equal(sk.bits, want.bits)
     lookups, hits = sk.flow_cache_stats()
     assert lookups == 10_000 and 2_500 <= hits <= 5_100       # the second pass of the last window hits (lost insert races aside)
-
-
-@pytest.mark.parametrize("grid,tiles_per_cta", [(0, 2), (0, 1), (148, 3), (37, 2), (8, 1), (1, 2)])
-def test_partition_scan_is_exact_for_every_grid_and_skew(grid, tiles_per_cta):
-    """Scan mode 5 routes keys to per-CTA shared-memory tables.  Small grids overflow
-    their 31-entry bins constantly (the producers' overflow list and direct update), a few hot keys
-    skew the buckets, the tables fill up; several launches per window; bits stay exact."""
-    rng = np.random.default_rng(17)
-    base_c, base_o = O.distinct_pairs(300_000, 77)
-    hot_c = np.repeat(np.array([0xC0A80101, 0, 0xFFFFFFFF], np.uint32), 3)
-    hot_o = np.array([1, 2, 3, 0xFFFFFFFF, 0, 7, 0xFFFFFFFF, 0, 9], np.uint32)
-    sk = P.Dhla(P.DhgParams())
-    sk.set_scan_mode("partition")
-    sk.set_partition(grid, tiles_per_cta)
-    ora = O.OracleSketch()
-    total = 0
-    for n in (2_000_001, 37, 4096, 1_234_567):
-        pick = rng.integers(0, len(base_c), size=n)
-        c, o = base_c[pick], base_o[pick]
-        heavy = rng.random(n) < 0.3                      # 30% of the packets on 9 keys
-        hp = rng.integers(0, len(hot_c), size=n)
-        c, o = np.where(heavy, hot_c[hp], c), np.where(heavy, hot_o[hp], o)
-        sk.update_batch(c, o)
-        ora.update_batch(c, o, threads=4)
-        total += n - n % 4
-        assert np.array_equal(sk.bits, ora.bits)
-    st = sk.partition_stats()
-    assert st["lookups"] + st["direct"] == total          # every whole quad went through the kernel
-    assert 0 < st["hits"] < st["lookups"]
-
-
-def test_partition_scan_survives_more_keys_than_table_entries():
-    """12M distinct pairs against 148 x 32768 table entries: most keys are never recorded."""
-    cand, opp = O.distinct_pairs(12_000_000, 90)
-    ora = O.OracleSketch(r=5, g=1024, k=16, alpha=6)
-    ora.update_batch(cand, opp, threads=8)
-    sk = P.Dhla(P.DhgParams(r=5, g=1024, k=16, alpha=6))
-    sk.set_scan_mode("partition")
-    sk.update_batch(cand, opp)
-    assert sha(sk.bits) == sha(ora.bits)
-    assert sk.partition_stats()["unstored"] > 0
 
 
 def test_restore_begin_end_overlaps_the_next_window():
@@ -625,7 +584,7 @@ def _window(n_packets, n_hosts, n_scanners, seed):
     return src, dst, ct, ot, hosts[n_hosts:]
 
 
-@pytest.mark.parametrize("mode", ["partition", "flow_cache", "test_agg", "test", "red"])
+@pytest.mark.parametrize("mode", ["flow_cache", "test_agg", "test", "red"])
 def test_100m_packet_window_bits_and_superpoints_equal_oracle(mode):
     """BASELINE config 2 size.  The oracle scans the distinct flows only; the GPU
     scans all 100M packets; bits, super point set and estimates must agree."""
