@@ -204,6 +204,9 @@ int dhsa_update_records_device(dhsa_sketch_t *s, const void *records_dev, uint64
                                uint64_t rec_lo, uint64_t rec_hi, uint32_t window_seconds,
                                uint32_t window_id, int direction);
 int dhsa_record_tally(dhsa_sketch_t *s, uint64_t *records_fed, uint64_t *records_dropped);
+/* The same two counters as they stood when the last collected read-out (dhsa_restore /
+ * dhsa_restore_end) ran: copied back with its reports, so no further synchronisation. */
+int dhsa_record_tally_at_restore(dhsa_sketch_t *s, uint64_t *records_fed, uint64_t *records_dropped);
 
 /* ---- exact oracle on the GPU: ingest.exact_oracle (pkg/src/dhsa/ingest.py:159-176) -----------
  * Exact number of distinct opposites per candidate host, by a hash set of whole pairs and

@@ -75,6 +75,7 @@ SIGNATURES = {
     "dhsa_plan_windows": [_vp, _vp, _u64, C.c_uint32, C.c_int64, _vp, C.c_uint32, C.POINTER(C.c_uint32)],
     "dhsa_update_records_device": [_vp, _vp, _u64, _u64, _u64, C.c_uint32, C.c_uint32, C.c_int],
     "dhsa_record_tally": [_vp, C.POINTER(_u64), C.POINTER(_u64)],
+    "dhsa_record_tally_at_restore": [_vp, C.POINTER(_u64), C.POINTER(_u64)],
     "dhsa_exact_create": [C.c_int, _u64, C.POINTER(_vp)],
     "dhsa_exact_destroy": [_vp],
     "dhsa_exact_add_pairs": [_vp, _vp, _vp, _u64, _vp],

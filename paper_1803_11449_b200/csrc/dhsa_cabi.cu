@@ -108,6 +108,7 @@ struct dhsa_sketch {
     bool graph_disabled;
     ReportOut *reports_pinned;      // the first kPinnedReports rows land here with the control block
     cudaEvent_t restore_ev;         // read-out enqueued by dhsa_restore_begin has landed in the pinned mirrors
+    unsigned long long *tally_pinned;  // record tally as of the last read-out (copied with the control block)
     bool restore_pending;
     uint64_t restore_max_candidates;
 
@@ -241,6 +242,8 @@ extern "C" int dhsa_create(const dhsa_params_t *params, int device, dhsa_sketch_
     CU(cudaMallocHost(&s->ctl_host, sizeof(Control)));
     CU(cudaMallocHost(&s->reports_pinned, kPinnedReports * sizeof(ReportOut)));
     CU(cudaEventCreateWithFlags(&s->restore_ev, cudaEventDisableTiming));
+    CU(cudaMallocHost(&s->tally_pinned, 2 * sizeof(unsigned long long)));
+    s->tally_pinned[0] = s->tally_pinned[1] = 0;
     s->graph_disabled = getenv("DHSA_NO_GRAPH") != nullptr;
     CU(cudaMemsetAsync(s->bits, 0, s->alloc_bytes + kCounterBytes, s->stream));
     CU(cudaMemsetAsync(s->ctl, 0, sizeof(Control), s->stream));
@@ -280,6 +283,7 @@ extern "C" int dhsa_destroy(dhsa_sketch_t *s)
     cudaFreeHost(s->ctl_host);
     cudaFreeHost(s->reports_pinned);
     cudaEventDestroy(s->restore_ev);
+    cudaFreeHost(s->tally_pinned);
     if (s->restore_graph) cudaGraphExecDestroy(s->restore_graph);
     cudaStreamDestroy(s->own_stream);
     cudaStreamDestroy(s->copy_stream);
@@ -645,6 +649,17 @@ extern "C" int dhsa_record_tally(dhsa_sketch_t *s, uint64_t *records_fed, uint64
     CU(cudaMemcpyAsync(v, s->tally, sizeof v, cudaMemcpyDeviceToHost, s->stream));
     CU(cudaStreamSynchronize(s->stream));
     *records_fed = v[0], *records_dropped = v[1];
+    return DHSA_OK;
+}
+
+extern "C" int dhsa_record_tally_at_restore(dhsa_sketch_t *s, uint64_t *records_fed, uint64_t *records_dropped)
+{
+    NEED(s);
+    NEED(records_fed);
+    NEED(records_dropped);
+    std::lock_guard<std::mutex> lk(s->mu);
+    if (s->restore_pending) return fail(DHSA_ECONFIG, "the read-out that carries the tally has not been collected");
+    *records_fed = s->tally_pinned[0], *records_dropped = s->tally_pinned[1];
     return DHSA_OK;
 }
 
@@ -1113,6 +1128,7 @@ static int enqueue_restore(dhsa_sketch *s, double theta, uint64_t max_candidates
     CU(cudaMemcpyAsync(s->ctl_host, s->ctl, sizeof(Control), cudaMemcpyDeviceToHost, s->stream));
     const uint64_t rows = s->cand_cap < kPinnedReports ? s->cand_cap : kPinnedReports;
     CU(cudaMemcpyAsync(s->reports_pinned, s->reports, rows * sizeof(ReportOut), cudaMemcpyDeviceToHost, s->stream));
+    CU(cudaMemcpyAsync(s->tally_pinned, s->tally, 2 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s->stream));
     return DHSA_OK;
 }
 

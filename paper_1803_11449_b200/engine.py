@@ -137,6 +137,24 @@ class WindowSession:
             self.cfg.theta, max_candidates=self.cfg.max_candidates, workers=self.cfg.workers
         )
 
+    def seal_and_restore_begin(self) -> None:
+        """seal() + restore() without stopping the device: the window freezes, its read-out is
+        queued behind its last update, and the caller goes on feeding the next window (another
+        sketch, same stream) before collecting with ``restore_end``."""
+        self._check_open()
+        self.sealed = True
+        self.sketch.restore_superpoints_begin(self.cfg.theta, max_candidates=self.cfg.max_candidates)
+
+    def restore_end(self) -> List[SuperPointReport]:
+        reports = self.sketch.restore_superpoints_end()
+        if getattr(self, "_fed_records", False):   # the tally came back with the reports
+            fed, late = C.c_uint64(), C.c_uint64()
+            _cabi.check(self._lib.dhsa_record_tally_at_restore(self.sketch._h, C.byref(fed), C.byref(late)))
+            self.pairs += int(fed.value)
+            self.dropped += int(late.value)
+            self._fed_records = False
+        return reports
+
 
 def _as_record_bytes(records) -> np.ndarray:
     """Flat uint8 view of host records in the IPPR layout."""
@@ -275,14 +293,21 @@ class DetectionEngine:
             segments.extend(cuts)
             for idx, (lo, wid) in enumerate(segments):
                 hi = segments[idx + 1][0] if idx + 1 < len(segments) else n
+                closing = None
                 if session is not None and wid > session.sketch.window_id:
-                    yield self._finish(session, on_sealed)
+                    if on_sealed is not None:          # the hook wants the sealed sketch now: no overlap
+                        yield self._finish(session, on_sealed)
+                    else:                              # queue its read-out, collect after the next feed
+                        session.seal_and_restore_begin()
+                        closing = session
                     session = None
                 if session is None:
                     session = WindowSession(cfg, wid, self.backend, device=self._device_index(),
                                             sketch=self._take_idle(wid))
                     session.sketch.use_stream(torch.cuda.current_stream(session.sketch.device).cuda_stream)
                 session.feed_records(ptr, n, lo, hi)
+                if closing is not None:
+                    yield self._collect(closing)
         if session is not None:
             yield self._finish(session, on_sealed)
 
@@ -294,10 +319,16 @@ class DetectionEngine:
         return sk
 
     def _finish(self, session: WindowSession, on_sealed) -> WindowResult:
+        if on_sealed is None:
+            session.seal_and_restore_begin()
+            return self._collect(session)
         session.seal()
-        if on_sealed is not None:
-            on_sealed(session.sketch)
-        reports = session.restore()
+        on_sealed(session.sketch)
+        return self._collect(session, session.restore())
+
+    def _collect(self, session: WindowSession, reports=None) -> WindowResult:
+        if reports is None:
+            reports = session.restore_end()
         result = WindowResult(
             window_id=session.sketch.window_id,
             reports=reports,
