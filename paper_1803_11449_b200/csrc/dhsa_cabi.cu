@@ -53,7 +53,8 @@ static int cuda_fail(cudaError_t e, const char *what)
 // ------------------------------------------------------------------ handle --
 
 static const uint64_t kCounterBytes = 256;   // device counters kept behind the bit array
-static const uint64_t kPinnedReports = 256;  // report rows copied back inside the read-out graph
+static const uint64_t kPinnedReports = 256;
+static const uint32_t kPinnedBoundaries = 64;  // report rows copied back inside the read-out graph
 static const int kStageBufs = 3;            // staging buffers of the host-input pipeline
 static const uint64_t kStagePackets = 1ull << 22;  // packets per staged chunk (16 MiB per array)
 
@@ -117,6 +118,8 @@ struct dhsa_sketch {
     uint32_t *plan_block_max;
     long long *plan_carry;
     PlanBoundary *plan_out;
+    uint32_t *plan_rise;            // blocks in which the running window maximum rises
+    uint8_t *plan_pinned;           // count (8 bytes) + the first kPinnedBoundaries boundaries
     unsigned int *plan_count;
     uint64_t plan_blocks_cap;
     uint32_t plan_out_cap;
@@ -273,7 +276,9 @@ extern "C" int dhsa_destroy(dhsa_sketch_t *s)
     cudaFree(s->plan_block_max);
     cudaFree(s->plan_carry);
     cudaFree(s->plan_out);
+    cudaFree(s->plan_rise);
     cudaFree(s->plan_count);
+    if (s->plan_pinned) cudaFreeHost(s->plan_pinned);
     cudaFree(s->fcache);
     if (s->fc_stats_host) {
         cudaFreeHost(s->fc_stats_host);
@@ -472,7 +477,18 @@ static void launch_scan_src(dhsa_sketch *s, int mode, const SRC &src)
     // flow cache: 4 packets per lane at 3 CTAs/SM measured best on B200 (profiles/r01_flowcache_variants.txt);
     // 8 packets per lane, 4 CTAs/SM (spills) and L2::evict_last table loads were slower or equal; staging the
     // packet stream by TMA was 2-3% faster than register prefetch and is the only form kept
-    default: LAUNCH((k_scan_flowcache<R, SRC>), 3); break;
+    default: {
+        // flow cache: dynamic shared memory (TMA stage rings + miss queues), 3 CTAs per SM
+        static int occ = 0;
+        auto kernel = k_scan_flowcache<R, SRC>;
+        const int smem = FcSmem<SRC>::kBytes;
+        if (!occ) {
+            cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+            if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kernel, 256, smem) != cudaSuccess || occ < 1) occ = 3;
+        }
+        kernel<<<grid_for(s, nvec, 256, occ), 256, smem, s->stream>>>(src, w, s->dp);
+        break;
+    }
     }
 #undef LAUNCH
     s->launches++;
@@ -588,8 +604,7 @@ static int scan_records_locked(dhsa_sketch *s, const uint8_t *records, uint64_t 
             src.first_rec = 4 * q_lo;
             src.rec_lo = rec_lo;
             src.rec_hi = rec_hi;
-            src.window_seconds = window_seconds;
-            src.window_id = window_id;
+            src.set_window(window_seconds, window_id);
             src.cand_is_dst = cand_is_dst;
             src.tally = s->tally;
             src.tally_late = tally_late;
@@ -703,32 +718,48 @@ extern "C" int dhsa_plan_windows(dhsa_sketch_t *s, const void *records_dev, uint
         const uint32_t nc = cap > s->plan_out_cap ? cap : s->plan_out_cap;
         cudaFree(s->plan_block_max);
         cudaFree(s->plan_carry);
+        cudaFree(s->plan_rise);
         cudaFree(s->plan_out);
-        s->plan_block_max = nullptr, s->plan_carry = nullptr, s->plan_out = nullptr;
+        s->plan_block_max = nullptr, s->plan_carry = nullptr, s->plan_out = nullptr, s->plan_rise = nullptr;
         s->plan_blocks_cap = 0, s->plan_out_cap = 0;
         CU(cudaMalloc(&s->plan_block_max, nb * sizeof(uint32_t)));
         CU(cudaMalloc(&s->plan_carry, nb * sizeof(long long)));
+        CU(cudaMalloc(&s->plan_rise, nb * sizeof(uint32_t)));
         CU(cudaMalloc(&s->plan_out, (size_t)nc * sizeof(PlanBoundary)));
-        if (!s->plan_count) CU(cudaMalloc(&s->plan_count, sizeof(unsigned int)));
+        if (!s->plan_count) {
+            CU(cudaMalloc(&s->plan_count, 2 * sizeof(unsigned int)));  // [0] boundaries, [1] blocks where the maximum rises
+            CU(cudaMallocHost(&s->plan_pinned, sizeof(unsigned int) + kPinnedBoundaries * sizeof(PlanBoundary) + 8));
+        }
         s->plan_blocks_cap = nb;
         s->plan_out_cap = nc;
     }
     const uint32_t *rec_words = static_cast<const uint32_t *>(records_dev);
-    CU(cudaMemsetAsync(s->plan_count, 0, sizeof(unsigned int), s->stream));
+    CU(cudaMemsetAsync(s->plan_count, 0, 2 * sizeof(unsigned int), s->stream));
     k_plan_blockmax<<<(unsigned)nblocks, 256, 0, s->stream>>>(rec_words, n_records, window_seconds, s->plan_block_max);
-    k_plan_carry<<<1, 1024, 0, s->stream>>>(s->plan_block_max, nblocks, (long long)open_window, s->plan_carry);
-    k_plan_boundaries<<<(unsigned)nblocks, 256, 0, s->stream>>>(rec_words, n_records, window_seconds, s->plan_block_max,
-                                                              s->plan_carry, s->plan_out, cap, s->plan_count);
+    k_plan_carry<<<1, 1024, 0, s->stream>>>(s->plan_block_max, nblocks, (long long)open_window, s->plan_carry,
+                                            s->plan_rise, s->plan_count + 1);
+    const unsigned bgrid = (unsigned)(nblocks < 256 ? nblocks : 256);
+    k_plan_boundaries<<<bgrid, 256, 0, s->stream>>>(rec_words, n_records, window_seconds, s->plan_carry, s->plan_rise,
+                                                    s->plan_count + 1, s->plan_out, cap, s->plan_count);
     s->launches += 3;
     CU(cudaGetLastError());
-    unsigned int n = 0;
-    CU(cudaMemcpyAsync(&n, s->plan_count, sizeof n, cudaMemcpyDeviceToHost, s->stream));
+    // the count and the first few boundaries come back together: one synchronisation per chunk
+    unsigned int *n_pinned = reinterpret_cast<unsigned int *>(s->plan_pinned);
+    PlanBoundary *b_pinned = reinterpret_cast<PlanBoundary *>(s->plan_pinned + 8);
+    const uint32_t first = cap < kPinnedBoundaries ? cap : kPinnedBoundaries;
+    CU(cudaMemcpyAsync(n_pinned, s->plan_count, sizeof(unsigned int), cudaMemcpyDeviceToHost, s->stream));
+    CU(cudaMemcpyAsync(b_pinned, s->plan_out, (size_t)first * sizeof(PlanBoundary), cudaMemcpyDeviceToHost, s->stream));
     CU(cudaStreamSynchronize(s->stream));
+    const unsigned int n = *n_pinned;
     if (n > cap) return fail(DHSA_EDATA, "record stream opens %u windows, more than the plan capacity %u", n, cap);
     static_assert(sizeof(PlanBoundary) == sizeof(dhsa_boundary_t), "boundary layouts must match");
     if (n) {
-        CU(cudaMemcpyAsync(out_host, s->plan_out, (size_t)n * sizeof(PlanBoundary), cudaMemcpyDeviceToHost, s->stream));
-        CU(cudaStreamSynchronize(s->stream));
+        if (n <= first) {
+            memcpy(out_host, b_pinned, (size_t)n * sizeof(PlanBoundary));
+        } else {
+            CU(cudaMemcpyAsync(out_host, s->plan_out, (size_t)n * sizeof(PlanBoundary), cudaMemcpyDeviceToHost, s->stream));
+            CU(cudaStreamSynchronize(s->stream));
+        }
         qsort(out_host, n, sizeof(dhsa_boundary_t), cmp_boundary);
     }
     *n_out = n;
@@ -1501,7 +1532,7 @@ extern "C" int dhsa_exact_add_records(dhsa_exact_t *e, const void *records_dev, 
         src.nquads = q_hi - q_lo;
         src.first_rec = 4 * q_lo;
         src.rec_lo = rec_lo, src.rec_hi = rec_hi;
-        src.window_seconds = window_seconds, src.window_id = window_id;
+        src.set_window(window_seconds, window_id);
         src.cand_is_dst = pass;
         src.tally = nullptr, src.tally_late = 0;
         k_exact_insert<RecordSource><<<exact_grid(e, src.nquads), 256, 0, (cudaStream_t)cuda_stream>>>(src, e->t);

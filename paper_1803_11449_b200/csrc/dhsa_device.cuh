@@ -365,6 +365,7 @@ struct RecordSource {
     uint64_t rec_lo, rec_hi;  // records of this launch: one window's contiguous segment
     uint32_t window_seconds;
     uint32_t window_id;
+    uint32_t ts_lo, ts_hi;    // timestamps of this window, inclusive (set_window)
     int cand_is_dst;          // direction policy: 0 "src" (cand = src), 1 "dst" (cand = dst)
     unsigned long long *tally;  // [0] pairs fed (on-time records), [1] late records dropped
     int tally_late;             // 0 on the second pass of "both", so a late record is counted once
@@ -372,6 +373,15 @@ struct RecordSource {
     struct Raw {
         uint4 a, b, c;
     };
+    // timestamps with ts // seconds == id, clamped to 32 bits; seconds == 0 takes every record
+    __host__ void set_window(uint32_t seconds, uint32_t id)
+    {
+        window_seconds = seconds, window_id = id;
+        const unsigned long long lo = (unsigned long long)seconds * id, hi = lo + seconds - 1ull;
+        ts_lo = seconds == 0u ? 0u : (lo > 0xFFFFFFFFull ? 0xFFFFFFFFu : (uint32_t)lo);
+        ts_hi = seconds == 0u ? 0xFFFFFFFFu : (hi > 0xFFFFFFFFull ? 0xFFFFFFFFu : (uint32_t)hi);
+        if (seconds != 0u && lo > 0xFFFFFFFFull) ts_lo = 1u, ts_hi = 0u;  // window beyond any 32-bit timestamp: empty
+    }
     __host__ __device__ __forceinline__ uint64_t vectors() const { return nquads; }
     __device__ __forceinline__ void load(Raw &r, uint64_t v, uint64_t pol) const
     {
@@ -384,7 +394,7 @@ struct RecordSource {
     }
     // staged form: one warp trip = 32 quads = 1536 contiguous bytes of records
     static constexpr int kStageBytes = 1536;
-    static constexpr int kStages = 2;  // keeps the kernel inside 48 KB of static shared memory
+    static constexpr int kStages = 4;
     __device__ __forceinline__ void stage_issue(uint32_t smem_dst, uint32_t mbar, uint64_t base, uint32_t count,
                                                 uint64_t pol) const
     {
@@ -408,8 +418,9 @@ struct RecordSource {
             const uint32_t ts = w[3 * j];
             const uint32_t src = __byte_perm(w[3 * j + 1], 0, 0x0123);  // network order -> host order
             const uint32_t dst = __byte_perm(w[3 * j + 2], 0, 0x0123);
+            // ts // window_seconds == window_id as a range test (no division): [ts_lo, ts_hi] was set by the host.
             // window_seconds == 0: no windowing, every record of the range is taken (exact oracle over a whole trace)
-            const bool fresh = mine && (window_seconds == 0u || (ts / window_seconds) == window_id);
+            const bool fresh = mine && ts >= ts_lo && ts <= ts_hi;
             cs[j] = cand_is_dst ? dst : src;
             os[j] = cand_is_dst ? src : dst;
             ok[j] = fresh;
@@ -570,6 +581,14 @@ __device__ __forceinline__ void fc_drain32(uint32_t *__restrict__ words, const D
     }
 }
 
+template <typename SRC>
+struct FcSmem {
+    static constexpr int kStageBytesAll = 8 * SRC::kStages * SRC::kStageBytes;
+    static constexpr int kMbarBytesAll = 8 * SRC::kStages * 8;
+    static constexpr int kQueueBytesAll = 8 * (32 + 128) * (int)sizeof(FcMiss);
+    static constexpr int kBytes = kStageBytesAll + kMbarBytesAll + kQueueBytesAll;
+};
+
 // The packet stream is staged by TMA: every warp owns a ring of SRC::kStages
 // shared-memory slots and one mbarrier per slot; lane 0 keeps the ring full with
 // cp.async.bulk copies (one warp trip per slot), all lanes wait on the slot's
@@ -577,9 +596,14 @@ __device__ __forceinline__ void fc_drain32(uint32_t *__restrict__ words, const D
 template <int R, typename SRC>
 __global__ void __launch_bounds__(256, DHSA_FC_CTAS_PER_SM) k_scan_flowcache(SRC src, uint32_t *__restrict__ words, DevParams p)
 {
-    __shared__ FcMiss queue_s[8][32 + 128];
-    __shared__ __align__(128) uint8_t stage_s[8][SRC::kStages][SRC::kStageBytes];
-    __shared__ __align__(8) unsigned long long mbar_s[8][SRC::kStages];
+    // dynamic shared memory (FcSmem<SRC>::kBytes): per-warp stage rings, mbarriers, miss queues
+    extern __shared__ __align__(128) uint8_t fc_smem[];
+    typedef uint8_t StageRing[SRC::kStages][SRC::kStageBytes];
+    StageRing *stage_s = reinterpret_cast<StageRing *>(fc_smem);
+    typedef unsigned long long MbarRing[SRC::kStages];
+    MbarRing *mbar_s = reinterpret_cast<MbarRing *>(fc_smem + FcSmem<SRC>::kStageBytesAll);
+    typedef FcMiss MissQueue[32 + 128];
+    MissQueue *queue_s = reinterpret_cast<MissQueue *>(fc_smem + FcSmem<SRC>::kStageBytesAll + FcSmem<SRC>::kMbarBytesAll);
     const uint32_t lane = threadIdx.x & 31u, wib = threadIdx.x >> 5;
     FcMiss *q = queue_s[wib];
     uint32_t qn = 0;
@@ -767,47 +791,52 @@ __global__ void __launch_bounds__(256) k_plan_blockmax(const uint32_t *__restric
 {
     __shared__ uint32_t warp_max[8];
     const uint64_t lo = (uint64_t)blockIdx.x * DHSA_PLAN_BLOCK;
-    uint32_t m = 0;
+    uint32_t m = 0;  // floor division is monotone: max(ts) // w == max(ts // w), so divide once per block
     for (uint32_t q = threadIdx.x; q < DHSA_PLAN_BLOCK; q += 256) {
         const uint64_t t = lo + q;
-        if (t < n) m = max(m, rec_words[3 * t] / window_seconds);
+        if (t < n) m = max(m, rec_words[3 * t]);
     }
     for (int d = 16; d > 0; d >>= 1) m = max(m, __shfl_xor_sync(0xFFFFFFFFu, m, d));
     if ((threadIdx.x & 31) == 0) warp_max[threadIdx.x >> 5] = m;
     __syncthreads();
     if (threadIdx.x == 0) {
         for (int w = 1; w < 8; w++) m = max(m, warp_max[w]);
-        block_max[blockIdx.x] = m;
+        block_max[blockIdx.x] = m / window_seconds;
     }
 }
 
-// carry[b] = max(seed, block_max[0 .. b-1]) as a signed 64-bit value (seed -1 = no window open yet)
+// carry[b] = max(seed, block_max[0 .. b-1]) as a signed 64-bit value (seed -1 = no window open yet),
+// and the list of blocks in which the running maximum rises (the only ones pass 3 has to read).
+// One CTA: every thread takes a contiguous run of blocks, the runs' maxima are scanned across the CTA.
 __global__ void __launch_bounds__(1024) k_plan_carry(const uint32_t *__restrict__ block_max, uint64_t nblocks,
-                                                     long long seed, long long *__restrict__ carry)
+                                                     long long seed, long long *__restrict__ carry,
+                                                     uint32_t *__restrict__ rise_list, unsigned int *__restrict__ rise_count)
 {
     __shared__ long long warp_tot[32];
-    __shared__ long long running_s;
     const uint32_t lane = threadIdx.x & 31u, wid = threadIdx.x >> 5;
-    if (threadIdx.x == 0) running_s = seed;
+    const uint64_t per = (nblocks + 1023) / 1024;
+    const uint64_t lo = min((uint64_t)threadIdx.x * per, nblocks), hi = min(lo + per, nblocks);
+    long long local = -1;
+    for (uint64_t b = lo; b < hi; b++) local = max(local, (long long)block_max[b]);
+    long long inc = local;
+    for (int d = 1; d < 32; d <<= 1) {
+        const long long t = __shfl_up_sync(0xFFFFFFFFu, inc, d);
+        if (lane >= (uint32_t)d) inc = max(inc, t);
+    }
+    if (lane == 31) warp_tot[wid] = inc;
     __syncthreads();
-    for (uint64_t b0 = 0; b0 < nblocks; b0 += 1024) {
-        const uint64_t b = b0 + threadIdx.x;
-        const long long mine = b < nblocks ? (long long)block_max[b] : -1;
-        long long inc = mine;
-        for (int d = 1; d < 32; d <<= 1) {
-            const long long t = __shfl_up_sync(0xFFFFFFFFu, inc, d);
-            if (lane >= (uint32_t)d) inc = max(inc, t);
+    long long run = seed;
+    for (uint32_t w = 0; w < wid; w++) run = max(run, warp_tot[w]);
+    long long excl = __shfl_up_sync(0xFFFFFFFFu, inc, 1);
+    if (lane == 0) excl = -1;
+    run = max(run, excl);
+    for (uint64_t b = lo; b < hi; b++) {
+        const long long mine = (long long)block_max[b];
+        carry[b] = run;
+        if (mine > run) {
+            rise_list[atomicAdd(rise_count, 1u)] = (uint32_t)b;
+            run = mine;
         }
-        if (lane == 31) warp_tot[wid] = inc;
-        __syncthreads();
-        long long before = running_s;  // everything before this chunk
-        for (uint32_t w = 0; w < wid; w++) before = max(before, warp_tot[w]);
-        long long excl = __shfl_up_sync(0xFFFFFFFFu, inc, 1);
-        if (lane == 0) excl = -1;
-        if (b < nblocks) carry[b] = max(before, excl);
-        __syncthreads();
-        if (threadIdx.x == 1023) running_s = max(before, inc);
-        __syncthreads();
     }
 }
 
@@ -818,47 +847,52 @@ struct PlanBoundary {
 
 __global__ void __launch_bounds__(256) k_plan_boundaries(const uint32_t *__restrict__ rec_words, uint64_t n,
                                                          uint32_t window_seconds,
-                                                         const uint32_t *__restrict__ block_max,
                                                          const long long *__restrict__ carry,
+                                                         const uint32_t *__restrict__ rise_list,
+                                                         const unsigned int *__restrict__ rise_count,
                                                          PlanBoundary *__restrict__ out, unsigned int cap,
                                                          unsigned int *__restrict__ count)
 {
-    // no record of this block raises the running maximum: nothing to find, nothing to read
-    if ((long long)block_max[blockIdx.x] <= carry[blockIdx.x]) return;
-    // 256 threads x 16 consecutive records: thread-local running max, block scan of the
-    // per-thread maxima, then each thread replays its 16 records against its own carry-in
+    // only blocks in which the running maximum rises are visited (a handful per chunk of a
+    // time-ordered trace).  256 threads x 16 consecutive records: thread-local running max, block
+    // scan of the per-thread maxima, then each thread replays its 16 records against its own carry-in
     __shared__ long long warp_tot[8];
     const uint32_t lane = threadIdx.x & 31u, wid = threadIdx.x >> 5;
-    const uint64_t t0 = (uint64_t)blockIdx.x * DHSA_PLAN_BLOCK + (uint64_t)threadIdx.x * 16;
-    long long win[16];
-    long long tmax = -1;
+    const unsigned int n_rise = *rise_count;
+    for (unsigned int r = blockIdx.x; r < n_rise; r += gridDim.x) {
+        const uint32_t blk = rise_list[r];
+        const uint64_t t0 = (uint64_t)blk * DHSA_PLAN_BLOCK + (uint64_t)threadIdx.x * 16;
+        long long win[16];
+        long long tmax = -1;
 #pragma unroll
-    for (int q = 0; q < 16; q++) {
-        win[q] = t0 + q < n ? (long long)(rec_words[3 * (t0 + q)] / window_seconds) : -1;
-        tmax = max(tmax, win[q]);
-    }
-    long long inc = tmax;
-    for (int d = 1; d < 32; d <<= 1) {
-        const long long t = __shfl_up_sync(0xFFFFFFFFu, inc, d);
-        if (lane >= (uint32_t)d) inc = max(inc, t);
-    }
-    if (lane == 31) warp_tot[wid] = inc;
-    __syncthreads();
-    long long run = carry[blockIdx.x];
-    for (uint32_t w = 0; w < wid; w++) run = max(run, warp_tot[w]);
-    long long excl = __shfl_up_sync(0xFFFFFFFFu, inc, 1);
-    if (lane == 0) excl = -1;
-    run = max(run, excl);
+        for (int q = 0; q < 16; q++) {
+            win[q] = t0 + q < n ? (long long)(rec_words[3 * (t0 + q)] / window_seconds) : -1;
+            tmax = max(tmax, win[q]);
+        }
+        long long inc = tmax;
+        for (int d = 1; d < 32; d <<= 1) {
+            const long long t = __shfl_up_sync(0xFFFFFFFFu, inc, d);
+            if (lane >= (uint32_t)d) inc = max(inc, t);
+        }
+        if (lane == 31) warp_tot[wid] = inc;
+        __syncthreads();
+        long long run = carry[blk];
+        for (uint32_t w = 0; w < wid; w++) run = max(run, warp_tot[w]);
+        long long excl = __shfl_up_sync(0xFFFFFFFFu, inc, 1);
+        if (lane == 0) excl = -1;
+        run = max(run, excl);
 #pragma unroll
-    for (int q = 0; q < 16; q++) {
-        if (win[q] > run) {
-            run = win[q];
-            const unsigned int pos = atomicAdd(count, 1u);
-            if (pos < cap) {
-                out[pos].position = t0 + q;
-                out[pos].window_id = run;
+        for (int q = 0; q < 16; q++) {
+            if (win[q] > run) {
+                run = win[q];
+                const unsigned int pos = atomicAdd(count, 1u);
+                if (pos < cap) {
+                    out[pos].position = t0 + q;
+                    out[pos].window_id = run;
+                }
             }
         }
+        __syncthreads();  // warp_tot is reused by the next block of this CTA
     }
 }
 

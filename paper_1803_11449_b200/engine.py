@@ -186,6 +186,7 @@ class DetectionEngine:
         self.device = device
         self.chunk_records = max(4, (int(chunk_records) + 3) & ~3)
         self._idle: List[Dhla] = []   # sketches nobody else holds any more, reset for reuse
+        self._planner: Optional[Dhla] = None
 
     def run(self, records, on_sealed: Optional[Callable[[Dhla], None]] = None) -> List[WindowResult]:
         """Detect super points per tumbling window.
@@ -266,13 +267,13 @@ class DetectionEngine:
         session: Optional[WindowSession] = None
         cap = 4096
         bounds = np.empty(cap, dtype=_BOUNDARY_DTYPE)
-        planner: Optional[Dhla] = None  # a 768-byte sketch whose handle runs the plan kernels
         for chunk, n in self._device_chunks(records):
             import torch
 
-            if planner is None:
-                planner = Dhla(DhgParams(r=3, g=8, k=8, alpha=8, key_width=16), device=self._device_index())
-                planner.use_stream(torch.cuda.current_stream(planner.device).cuda_stream)
+            if self._planner is None:  # a 768-byte sketch whose handle runs the plan kernels; kept across runs
+                self._planner = Dhla(DhgParams(r=3, g=8, k=8, alpha=8, key_width=16), device=self._device_index())
+            planner = self._planner
+            planner.use_stream(torch.cuda.current_stream(planner.device).cuda_stream)
             ptr = chunk.data_ptr()
             open_window = session.sketch.window_id if session is not None else -1
             n_b = C.c_uint32()
