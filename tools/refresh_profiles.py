@@ -10,14 +10,16 @@ TAG = sys.argv[1] if len(sys.argv) > 1 else "r01"
 OUT = "profiles"
 
 
-def ncu(page):
-    return subprocess.run(["ncu", "-i", f"gpurun_out/prof_scan_{TAG}.ncu-rep", "--page", page, "--csv"],
+def ncu(rep, page):
+    return subprocess.run(["ncu", "-i", f"gpurun_out/{rep}.ncu-rep", "--page", page, "--csv"],
                           capture_output=True, text=True).stdout
 
 
-raw = ncu("raw")
+raw = ncu(f"prof_scan_{TAG}", "raw")
+raw_vec4 = ncu(f"prof_vec4_{TAG}", "raw")
 open(f"{OUT}/{TAG}_k_scan_flowcache_raw.csv", "w").write(raw)
-open(f"{OUT}/{TAG}_k_scan_flowcache_details.csv", "w").write(ncu("details"))
+open(f"{OUT}/{TAG}_k_scan_flowcache_details.csv", "w").write(ncu(f"prof_scan_{TAG}", "details"))
+open(f"{OUT}/{TAG}_k_scan_vec4_mode2_raw.csv", "w").write(raw_vec4)
 KEYS = ['gpu__time_duration.sum', 'dram__bytes_read.sum', 'dram__bytes_write.sum',
         'gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed',
         'l1tex__m_l1tex2xbar_req_cycles_active.avg.pct_of_peak_sustained_elapsed',
@@ -26,9 +28,12 @@ KEYS = ['gpu__time_duration.sum', 'dram__bytes_read.sum', 'dram__bytes_write.sum
         'l1tex__t_sectors_pipe_lsu_mem_global_op_red.sum', 'l1tex__t_sectors_pipe_lsu_mem_global_op_st.sum',
         'l1tex__m_xbar2l1tex_read_sectors_mem_global_op_tma_ld.sum', 'lts__t_sectors.sum',
         'lts__t_sectors_srcunit_tex_op_read.sum', 'lts__t_sectors_srcunit_tex_op_red.sum',
+        'lts__t_sectors_srcunit_tex_op_write.sum', 'lts__t_requests_srcunit_ltcfabric.sum',
         'sm__throughput.avg.pct_of_peak_sustained_elapsed', 'sm__warps_active.avg.pct_of_peak_sustained_active',
         'smsp__issue_active.avg.pct_of_peak_sustained_active', 'launch__registers_per_thread', 'launch__grid_size',
-        'launch__block_size', 'sm__cycles_elapsed.avg', 'smsp__inst_executed.sum']
+        'launch__block_size', 'sm__cycles_elapsed.avg', 'smsp__inst_executed.sum',
+        'smsp__average_warps_issue_stalled_long_scoreboard_per_issue_active.ratio',
+        'smsp__average_warps_issue_stalled_short_scoreboard_per_issue_active.ratio']
 
 
 def pick(text):
@@ -38,17 +43,26 @@ def pick(text):
 
 
 summary = {
-    "k_scan_vec4<5,2> (scan mode test_agg, no flow cache; first capture of the round)":
-        pick(open(f"{OUT}/{TAG}_k_scan_vec4_mode2_raw.csv").read()),
-    "k_scan_flowcache<5,SoaSource> (scan mode auto/flow_cache, 64 MiB table, TMA-staged packet stream)": pick(raw),
+    "k_scan_vec4<5,2> (scan mode test_agg, no flow cache)": pick(raw_vec4),
+    "k_scan_flowcache<5,SoaSource> (scan mode auto/flow_cache: 32 MiB table of 32-bit (cand, h1(opp)) keys, "
+    "8 ways per sector, TMA-staged packet stream)": pick(raw),
 }
 json.dump(summary, open(f"{OUT}/{TAG}_scan_kernels_ncu_summary.json", "w"), indent=1)
-fc = list(summary.values())[1]
 conv = {'Mbyte': 1e6, 'Gbyte': 1e9, 'Kbyte': 1e3, 'byte': 1}
-traffic = sum(fc[k][0] * conv[fc[k][1]] for k in ('dram__bytes_read.sum', 'dram__bytes_write.sum'))
-t = json.load(open(f"{OUT}/{TAG}_traffic.json"))
-t['k_scan_flowcache<5>']['dram_bytes_per_launch'] = traffic
-json.dump(t, open(f"{OUT}/{TAG}_traffic.json", "w"), indent=1)
+
+
+def dram(entry):
+    return sum(entry[k][0] * conv[entry[k][1]] for k in ('dram__bytes_read.sum', 'dram__bytes_write.sum'))
+
+
+vec4, fc = list(summary.values())
+traffic = {
+    "source": f"ncu --set full captures summarised in profiles/{TAG}_scan_kernels_ncu_summary.json (one 100M-packet launch)",
+    "k_scan_flowcache<5>": {"dram_bytes_per_launch": dram(fc), "algorithmic_bytes_per_launch": 8e8,
+                            "note": "the 32 MiB key table and the 10 MiB sketch stay L2-resident: DRAM traffic is the packet stream"},
+    "k_scan_vec4<5,2>": {"dram_bytes_per_launch": dram(vec4), "algorithmic_bytes_per_launch": 8e8},
+}
+json.dump(traffic, open(f"{OUT}/{TAG}_traffic.json", "w"), indent=1)
 for k, v in fc.items():
     print(k, v)
 print("traffic", traffic)
@@ -56,6 +70,11 @@ print("traffic", traffic)
 shutil.copy(f"gpurun_out/launches_{TAG}.csv", f"{OUT}/{TAG}_launch_list_bench_steps2.csv")
 for name in ("", "_reference", "_test_agg", "_test", "_red"):
     shutil.copy(f"gpurun_out/bench_{TAG}{name}.json", f"{OUT}/{TAG}_bench{name}.json")
+for src, dst in ((f"config3_{TAG}.json", f"{TAG}_config3_1b_packet_window.json"),
+                 (f"config4_{TAG}.json", f"{TAG}_config4_ddos_contention.json"),
+                 (f"config5_{TAG}.json", f"{TAG}_config5_accuracy_sweep.json"),
+                 (f"tools_{TAG}.json", f"{TAG}_tools.json")):
+    shutil.copy(f"gpurun_out/{src}", f"{OUT}/{dst}")
 rows = [r for r in csv.reader(open(f"{OUT}/{TAG}_launch_list_bench_steps2.csv")) if len(r) > 10]
 hdr = rows[0]
 ki, vi = hdr.index('Kernel Name'), hdr.index('Metric Value')
