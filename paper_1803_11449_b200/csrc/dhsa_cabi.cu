@@ -15,8 +15,12 @@
 #include <stdlib.h>
 #include <string.h>
 
+#include <condition_variable>
+#include <deque>
 #include <mutex>
 #include <new>
+#include <thread>
+#include <vector>
 
 using namespace dhsa;
 
@@ -57,6 +61,14 @@ static const uint64_t kPinnedReports = 256;
 static const uint32_t kPinnedBoundaries = 64;  // report rows copied back inside the read-out graph
 static const int kStageBufs = 3;            // staging buffers of the host-input pipeline
 static const uint64_t kStagePackets = 1ull << 22;  // packets per staged chunk (16 MiB per array)
+static const int kHostSlots = 4;                    // pinned bounce slots for pageable host input
+static const uint64_t kHostSlotPackets = 1ull << 20;  // packets per slot (4 MiB per array)
+
+struct HostSlot {
+    uint32_t *cand, *opp;  // pinned
+    cudaEvent_t dma_done;  // the last copy out of this slot has finished
+    bool busy, used;
+};
 
 struct dhsa_sketch {
     dhsa_params_t params;
@@ -129,6 +141,13 @@ struct dhsa_sketch {
     cudaEvent_t ev_copied[kStageBufs], ev_scanned[kStageBufs];
     bool staging_ready;
     uint64_t stage_seq;
+
+    // pageable host input: pinned bounce slots filled by the calling threads (in parallel, outside mu)
+    HostSlot hslots[kHostSlots];
+    bool hslots_ready;
+    unsigned hslot_next;
+    std::mutex hmu;
+    std::condition_variable hcv;
 };
 
 static int use_device(const dhsa_sketch *s)
@@ -272,6 +291,12 @@ extern "C" int dhsa_destroy(dhsa_sketch_t *s)
             cudaEventDestroy(s->ev_scanned[b]);
         }
     }
+    if (s->hslots_ready)
+        for (int i = 0; i < kHostSlots; i++) {
+            cudaFreeHost(s->hslots[i].cand);
+            cudaFreeHost(s->hslots[i].opp);
+            cudaEventDestroy(s->hslots[i].dma_done);
+        }
     cudaFree(s->bits);
     cudaFree(s->plan_block_max);
     cudaFree(s->plan_carry);
@@ -791,32 +816,192 @@ static int ensure_staging(dhsa_sketch *s)
     return DHSA_OK;
 }
 
+// ---- parallel memcpy for pageable host input ---------------------------------------------
+// A pageable cudaMemcpyAsync is a single-threaded copy into the driver's bounce buffer
+// (measured 1.4 Gpps = 11 GB/s); PCIe takes 55 GB/s.  So pageable arrays are copied into pinned
+// slots by several host threads -- a small process-wide pool plus the caller -- and DMA'd from there.
+class CopyPool {
+public:
+    static CopyPool &get()
+    {
+        static CopyPool *pool = new CopyPool();  // leaked on purpose: no destructor races at exit
+        return *pool;
+    }
+    // dst <- src, split over the pool and the calling thread; returns when every byte is copied
+    void copy(void *dst, const void *src, size_t bytes)
+    {
+        const size_t piece_min = 1u << 19;
+        size_t pieces = bytes / piece_min;
+        if (pieces > workers_.size() + 1) pieces = workers_.size() + 1;
+        if (pieces <= 1) {
+            memcpy(dst, src, bytes);
+            return;
+        }
+        const size_t per = ((bytes / pieces) + 63) & ~(size_t)63;
+        Job job;
+        job.pending = (int)pieces - 1;
+        {
+            std::lock_guard<std::mutex> lk(mu_);
+            for (size_t i = 1; i < pieces; i++) {
+                const size_t lo = i * per, hi = (i + 1 == pieces) ? bytes : (i + 1) * per;
+                tasks_.push_back(Task{(char *)dst + lo, (const char *)src + lo, hi - lo, &job});
+            }
+        }
+        cv_.notify_all();
+        memcpy(dst, src, per);
+        std::unique_lock<std::mutex> lk(job.mu);
+        job.cv.wait(lk, [&] { return job.pending == 0; });
+    }
+
+private:
+    struct Job {
+        std::mutex mu;
+        std::condition_variable cv;
+        int pending;
+    };
+    struct Task {
+        char *dst;
+        const char *src;
+        size_t bytes;
+        Job *job;
+    };
+    CopyPool()
+    {
+        unsigned hw = std::thread::hardware_concurrency();
+        unsigned n = hw > 4 ? (hw - 2 < 6 ? hw - 2 : 6) : (hw > 1 ? hw - 1 : 0);
+        for (unsigned i = 0; i < n; i++) {
+            workers_.emplace_back([this] { run(); });
+            workers_.back().detach();
+        }
+    }
+    void run()
+    {
+        for (;;) {
+            Task t;
+            {
+                std::unique_lock<std::mutex> lk(mu_);
+                cv_.wait(lk, [&] { return !tasks_.empty(); });
+                t = tasks_.front();
+                tasks_.pop_front();
+            }
+            memcpy(t.dst, t.src, t.bytes);
+            std::lock_guard<std::mutex> lk(t.job->mu);
+            if (--t.job->pending == 0) t.job->cv.notify_one();
+        }
+    }
+    std::mutex mu_;
+    std::condition_variable cv_;
+    std::deque<Task> tasks_;
+    std::vector<std::thread> workers_;
+};
+
+static bool is_pageable(const void *p)
+{
+    cudaPointerAttributes a;
+    if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+        (void)cudaGetLastError();
+        return true;
+    }
+    return a.type == cudaMemoryTypeUnregistered;
+}
+
+static int ensure_host_slots(dhsa_sketch *s)
+{
+    std::lock_guard<std::mutex> lk(s->hmu);
+    if (s->hslots_ready) return DHSA_OK;
+    for (int i = 0; i < kHostSlots; i++) {
+        CU(cudaMallocHost(&s->hslots[i].cand, kHostSlotPackets * 4));
+        CU(cudaMallocHost(&s->hslots[i].opp, kHostSlotPackets * 4));
+        CU(cudaEventCreateWithFlags(&s->hslots[i].dma_done, cudaEventDisableTiming));
+        s->hslots[i].busy = s->hslots[i].used = false;
+    }
+    s->hslots_ready = true;
+    return DHSA_OK;
+}
+
+// One staged chunk: H2D from `cand`/`opp` (pinned, or pageable through the driver) into the device
+// ring on the copy stream, then its scan on the launch stream.  Lock held.
+static int stage_and_scan_locked(dhsa_sketch *s, const uint32_t *cand, const uint32_t *opp, uint64_t cnt,
+                                 cudaEvent_t also_record, int *buf_out)
+{
+    const int b = (int)(s->stage_seq % kStageBufs);
+    if (s->stage_seq >= (uint64_t)kStageBufs) CU(cudaStreamWaitEvent(s->copy_stream, s->ev_scanned[b], 0));
+    CU(cudaMemcpyAsync(s->stage_cand[b], cand, cnt * 4, cudaMemcpyHostToDevice, s->copy_stream));
+    CU(cudaMemcpyAsync(s->stage_opp[b], opp, cnt * 4, cudaMemcpyHostToDevice, s->copy_stream));
+    CU(cudaEventRecord(s->ev_copied[b], s->copy_stream));
+    if (also_record) CU(cudaEventRecord(also_record, s->copy_stream));
+    CU(cudaStreamWaitEvent(s->stream, s->ev_copied[b], 0));
+    if (int rc = scan_locked(s, s->stage_cand[b], s->stage_opp[b], cnt)) return rc;
+    CU(cudaEventRecord(s->ev_scanned[b], s->stream));
+    s->stage_seq++;
+    if (buf_out) *buf_out = b;
+    return DHSA_OK;
+}
+
+// Pageable arrays: every chunk is copied into a pinned slot by this thread (and the copy pool)
+// with no sketch lock held -- callers on several threads, as the reference's pool submits them
+// (pkg/src/dhsa/engine.py:81-86), fill different slots at once -- then queued under the lock.
+// The caller's arrays are no longer needed once the last chunk sits in its slot.
+static int update_host_pageable(dhsa_sketch *s, const uint32_t *cand_host, const uint32_t *opp_host, uint64_t n)
+{
+    if (int rc = ensure_host_slots(s)) return rc;
+    for (uint64_t off = 0; off < n; off += kHostSlotPackets) {
+        const uint64_t cnt = (n - off < kHostSlotPackets) ? (n - off) : kHostSlotPackets;
+        int slot = -1;
+        {
+            std::unique_lock<std::mutex> lk(s->hmu);
+            s->hcv.wait(lk, [&] {
+                for (int i = 0; i < kHostSlots; i++)
+                    if (!s->hslots[i].busy) return true;
+                return false;
+            });
+            // round robin: the slot whose last DMA is oldest, so filling it never waits for a copy in flight
+            for (int k = 0; k < kHostSlots && slot < 0; k++) {
+                const int i = (int)((s->hslot_next + k) % kHostSlots);
+                if (!s->hslots[i].busy) slot = i;
+            }
+            s->hslot_next = (unsigned)slot + 1u;
+            s->hslots[slot].busy = true;
+        }
+        HostSlot &h = s->hslots[slot];
+        int rc = DHSA_OK;
+        if (h.used && cudaEventSynchronize(h.dma_done) != cudaSuccess) rc = cuda_fail(cudaGetLastError(), "host slot wait");
+        if (rc == DHSA_OK) {
+            CopyPool::get().copy(h.cand, cand_host + off, cnt * 4);
+            CopyPool::get().copy(h.opp, opp_host + off, cnt * 4);
+            std::lock_guard<std::mutex> lk(s->mu);
+            rc = ensure_staging(s);
+            if (rc == DHSA_OK) rc = stage_and_scan_locked(s, h.cand, h.opp, cnt, h.dma_done, nullptr);
+            h.used = true;
+        }
+        {
+            std::lock_guard<std::mutex> lk(s->hmu);
+            h.busy = false;
+        }
+        s->hcv.notify_one();
+        if (rc != DHSA_OK) return rc;
+    }
+    return DHSA_OK;
+}
+
 // Host packets -> HBM staging ring -> scan.  Copies run on their own stream and
 // overlap the scan of the previous chunk; pinned sources are DMA'd in place,
-// pageable ones go through the driver's bounce buffers.  Returns once the last
-// byte of the caller's arrays has been read.
+// pageable ones through pinned slots filled by several host threads.  Returns once
+// the last byte of the caller's arrays has been read.
 extern "C" int dhsa_update_host(dhsa_sketch_t *s, const uint32_t *cand_host, const uint32_t *opp_host, uint64_t n)
 {
     NEED(s);
     if (n == 0) return DHSA_OK;
     NEED(cand_host);
     NEED(opp_host);
-    std::lock_guard<std::mutex> lk(s->mu);
     if (int rc = use_device(s)) return rc;
+    if (is_pageable(cand_host) || is_pageable(opp_host)) return update_host_pageable(s, cand_host, opp_host, n);
+    std::lock_guard<std::mutex> lk(s->mu);
     if (int rc = ensure_staging(s)) return rc;
     int last = -1;
     for (uint64_t off = 0; off < n; off += kStagePackets) {
         const uint64_t cnt = (n - off < kStagePackets) ? (n - off) : kStagePackets;
-        const int b = (int)(s->stage_seq % kStageBufs);
-        if (s->stage_seq >= (uint64_t)kStageBufs) CU(cudaStreamWaitEvent(s->copy_stream, s->ev_scanned[b], 0));
-        CU(cudaMemcpyAsync(s->stage_cand[b], cand_host + off, cnt * 4, cudaMemcpyHostToDevice, s->copy_stream));
-        CU(cudaMemcpyAsync(s->stage_opp[b], opp_host + off, cnt * 4, cudaMemcpyHostToDevice, s->copy_stream));
-        CU(cudaEventRecord(s->ev_copied[b], s->copy_stream));
-        CU(cudaStreamWaitEvent(s->stream, s->ev_copied[b], 0));
-        if (int rc = scan_locked(s, s->stage_cand[b], s->stage_opp[b], cnt)) return rc;
-        CU(cudaEventRecord(s->ev_scanned[b], s->stream));
-        s->stage_seq++;
-        last = b;
+        if (int rc = stage_and_scan_locked(s, cand_host + off, opp_host + off, cnt, nullptr, &last)) return rc;
     }
     if (last >= 0) CU(cudaEventSynchronize(s->ev_copied[last]));
     return DHSA_OK;
