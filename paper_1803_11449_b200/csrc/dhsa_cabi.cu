@@ -703,6 +703,108 @@ extern "C" int dhsa_record_tally_at_restore(dhsa_sketch_t *s, uint64_t *records_
     return DHSA_OK;
 }
 
+// ---- parallel memcpy for pageable host input ---------------------------------------------
+// A pageable cudaMemcpyAsync is a single-threaded copy into the driver's bounce buffer
+// (measured 1.4 Gpps = 11 GB/s); PCIe takes 55 GB/s.  So pageable arrays are copied into pinned
+// slots by several host threads -- a small process-wide pool plus the caller -- and DMA'd from there.
+class CopyPool {
+public:
+    static CopyPool &get()
+    {
+        static CopyPool *pool = new CopyPool();  // leaked on purpose: no destructor races at exit
+        return *pool;
+    }
+    // dst <- src, split over the pool and the calling thread; returns when every byte is copied
+    void copy(void *dst, const void *src, size_t bytes)
+    {
+        const size_t piece_min = 1u << 19;
+        size_t pieces = bytes / piece_min;
+        if (pieces > workers_.size() + 1) pieces = workers_.size() + 1;
+        if (pieces <= 1) {
+            memcpy(dst, src, bytes);
+            return;
+        }
+        const size_t per = ((bytes / pieces) + 63) & ~(size_t)63;
+        Job job;
+        job.pending = (int)pieces - 1;
+        {
+            std::lock_guard<std::mutex> lk(mu_);
+            for (size_t i = 1; i < pieces; i++) {
+                const size_t lo = i * per, hi = (i + 1 == pieces) ? bytes : (i + 1) * per;
+                tasks_.push_back(Task{(char *)dst + lo, (const char *)src + lo, hi - lo, &job});
+            }
+        }
+        cv_.notify_all();
+        memcpy(dst, src, per);
+        std::unique_lock<std::mutex> lk(job.mu);
+        job.cv.wait(lk, [&] { return job.pending == 0; });
+    }
+
+private:
+    struct Job {
+        std::mutex mu;
+        std::condition_variable cv;
+        int pending;
+    };
+    struct Task {
+        char *dst;
+        const char *src;
+        size_t bytes;
+        Job *job;
+    };
+    CopyPool()
+    {
+        unsigned hw = std::thread::hardware_concurrency();
+        unsigned n = hw > 4 ? (hw - 2 < 6 ? hw - 2 : 6) : (hw > 1 ? hw - 1 : 0);
+        for (unsigned i = 0; i < n; i++) {
+            workers_.emplace_back([this] { run(); });
+            workers_.back().detach();
+        }
+    }
+    void run()
+    {
+        for (;;) {
+            Task t;
+            {
+                std::unique_lock<std::mutex> lk(mu_);
+                cv_.wait(lk, [&] { return !tasks_.empty(); });
+                t = tasks_.front();
+                tasks_.pop_front();
+            }
+            memcpy(t.dst, t.src, t.bytes);
+            std::lock_guard<std::mutex> lk(t.job->mu);
+            if (--t.job->pending == 0) t.job->cv.notify_one();
+        }
+    }
+    std::mutex mu_;
+    std::condition_variable cv_;
+    std::deque<Task> tasks_;
+    std::vector<std::thread> workers_;
+};
+
+static bool is_pageable(const void *p)
+{
+    cudaPointerAttributes a;
+    if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+        (void)cudaGetLastError();
+        return true;
+    }
+    return a.type == cudaMemoryTypeUnregistered;
+}
+
+// Process-wide pinned bounce ring for pageable record buffers (per device, allocated on first use).
+static const int kBounceSlots = 4;
+static const uint64_t kBounceBytes = 8ull << 20;
+struct BounceRing {
+    std::mutex mu;
+    bool ready = false;
+    uint8_t *buf[kBounceSlots];
+    cudaEvent_t done[kBounceSlots];
+    bool used[kBounceSlots];
+    unsigned next = 0;
+};
+static BounceRing g_bounce[16];
+
 extern "C" int dhsa_copy_to_device_async(int device, void *dst_dev, const void *src_host, uint64_t nbytes,
                                          void *cuda_stream)
 {
@@ -710,7 +812,31 @@ extern "C" int dhsa_copy_to_device_async(int device, void *dst_dev, const void *
     NEED(dst_dev);
     NEED(src_host);
     CU(cudaSetDevice(device));
-    CU(cudaMemcpyAsync(dst_dev, src_host, nbytes, cudaMemcpyHostToDevice, (cudaStream_t)cuda_stream));
+    cudaStream_t stream = (cudaStream_t)cuda_stream;
+    if (!is_pageable(src_host) || device < 0 || device >= 16) {
+        CU(cudaMemcpyAsync(dst_dev, src_host, nbytes, cudaMemcpyHostToDevice, stream));
+        return DHSA_OK;
+    }
+    // pageable: several host threads copy into pinned slots, the DMA of a slot overlaps the fill of the next
+    BounceRing &r = g_bounce[device];
+    std::lock_guard<std::mutex> lk(r.mu);
+    if (!r.ready) {
+        for (int i = 0; i < kBounceSlots; i++) {
+            CU(cudaMallocHost(&r.buf[i], kBounceBytes));
+            CU(cudaEventCreateWithFlags(&r.done[i], cudaEventDisableTiming));
+            r.used[i] = false;
+        }
+        r.ready = true;
+    }
+    for (uint64_t off = 0; off < nbytes; off += kBounceBytes) {
+        const uint64_t cnt = nbytes - off < kBounceBytes ? nbytes - off : kBounceBytes;
+        const int i = (int)(r.next++ % kBounceSlots);
+        if (r.used[i]) CU(cudaEventSynchronize(r.done[i]));
+        CopyPool::get().copy(r.buf[i], (const uint8_t *)src_host + off, cnt);
+        CU(cudaMemcpyAsync((uint8_t *)dst_dev + off, r.buf[i], cnt, cudaMemcpyHostToDevice, stream));
+        CU(cudaEventRecord(r.done[i], stream));
+        r.used[i] = true;
+    }
     return DHSA_OK;
 }
 
@@ -814,95 +940,6 @@ static int ensure_staging(dhsa_sketch *s)
     s->staging_ready = true;
     s->stage_seq = 0;
     return DHSA_OK;
-}
-
-// ---- parallel memcpy for pageable host input ---------------------------------------------
-// A pageable cudaMemcpyAsync is a single-threaded copy into the driver's bounce buffer
-// (measured 1.4 Gpps = 11 GB/s); PCIe takes 55 GB/s.  So pageable arrays are copied into pinned
-// slots by several host threads -- a small process-wide pool plus the caller -- and DMA'd from there.
-class CopyPool {
-public:
-    static CopyPool &get()
-    {
-        static CopyPool *pool = new CopyPool();  // leaked on purpose: no destructor races at exit
-        return *pool;
-    }
-    // dst <- src, split over the pool and the calling thread; returns when every byte is copied
-    void copy(void *dst, const void *src, size_t bytes)
-    {
-        const size_t piece_min = 1u << 19;
-        size_t pieces = bytes / piece_min;
-        if (pieces > workers_.size() + 1) pieces = workers_.size() + 1;
-        if (pieces <= 1) {
-            memcpy(dst, src, bytes);
-            return;
-        }
-        const size_t per = ((bytes / pieces) + 63) & ~(size_t)63;
-        Job job;
-        job.pending = (int)pieces - 1;
-        {
-            std::lock_guard<std::mutex> lk(mu_);
-            for (size_t i = 1; i < pieces; i++) {
-                const size_t lo = i * per, hi = (i + 1 == pieces) ? bytes : (i + 1) * per;
-                tasks_.push_back(Task{(char *)dst + lo, (const char *)src + lo, hi - lo, &job});
-            }
-        }
-        cv_.notify_all();
-        memcpy(dst, src, per);
-        std::unique_lock<std::mutex> lk(job.mu);
-        job.cv.wait(lk, [&] { return job.pending == 0; });
-    }
-
-private:
-    struct Job {
-        std::mutex mu;
-        std::condition_variable cv;
-        int pending;
-    };
-    struct Task {
-        char *dst;
-        const char *src;
-        size_t bytes;
-        Job *job;
-    };
-    CopyPool()
-    {
-        unsigned hw = std::thread::hardware_concurrency();
-        unsigned n = hw > 4 ? (hw - 2 < 6 ? hw - 2 : 6) : (hw > 1 ? hw - 1 : 0);
-        for (unsigned i = 0; i < n; i++) {
-            workers_.emplace_back([this] { run(); });
-            workers_.back().detach();
-        }
-    }
-    void run()
-    {
-        for (;;) {
-            Task t;
-            {
-                std::unique_lock<std::mutex> lk(mu_);
-                cv_.wait(lk, [&] { return !tasks_.empty(); });
-                t = tasks_.front();
-                tasks_.pop_front();
-            }
-            memcpy(t.dst, t.src, t.bytes);
-            std::lock_guard<std::mutex> lk(t.job->mu);
-            if (--t.job->pending == 0) t.job->cv.notify_one();
-        }
-    }
-    std::mutex mu_;
-    std::condition_variable cv_;
-    std::deque<Task> tasks_;
-    std::vector<std::thread> workers_;
-};
-
-static bool is_pageable(const void *p)
-{
-    cudaPointerAttributes a;
-    if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
-        (void)cudaGetLastError();
-        return true;
-    }
-    return a.type == cudaMemoryTypeUnregistered;
 }
 
 static int ensure_host_slots(dhsa_sketch *s)
