@@ -139,6 +139,9 @@ int dhsa_seal(dhsa_sketch_t *s);
  *      pkg/src/dhsa/dhla.py:372 and pkg/tests/test_dhla.py:88-90) ----------------- */
 int dhsa_download_bits(dhsa_sketch_t *s, uint8_t *bits_host, uint64_t nbytes);
 int dhsa_upload_bits(dhsa_sketch_t *s, const uint8_t *bits_host, uint64_t nbytes);
+/* Dhla.estimator(i, j) (pkg/src/dhsa/dhla.py:107-109): the g/8 bytes of one cell (a copy). */
+int dhsa_download_cell(dhsa_sketch_t *s, int32_t array, uint64_t index, uint8_t *cell_host,
+                       uint64_t nbytes);
 
 /* ---- read-out ---------------------------------------------------------------- */
 

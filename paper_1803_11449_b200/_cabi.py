@@ -64,6 +64,7 @@ SIGNATURES = {
     "dhsa_seal": [_vp],
     "dhsa_download_bits": [_vp, _vp, _u64],
     "dhsa_upload_bits": [_vp, _vp, _u64],
+    "dhsa_download_cell": [_vp, C.c_int32, _u64, _vp, _u64],
     "dhsa_zero_counts": [_vp, _vp, _vp],
     "dhsa_hot_sets": [_vp, C.c_double, _vp, _vp],
     "dhsa_estimate": [_vp, C.c_double, C.POINTER(RestoreInfo)],

@@ -1066,6 +1066,24 @@ extern "C" int dhsa_download_bits(dhsa_sketch_t *s, uint8_t *bits_host, uint64_t
     return DHSA_OK;
 }
 
+extern "C" int dhsa_download_cell(dhsa_sketch_t *s, int32_t array, uint64_t index, uint8_t *cell_host, uint64_t nbytes)
+{
+    NEED(s);
+    NEED(cell_host);
+    const uint64_t cell_bytes = (uint64_t)s->params.g / 8;
+    if (array < 0 || array >= s->params.r || index >= (1ull << s->params.k))
+        return fail(DHSA_ECONFIG, "estimator (%d, %llu) outside the sketch's %d x 2^%d cells", array,
+                    (unsigned long long)index, s->params.r, s->params.k);
+    if (nbytes != cell_bytes) return fail(DHSA_EDATA, "cell buffer is %llu bytes, an estimator holds %llu",
+                                          (unsigned long long)nbytes, (unsigned long long)cell_bytes);
+    std::lock_guard<std::mutex> lk(s->mu);
+    if (int rc = use_device(s)) return rc;
+    const uint64_t off = (((uint64_t)array << s->params.k) + index) * cell_bytes;
+    CU(cudaMemcpyAsync(cell_host, s->bits + off, cell_bytes, cudaMemcpyDeviceToHost, s->stream));
+    CU(cudaStreamSynchronize(s->stream));
+    return DHSA_OK;
+}
+
 extern "C" int dhsa_upload_bits(dhsa_sketch_t *s, const uint8_t *bits_host, uint64_t nbytes)
 {
     NEED(s);

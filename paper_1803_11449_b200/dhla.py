@@ -145,6 +145,14 @@ class Dhla:
         _cabi.check(self._lib.dhsa_download_bits(self._h, out.ctypes.data, out.nbytes))
         return out
 
+    def estimator(self, i: int, j: int) -> np.ndarray:
+        """The g/8 bytes of estimator j of array i (pkg/src/dhsa/dhla.py:107-109).  A copy: the
+        reference returns a LinearEstimator view over its host array; here the bits live on the
+        device (wrap the bytes in the reference's LinearEstimator if that class is wanted)."""
+        out = np.empty(self.params.g // 8, dtype=np.uint8)
+        _cabi.check(self._lib.dhsa_download_cell(self._h, int(i), int(j), out.ctypes.data, out.nbytes))
+        return out
+
     def load_bits(self, bits: np.ndarray) -> None:
         p = self.params
         arr = np.ascontiguousarray(bits, dtype=np.uint8)

@@ -269,6 +269,19 @@ def test_auto_mode_falls_back_when_flows_do_not_repeat():
     assert sk.flow_cache_stats()[0] == 1_000_000
 
 
+def test_estimator_returns_one_cell():
+    # pkg/src/dhsa/dhla.py:107-109
+    sk = P.Dhla(P.DhgParams(**PARAM_SETS["small"]))
+    rnd = np.random.default_rng(3).integers(0, 256, size=sk.bits.shape, dtype=np.uint8)
+    sk.load_bits(rnd)
+    for i, j in ((0, 0), (2, 517), (4, 1023)):
+        assert np.array_equal(sk.estimator(i, j), rnd[i, j])
+    with pytest.raises(P.ConfigError):
+        sk.estimator(5, 0)
+    with pytest.raises(P.ConfigError):
+        sk.estimator(0, 1024)
+
+
 def test_reset_and_load_bits_round_trip():
     sk = P.Dhla(P.DhgParams(**PARAM_SETS["small"]))
     rnd = np.random.default_rng(2).integers(0, 256, size=sk.bits.shape, dtype=np.uint8)
