@@ -321,7 +321,7 @@ extern "C" int dhsa_destroy(dhsa_sketch_t *s)
     return DHSA_OK;
 }
 
-// The flow cache asserts "this pair's bits are in the sketch": it must be emptied
+// The flow cache asserts "this key's bits are in the sketch": it must be emptied
 // whenever bits can disappear (reset, upload).  Stream-ordered with the scans.
 static int clear_flow_cache_locked(dhsa_sketch *s, bool clear_stats = true)
 {
@@ -503,14 +503,18 @@ static void launch_scan_src(dhsa_sketch *s, int mode, const SRC &src)
     // 8 packets per lane, 4 CTAs/SM (spills) and L2::evict_last table loads were slower or equal; staging the
     // packet stream by TMA was 2-3% faster than register prefetch and is the only form kept
     default: {
-        // flow cache: dynamic shared memory (TMA stage rings + miss queues), 3 CTAs per SM
+        // flow cache: dynamic shared memory (TMA stage rings + miss queues), 3 CTAs per SM.
+        // The opt-in to more than 48 KB is per device, the occupancy is the same on every B200.
         static int occ = 0;
+        static bool opted_in[64] = {false};
         auto kernel = k_scan_flowcache<R, SRC>;
         const int smem = FcSmem<SRC>::kBytes;
-        if (!occ) {
+        if (s->device < 64 && !opted_in[s->device]) {
             cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-            if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kernel, 256, smem) != cudaSuccess || occ < 1) occ = 3;
+            opted_in[s->device] = true;
         }
+        if (!occ && (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kernel, 256, smem) != cudaSuccess || occ < 1))
+            occ = 3;
         kernel<<<grid_for(s, nvec, 256, occ), 256, smem, s->stream>>>(src, w, s->dp);
         break;
     }

@@ -130,7 +130,7 @@ class Dhla:
         _cabi.check(self._lib.dhsa_set_flow_cache(self._h, int(n_sets)))
 
     def flow_cache_stats(self) -> tuple:
-        """(pairs looked up, pairs found) since the last reset."""
+        """(keys looked up, keys found) since the last reset."""
         a, b = C.c_uint64(), C.c_uint64()
         _cabi.check(self._lib.dhsa_flow_cache_stats(self._h, C.byref(a), C.byref(b)))
         return int(a.value), int(b.value)
