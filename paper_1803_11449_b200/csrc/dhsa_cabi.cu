@@ -1424,12 +1424,17 @@ static int run_restore(dhsa_sketch *s, double theta, uint64_t max_candidates)
             }
             const uint64_t before = s->launches;
             cudaGraph_t graph = nullptr;
+            // captured on the sketch's own stream (the caller's may be the legacy default stream, which
+            // cannot capture); the instantiated graph launches on whatever stream the sketch uses
+            cudaStream_t launch_stream = s->stream;
+            s->stream = s->own_stream;
             cudaError_t e = cudaStreamBeginCapture(s->stream, cudaStreamCaptureModeThreadLocal);
             if (e == cudaSuccess) {
                 const int rc = enqueue_restore(s, theta, max_candidates);
                 e = cudaStreamEndCapture(s->stream, &graph);
                 if (rc != DHSA_OK && e == cudaSuccess) e = cudaErrorUnknown;
             }
+            s->stream = launch_stream;
             if (e == cudaSuccess) e = cudaGraphInstantiate(&s->restore_graph, graph, 0);
             if (graph) cudaGraphDestroy(graph);
             s->graph_kernels = s->launches - before;

@@ -1,0 +1,41 @@
+#!/bin/bash
+# compute-sanitizer over a small end-to-end run of every kernel family (memcheck, then racecheck and synccheck on the scan)
+mkdir -p gpurun_out
+cat > /tmp/san_small.py <<'PY'
+import sys
+import numpy as np
+sys.path.insert(0, ".")
+import paper_1803_11449_b200 as P
+from oracle import oracle as O
+
+cand, opp = O.distinct_pairs(40_000, 14)
+for host, fan, seed in [(2_000_000 + 7 * n, 2048, 600 + n) for n in range(4)]:
+    c, o = O.plant_pairs(host, fan, seed)
+    cand, opp = np.concatenate([cand, c]), np.concatenate([opp, o])
+pick = np.random.default_rng(0).integers(0, len(cand), size=4 * len(cand))
+cand, opp = cand[pick], opp[pick]
+ora = O.OracleSketch()
+ora.update_batch(cand, opp)
+want = ora.restore_superpoints(1024)
+for mode in ("red", "test", "test_agg", "flow_cache", "auto"):
+    sk = P.Dhla(P.DhgParams())
+    sk.set_scan_mode(mode)
+    sk.update_batch(cand, opp)
+    sk.update_batch(cand[:1001], opp[:1001])
+    assert np.array_equal(sk.bits, ora.bits), mode
+    got = sk.restore_superpoints(1024)
+    assert [(r.host, r.saturated) for r in got] == [(r.host, r.saturated) for r in want], mode
+# records through the engine (plan kernels, RecordSource scan), exact counter, generator
+cfg = P.GeneratorConfig(background_hosts=2_000, superpoints=4, duplicate_factor=3, window_seconds=600, start_ts=2100)
+got = P.generate_trace_device(cfg, seed=5, fmt="both")
+eng = P.DetectionEngine(P.WindowConfig(theta=1024, window_seconds=300))
+res = eng.run(got["records"])
+c = P.ExactCounter(expected_pairs=got["flows"])
+c.add_pairs(got["cand"], got["opp"])
+hosts, counts, n_pairs, n_hosts = c.result(min_count=1024)
+print("sanitizer run ok:", [len(r.reports) for r in res], n_pairs, n_hosts)
+PY
+for tool in memcheck racecheck synccheck; do
+  timeout 1500 compute-sanitizer --tool $tool --print-limit 20 python /tmp/san_small.py > gpurun_out/sanitize_$tool.log 2>&1
+  echo "$tool exit $?"; tail -4 gpurun_out/sanitize_$tool.log
+done
