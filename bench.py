@@ -195,10 +195,18 @@ def run_ours(args, rank: int, local_rank: int, world: int) -> None:
     from paper_1803_11449_b200 import _cabi
     from paper_1803_11449_b200.multi import ShardedWindow
 
+    # DHSA_BENCH_SAME_DEVICE=1: every rank on cuda:0 with gloo for the rendezvous -- a way to run the
+    # N > 1 code path (slicing, barriers, peer-mapped OR merge over CUDA IPC) on a one-GPU box; not a measurement
+    same_device = os.environ.get("DHSA_BENCH_SAME_DEVICE") == "1"
+    if same_device:
+        local_rank = 0
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if same_device:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=dev)
 
     def barrier():
         if world > 1:
@@ -404,8 +412,8 @@ def run_ours(args, rank: int, local_rank: int, world: int) -> None:
 
     log("records path done")
     # -- max over ranks
-    stats = torch.tensor([ms_total, scan_ms, readout_ms, e2e[0] if e2e else 0.0, reset_ms], device=dev,
-                         dtype=torch.float64)
+    stats = torch.tensor([ms_total, scan_ms, readout_ms, e2e[0] if e2e else 0.0, reset_ms],
+                         device="cpu" if same_device else dev, dtype=torch.float64)
     if world > 1:
         dist.all_reduce(stats, op=dist.ReduceOp.MAX)
     ms_total, scan_ms, readout_ms, e2e_ms, reset_ms = (float(v) for v in stats.tolist())

@@ -122,6 +122,13 @@ class Dhla:
         else:
             _cabi.check(self._lib.dhsa_set_stream(self._h, C.c_void_p(int(cuda_stream))))
 
+    @property
+    def stream_handle(self) -> int:
+        """The cudaStream_t this sketch launches on."""
+        ptr = C.c_void_p()
+        _cabi.check(self._lib.dhsa_get_stream(self._h, C.byref(ptr)))
+        return int(ptr.value or 0)
+
     def set_scan_mode(self, mode) -> None:
         _cabi.check(self._lib.dhsa_set_scan_mode(self._h, SCAN_MODES.get(mode, mode)))
 

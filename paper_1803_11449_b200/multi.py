@@ -72,6 +72,32 @@ class CudaMergeOps:
     def seal(self) -> None:
         self.sketch.seal()
 
+    def device_barrier(self, dist, group=None) -> bool:
+        """Barrier across the ranks that never stops the host: a one-element NCCL all-reduce
+        enqueued behind the sketch's kernels on the sketch's stream.  It completes on a rank only
+        when every rank has reached it -- i.e. finished the kernels queued before it -- and the
+        kernels queued after it wait for it.  False (and nothing enqueued) when the process group
+        is not NCCL; the caller then falls back to seal() + dist.barrier()."""
+        import torch
+
+        if dist.get_backend(group) != "nccl":
+            return False
+        handle = self.sketch.stream_handle
+        if handle == 0:   # legacy default stream: torch's current stream must be it
+            if torch.cuda.current_stream(self.sketch.device).cuda_stream != 0:
+                return False
+            ctx = None
+        else:
+            ctx = torch.cuda.stream(torch.cuda.ExternalStream(handle, device=f"cuda:{self.sketch.device}"))
+        if getattr(self, "_token", None) is None:
+            self._token = torch.zeros(1, dtype=torch.int32, device=f"cuda:{self.sketch.device}")
+        if ctx is None:
+            dist.all_reduce(self._token, group=group)
+        else:
+            with ctx:
+                dist.all_reduce(self._token, group=group)
+        return True
+
     def export_handle(self) -> bytes:
         buf = (C.c_uint8 * 64)()
         _cabi.check(self._lib.dhsa_ipc_export(self.sketch._h, buf))
@@ -121,28 +147,51 @@ class CudaMergeOps:
                                                    self.sketch.memory_bytes))
 
 
+def peer_pointers(ops, dist, group=None) -> dict:
+    """{rank: mapped sketch} of every peer.  The handle exchange and the mapping (hundreds of
+    microseconds per peer) happen once per sketch -- its allocation never moves -- and are kept
+    on the ops object; collective on the first call only."""
+    cache = getattr(ops, "_peer_ptrs", None)
+    if cache is None:
+        world, rank = dist.get_world_size(group), dist.get_rank(group)
+        handles: List[Optional[bytes]] = [None] * world
+        dist.all_gather_object(handles, ops.export_handle(), group=group)
+        cache = {q: ops.open_handle(handles[q]) for q in range(world) if q != rank}
+        ops._peer_ptrs = cache
+    return cache
+
+
+def release_peers(ops) -> None:
+    ops.close_handles()
+    ops._peer_ptrs = None
+
+
+def _barrier(ops, dist, group=None) -> None:
+    """All ranks' queued work is done before anything queued after this runs: stream-ordered on
+    the device when the ops object offers it, else drain the stream and meet on the host."""
+    fn = getattr(ops, "device_barrier", None)
+    if fn is not None and fn(dist, group):
+        return
+    ops.seal()
+    dist.barrier(group)
+
+
 def merge_p2p(ops, dist, group=None) -> None:
-    """Reduce-scatter(OR) + all-gather over peer-mapped sketches.  Collective."""
+    """Reduce-scatter(OR) + all-gather over peer-mapped sketches.  Collective.  With NCCL the
+    three barriers are stream-ordered all-reduces, so the whole merge is enqueued without a single
+    host synchronisation: [barrier][k_or_merge][barrier][k_copy_slice x (P-1)][barrier]."""
     world, rank = dist.get_world_size(group), dist.get_rank(group)
     if world == 1:
         return
     ranges = byte_ranges(ops.alloc_bytes, world)
-    handles: List[Optional[bytes]] = [None] * world
-    dist.all_gather_object(handles, ops.export_handle(), group=group)
-    ptrs = {q: ops.open_handle(handles[q]) for q in range(world) if q != rank}
-    try:
-        ops.seal()             # my scan has landed ...
-        dist.barrier(group)    # ... and so has everyone's
-        lo, hi = ranges[rank]
-        ops.or_from_peers([ptrs[q] for q in sorted(ptrs)], lo, hi)
-        ops.seal()
-        dist.barrier(group)    # every owner's range is final
-        for q in sorted(ptrs):
-            ops.copy_from_peer(ptrs[q], *ranges[q])
-        ops.seal()
-        dist.barrier(group)    # nobody resets while a peer still reads
-    finally:
-        ops.close_handles()
+    ptrs = peer_pointers(ops, dist, group)
+    _barrier(ops, dist, group)    # my scan has landed, and so has everyone's
+    lo, hi = ranges[rank]
+    ops.or_from_peers([ptrs[q] for q in sorted(ptrs)], lo, hi)
+    _barrier(ops, dist, group)    # every owner's range is final
+    for q in sorted(ptrs):
+        ops.copy_from_peer(ptrs[q], *ranges[q])
+    _barrier(ops, dist, group)    # nobody resets while a peer still reads
 
 
 def merge_allgather(ops, dist, group=None) -> None:
@@ -176,6 +225,7 @@ class ShardedWindow:
         self.sketch = Dhla(params, device=device)
         self.ops = CudaMergeOps(self.sketch)
         self.merged_with = None
+        self._p2p_ok: Optional[bool] = None
 
     @property
     def world(self) -> int:
@@ -209,6 +259,10 @@ class ShardedWindow:
         import torch
 
         dist = self._dist
+        if self._p2p_ok is not None:     # agreed once; the topology does not change between windows
+            if self._p2p_ok:
+                merge_p2p(self.ops, dist, self.group)
+            return self._p2p_ok
         # agree up front whether every rank can map its peers (collective decision)
         can = 1
         try:
@@ -221,10 +275,20 @@ class ShardedWindow:
         flag = torch.tensor([can], dtype=torch.int32,
                             device=f"cuda:{self.sketch.device}" if on_gpu else "cpu")
         dist.all_reduce(flag, op=dist.ReduceOp.MIN, group=self.group)
-        if int(flag.item()) == 0:
-            return False
-        merge_p2p(self.ops, dist, self.group)
-        return True
+        self._p2p_ok = int(flag.item()) != 0
+        if self._p2p_ok:
+            merge_p2p(self.ops, dist, self.group)
+        return self._p2p_ok
+
+    def close(self) -> None:
+        """Unmap the peers' sketches (kept mapped across windows)."""
+        release_peers(self.ops)
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
 
     def restore(self):
         return self.sketch.restore_superpoints(self.theta, max_candidates=self.max_candidates)

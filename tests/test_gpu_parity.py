@@ -667,8 +667,21 @@ def _ipc_rank(rank, world, port, mode, q):
         ok = (np.array_equal(win.sketch.bits, ora.bits)
               and [(r.host, r.saturated) for r in got] == [(r.host, r.saturated) for r in want]
               and len(got) == 3)
+        # a second window on the same sketches: peers stay mapped, the agreed merge kind is reused
+        opened = len(win.ops._opened)
+        win.reset()
+        win.scan(cand[lo:hi][::2].copy(), opp[lo:hi][::2].copy())
+        used2 = win.merge()
+        ora2 = O.OracleSketch()
+        ora2.update_batch(np.concatenate([cand[packet_slice(len(cand), r, world)[0]:packet_slice(len(cand), r, world)[1]][::2]
+                                          for r in range(world)]),
+                          np.concatenate([opp[packet_slice(len(cand), r, world)[0]:packet_slice(len(cand), r, world)[1]][::2]
+                                          for r in range(world)]), threads=2)
+        ok = ok and used2 == used and len(win.ops._opened) == opened == world - 1 \
+            and np.array_equal(win.sketch.bits, ora2.bits)
         q.put((rank, used, bool(ok)))
         dist.barrier()
+        win.close()
     finally:
         dist.destroy_process_group()
 
@@ -695,3 +708,50 @@ def test_sharded_window_merges_over_cuda_ipc_between_processes(world):
         assert p_.exitcode == 0
     assert sorted(r[0] for r in results) == list(range(world))
     assert all(used == "p2p" and ok for _, used, ok in results), results
+
+
+def _nccl_single_rank(port, q):
+    import os
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_1803_11449_b200.multi import CudaMergeOps
+
+    os.environ["MASTER_ADDR"], os.environ["MASTER_PORT"] = "127.0.0.1", str(port)
+    torch.cuda.set_device(0)
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    try:
+        sk = P.Dhla(P.DhgParams())
+        ops = CudaMergeOps(sk)
+        cand, opp = O.distinct_pairs(50_000, 3)
+        results = []
+        for stream in (None, torch.cuda.Stream()):          # the sketch's own stream, then a torch stream
+            if stream is not None:
+                sk.use_stream(stream.cuda_stream)
+            sk.update_batch(cand, opp)
+            results.append(ops.device_barrier(dist))         # a stream-ordered all-reduce behind the scan
+            results.append(ops.device_barrier(dist))
+            sk.seal()
+        torch.cuda.synchronize()
+        q.put((results, int(ops._token.item())))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_device_barrier_is_a_stream_ordered_nccl_all_reduce():
+    """The merge's barriers under NCCL (multi.CudaMergeOps.device_barrier): enqueued on the sketch's
+    stream, no host synchronisation.  One rank is all this box can give NCCL; the call sequence, the
+    stream hand-over and the token are what is checked."""
+    import os
+
+    import torch.multiprocessing as mp
+
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    p_ = ctx.Process(target=_nccl_single_rank, args=(29900 + os.getpid() % 1000, q))
+    p_.start()
+    results, token = q.get(timeout=300)
+    p_.join(timeout=60)
+    assert p_.exitcode == 0
+    assert results == [True] * 4 and token == 0

@@ -117,6 +117,19 @@ def _worker(rank, world, port, tmpdir, mode, kw, n_packets):
         ops = HostOps(sk, os.path.join(tmpdir, f"rank{rank}.bits"))
         if mode == "p2p":
             merge_p2p(ops, dist)
+            # a second window on the same sketches: peers stay mapped (no second handle exchange)
+            opened = len(ops.opened)
+            extra_c, extra_o = O.distinct_pairs(500, 72 + rank)
+            if kw.get("key_width", 32) < 32:
+                extra_c = extra_c & np.uint32((1 << kw["key_width"]) - 1)
+            sk.update_batch(extra_c, extra_o)
+            merge_p2p(ops, dist)
+            assert len(ops.opened) == opened == world - 1
+            for q in range(world):
+                ec, eo = O.distinct_pairs(500, 72 + q)
+                if kw.get("key_width", 32) < 32:
+                    ec = ec & np.uint32((1 << kw["key_width"]) - 1)
+                cand, opp = np.concatenate([cand, ec]), np.concatenate([opp, eo])
         else:
             merge_allgather(ops, dist)
         whole = O.OracleSketch(**kw)
