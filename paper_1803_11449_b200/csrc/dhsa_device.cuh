@@ -1466,6 +1466,8 @@ struct ExactTables {
                                  // [3] all-ones pair seen, [4] count of host 0xFFFFFFFF
 };
 
+#define DHSA_EXACT_MAX_PROBES 2048ull
+
 __device__ __forceinline__ void exact_bump_host(const ExactTables &t, uint32_t host)
 {
     if (host == 0xFFFFFFFFu) {
@@ -1474,7 +1476,8 @@ __device__ __forceinline__ void exact_bump_host(const ExactTables &t, uint32_t h
     }
     const unsigned long long tag = ((unsigned long long)host + 1ull) << 32;
     unsigned long long slot = mix64((unsigned long long)host) & t.host_mask;
-    for (unsigned long long probes = 0; probes <= t.host_mask; probes++, slot = (slot + 1) & t.host_mask) {
+    for (unsigned long long probes = 0; probes <= t.host_mask && probes < DHSA_EXACT_MAX_PROBES;
+         probes++, slot = (slot + 1) & t.host_mask) {
         unsigned long long cur = t.hosts[slot];
         if (cur == 0ull) {
             const unsigned long long prev = atomicCAS(t.hosts + slot, 0ull, tag | 1ull);
@@ -1508,6 +1511,7 @@ __global__ void __launch_bounds__(256) k_exact_insert(SRC src, ExactTables t)
         uint32_t cs[4], os[4];
         bool ok[4];
         src.unpack(raw, v, cs, os, ok, on_time, late);
+        if (*reinterpret_cast<volatile unsigned long long *>(t.header + 2)) break;  // flagged full: the result is void anyway
 #pragma unroll
         for (int j = 0; j < 4; j++) {
             if (!ok[j]) continue;
@@ -1522,7 +1526,10 @@ __global__ void __launch_bounds__(256) k_exact_insert(SRC src, ExactTables t)
             const unsigned long long stored = key + 1ull;
             unsigned long long slot = mix64(key) & t.pair_mask;
             bool placed = false;
-            for (unsigned long long probes = 0; probes <= t.pair_mask; probes++, slot = (slot + 1) & t.pair_mask) {
+            // A table under its planned load never probes far; a long probe run means it is (nearly) full:
+            // flag it and stop -- walking a full table from every lane would be quadratic -- the caller rebuilds larger.
+            for (unsigned long long probes = 0; probes <= t.pair_mask && probes < DHSA_EXACT_MAX_PROBES;
+                 probes++, slot = (slot + 1) & t.pair_mask) {
                 unsigned long long cur = t.pairs[slot];
                 if (cur == 0ull) {
                     cur = atomicCAS(t.pairs + slot, 0ull, stored);

@@ -120,7 +120,9 @@ def exact_oracle(records, direction: str = "src", device: Optional[int] = None, 
     n = raw.numel() // RECORD_BYTES
     if n == 0:
         return {}
-    expected = max(1 << 16, n * (2 if direction == "both" else 1) // 4)
+    # plan for every record being a distinct pair (a trace without repeats), up to 2^27 pairs = a 4 GiB
+    # table; a window with more distinct pairs than that grows by rebuilding
+    expected = min(max(1 << 16, n * (2 if direction == "both" else 1)), 1 << 27)
     while True:
         counter = ExactCounter(expected, device=dev_index)
         counter.add_records(raw, direction)

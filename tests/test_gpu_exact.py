@@ -82,3 +82,24 @@ def test_exact_oracle_scores_a_100m_packet_window():
     sk.update_batch(ct, ot)
     m = P.evaluate(sk.restore_superpoints(1024), dict(zip(h.tolist(), c.tolist())), 1024)
     assert m.n_true == 50 and m.fnr == 0.0 and m.fpr <= 0.05 and m.mean_rel_err <= 0.10   # SPEC C5 bounds
+
+
+def test_undersized_tables_fail_fast_and_exact_oracle_regrows():
+    """A table far too small for the window is flagged full after a bounded probe run (it used to be
+    walked end to end by every lane: 23 s for 1.4M pairs) and exact_oracle rebuilds it larger."""
+    import time
+
+    import torch
+
+    cand, opp = O.distinct_pairs(1_000_000, 123)
+    c = P.ExactCounter(expected_pairs=1024)
+    t0 = time.perf_counter()
+    c.add_pairs(torch.from_numpy(cand.view(np.int32)).cuda(), torch.from_numpy(opp.view(np.int32)).cuda())
+    with pytest.raises(P.CapacityError):
+        c.result()
+    assert time.perf_counter() - t0 < 5.0
+    rec = np.zeros(len(cand), dtype=P.TRACE_DTYPE)
+    rec["src"], rec["dst"] = cand, opp
+    got = P.exact_oracle(rec)
+    hosts, counts = np.unique(cand, return_counts=True)      # the pairs are distinct: count = multiplicity of the host
+    assert got == dict(zip(hosts.tolist(), counts.tolist()))
