@@ -758,8 +758,13 @@ private:
     };
     CopyPool()
     {
+        // helper threads: DHSA_COPY_THREADS, else up to 6 while leaving two cores to the application
         unsigned hw = std::thread::hardware_concurrency();
         unsigned n = hw > 4 ? (hw - 2 < 6 ? hw - 2 : 6) : (hw > 1 ? hw - 1 : 0);
+        if (const char *env = getenv("DHSA_COPY_THREADS")) {
+            const long v = strtol(env, nullptr, 10);
+            if (v >= 0 && v <= 64) n = (unsigned)v;
+        }
         for (unsigned i = 0; i < n; i++) {
             workers_.emplace_back([this] { run(); });
             workers_.back().detach();
