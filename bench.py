@@ -80,7 +80,7 @@ class ClockSampler:
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}",
-                 "--format=csv,noheader,nounits", "-lms", "100"],
+                 "--format=csv,noheader,nounits", "-lms", "20"],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.thread = threading.Thread(target=self._pump, daemon=True)
             self.thread.start()
@@ -284,28 +284,31 @@ def run_ours(args, rank: int, local_rank: int, world: int) -> None:
     evs = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(args.steps)]
     t_begin, t_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     launches0 = sk.launch_count
-    with ClockSampler(local_rank) as clocks:
-        barrier()
-        t_begin.record(stream)
-        # Windows are pipelined the way a live detector runs them: the read-out of window k is
-        # enqueued (dhsa_restore_begin), window k + 1's reset and scan are queued behind it, and only
-        # then are window k's reports collected (dhsa_restore_end) -- the device never waits for the host.
-        collected = []
-        for k in range(args.steps):
-            ev = evs[k]
-            ev[0].record(stream)
-            win.reset()
-            ev[3].record(stream)
-            win.scan(cand_d, opp_d)
-            ev[1].record(stream)
-            if k:
-                collected.append(win.restore_end())          # window k - 1
-            win.merge()
-            win.restore_begin()
-            ev[2].record(stream)
-        collected.append(win.restore_end())
-        t_end.record(stream)
-        barrier()
+    # clocks and throttle reasons are sampled (nvidia-smi, every 20 ms) from here to the end of the last timed
+    # leg: the device-resident region alone lasts a few milliseconds, the e2e and record legs ~0.2 s
+    clocks = ClockSampler(local_rank)
+    clocks.__enter__()
+    barrier()
+    t_begin.record(stream)
+    # Windows are pipelined the way a live detector runs them: the read-out of window k is
+    # enqueued (dhsa_restore_begin), window k + 1's reset and scan are queued behind it, and only
+    # then are window k's reports collected (dhsa_restore_end) -- the device never waits for the host.
+    collected = []
+    for k in range(args.steps):
+        ev = evs[k]
+        ev[0].record(stream)
+        win.reset()
+        ev[3].record(stream)
+        win.scan(cand_d, opp_d)
+        ev[1].record(stream)
+        if k:
+            collected.append(win.restore_end())          # window k - 1
+        win.merge()
+        win.restore_begin()
+        ev[2].record(stream)
+    collected.append(win.restore_end())
+    t_end.record(stream)
+    barrier()
     if args.warmup == 0:
         reports = collected[0]
     same = all([(r.host, r.estimate, r.saturated) for r in c] == [(r.host, r.estimate, r.saturated) for r in reports]
@@ -411,6 +414,7 @@ def run_ours(args, rank: int, local_rank: int, world: int) -> None:
         del rec_dev, raw_dev
 
     log("records path done")
+    clocks.__exit__(None, None, None)
     # -- max over ranks
     stats = torch.tensor([ms_total, scan_ms, readout_ms, e2e[0] if e2e else 0.0, reset_ms],
                          device="cpu" if same_device else dev, dtype=torch.float64)
