@@ -12,7 +12,9 @@ is one whole window: reset the sketch, scan every packet, (N > 1: OR-merge the
 per-GPU sketches), estimate, restore and threshold-filter the super points.
 
 One JSON line on rank 0 (see the keys below).  `value` is device-resident
-throughput; `e2e` pushes the same window from pinned HOST arrays through the
+throughput, windows pipelined the way a live detector runs them (window k's
+read-out is enqueued, window k+1's reset and scan are queued behind it, then
+window k's reports are collected; --no-pipeline waits per window instead); `e2e` pushes the same window from pinned HOST arrays through the
 public API (`Dhla.update_batch(numpy)` -> C ABI), host<->device copies inside
 the timed region.  `--impl reference` times the reference's own compiled CPU
 loops (oracle/_ref, or the oracle port when that is absent) on the host cores.
@@ -295,6 +297,9 @@ def run_ours(args, rank: int, local_rank: int, world: int) -> None:
     # then are window k's reports collected (dhsa_restore_end) -- the device never waits for the host.
     collected = []
     for k in range(args.steps):
+        if args.no_pipeline:                                  # every window waits for its own reports
+            collected.append(step_device(evs[k]))
+            continue
         ev = evs[k]
         ev[0].record(stream)
         win.reset()
@@ -306,7 +311,8 @@ def run_ours(args, rank: int, local_rank: int, world: int) -> None:
         win.merge()
         win.restore_begin()
         ev[2].record(stream)
-    collected.append(win.restore_end())
+    if not args.no_pipeline:
+        collected.append(win.restore_end())
     t_end.record(stream)
     barrier()
     if args.warmup == 0:
@@ -470,8 +476,9 @@ def run_ours(args, rank: int, local_rank: int, world: int) -> None:
             "vs_baseline": None, "dtype": "u32/u64 integer hashing + f64 estimates", "data": "synthetic",
             "config": {"workload": WORKLOAD, "packets_per_gpu": n, "distinct_flows": flows, "theta": THETA,
                        "scan_mode": args.scan_mode, "merge": win.merged_with,
-                       "pipeline": "reports of window k collected after window k+1's reset+scan are queued "
-                                   "(restore_begin/_end); every window's reports are read back",
+                       "pipeline": ("none: every window waits for its reports (--no-pipeline)" if args.no_pipeline else
+                                    "reports of window k collected after window k+1's reset+scan are queued "
+                                    "(restore_begin/_end); every window's reports are read back"),
                        "flow_cache": ({"mib": args.flow_cache_mib,
                                        "hit_rate": (fc_hits / fc_lookups) if fc_lookups else None}
                                       if args.scan_mode in ("flow_cache", "auto") else None),
@@ -527,6 +534,8 @@ def main() -> None:
     ap.add_argument("--no-parity", action="store_true")
     ap.add_argument("--no-probe", action="store_true")
     ap.add_argument("--no-records", action="store_true", help="skip the raw-record (DetectionEngine) leg")
+    ap.add_argument("--no-pipeline", action="store_true",
+                    help="collect every window's reports before the next window is queued (default: one window later)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
     rank = int(os.environ.get("RANK", "0"))
