@@ -1189,7 +1189,7 @@ static int launch_estimate(dhsa_sketch *s, double theta)
 }
 
 // K3: stage chain -> verified keys in s->keys, count in ctl->n_candidates.
-static int launch_restore_stages(dhsa_sketch *s, uint64_t max_candidates)
+static int launch_restore_stages(dhsa_sketch *s, uint64_t max_candidates, bool verify, int *last_buf)
 {
     if (int rc = ensure_candidates(s, max_candidates)) return rc;
     const int r = s->params.r, n_stages = r - 2;
@@ -1202,9 +1202,11 @@ static int launch_restore_stages(dhsa_sketch *s, uint64_t max_candidates)
                                                   s->sub[cur], s->cl0[cur], s->sub[cur ^ 1], s->cl0[cur ^ 1], s->ctl);
         cur ^= 1;
     }
-    k_verify_keys<<<grid, 256, 0, s->stream>>>(n_stages, s->dp, max_candidates, s->sub[cur], s->cl0[cur], s->keys,
-                                               s->ctl);
-    s->launches += (uint64_t)n_stages + 1;
+    if (verify)
+        k_verify_keys<<<grid, 256, 0, s->stream>>>(n_stages, s->dp, max_candidates, s->sub[cur], s->cl0[cur], s->keys,
+                                                   s->ctl);
+    if (last_buf) *last_buf = cur;
+    s->launches += (uint64_t)n_stages + (verify ? 1 : 0);
     CU(cudaGetLastError());
     return DHSA_OK;
 }
@@ -1337,8 +1339,9 @@ extern "C" int dhsa_candidate_hosts(dhsa_sketch_t *s, double theta, uint64_t max
     if (int rc = use_device(s)) return rc;
     if (int rc = refuse_if_restore_pending(s)) return rc;
     if (int rc = launch_estimate(s, theta)) return rc;
-    if (int rc = launch_restore_stages(s, max_candidates)) return rc;
-    k_sort_small<<<1, 1024, DHSA_SORT_SMEM_MAX * sizeof(uint64_t), s->stream>>>(s->keys, &s->ctl->n_candidates, s->ctl);
+    if (int rc = launch_restore_stages(s, max_candidates, true, nullptr)) return rc;
+    k_sort_small<<<1, 1024, DHSA_SORT_SMEM_MAX * sizeof(uint64_t), s->stream>>>(s->keys, &s->ctl->n_candidates, s->ctl,
+                                                                                 nullptr, 0);
     s->launches++;
     CU(cudaGetLastError());
     if (int rc = read_control(s)) return rc;
@@ -1398,12 +1401,15 @@ extern "C" int dhsa_shared_zero_counts(dhsa_sketch_t *s, const uint64_t *hosts_h
 static int enqueue_restore(dhsa_sketch *s, double theta, uint64_t max_candidates)
 {
     if (int rc = launch_estimate(s, theta)) return rc;
-    if (int rc = launch_restore_stages(s, max_candidates)) return rc;
+    int cur = 0;
+    if (int rc = launch_restore_stages(s, max_candidates, false, &cur)) return rc;
     const int grid = s->sm_count * 4;
-    k_reestimate<<<grid, 256, 0, s->stream>>>(s->bits, s->dp, theta, s->keys, s->packed, s->ctl);
-    k_sort_small<<<1, 1024, DHSA_SORT_SMEM_MAX * sizeof(uint64_t), s->stream>>>(s->packed, &s->ctl->n_reports, s->ctl);
-    k_emit_reports<<<grid, 256, 0, s->stream>>>(s->packed, s->params.g, s->reports, s->ctl);
-    s->launches += 3;
+    // verify + re-estimate, then sort + emit: two launches for what were four
+    k_verify_reestimate<<<grid, 256, 0, s->stream>>>(s->params.r - 2, s->dp, max_candidates, s->sub[cur], s->cl0[cur],
+                                                     s->bits, theta, s->keys, s->packed, s->ctl);
+    k_sort_small<<<1, 1024, DHSA_SORT_SMEM_MAX * sizeof(uint64_t), s->stream>>>(s->packed, &s->ctl->n_reports, s->ctl,
+                                                                                 s->reports, s->params.g);
+    s->launches += 2;
     CU(cudaGetLastError());
     CU(cudaMemcpyAsync(s->ctl_host, s->ctl, sizeof(Control), cudaMemcpyDeviceToHost, s->stream));
     const uint64_t rows = s->cand_cap < kPinnedReports ? s->cand_cap : kPinnedReports;
@@ -1833,7 +1839,7 @@ extern "C" int dhsa_exact_result(dhsa_exact_t *e, uint64_t min_count, uint64_t *
         CU(cudaFuncSetAttribute(k_sort_small, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 DHSA_SORT_SMEM_MAX * (int)sizeof(uint64_t)));
         k_sort_small<<<1, 1024, DHSA_SORT_SMEM_MAX * sizeof(uint64_t), st>>>(
-            reinterpret_cast<uint64_t *>(e->out), e->n_out, nullptr);
+            reinterpret_cast<uint64_t *>(e->out), e->n_out, nullptr, nullptr, 0);
     } else {
         const uint64_t len = pow2_ge(n);
         const int grid = exact_grid(e, len);

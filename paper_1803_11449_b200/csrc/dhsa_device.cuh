@@ -1292,25 +1292,40 @@ __device__ __forceinline__ uint64_t pack_report(int sz, double denom, uint64_t h
     return (cls << 33) | (host << 1) | (uint64_t)(sz == 0);
 }
 
-// For every candidate: SZ, estimate, keep if estimate >= theta (dhla.py:190-194).
-__global__ void __launch_bounds__(256) k_reestimate(const uint8_t *__restrict__ bits, DevParams p,
-                                                    double theta, const uint64_t *__restrict__ keys,
-                                                    uint64_t *__restrict__ packed, Control *ctl)
+// Verify + re-estimate in one launch: one warp per partial key of the last stage -- key-width
+// cut, dh0(key) == cl0 (dhla.py:213-216; k_verify_keys is the stand-alone form behind
+// _candidate_hosts), then SZ, the estimate and the threshold filter (dhla.py:183-194).
+__global__ void __launch_bounds__(256) k_verify_reestimate(int n_stages, DevParams p,
+                                                           unsigned long long max_candidates,
+                                                           const uint64_t *__restrict__ in_sub,
+                                                           const uint32_t *__restrict__ in_cl0,
+                                                           const uint8_t *__restrict__ bits, double theta,
+                                                           uint64_t *__restrict__ keys,
+                                                           uint64_t *__restrict__ packed, Control *ctl)
 {
+    if (blockIdx.x == 0 && threadIdx.x == 0 && !ctl->any_empty) {
+        for (int st = 0; st < n_stages; st++)  // the numbers of the CapacityError text, as in k_verify_keys
+            if (ctl->stage_counts[st] > max_candidates) {
+                ctl->fail_stage = st + 1;
+                ctl->fail_count = ctl->stage_counts[st];
+                break;
+            }
+    }
+    if (stage_blocked(ctl, n_stages, max_candidates)) return;
     const uint32_t lane = threadIdx.x & 31u;
-    const uint64_t n = ctl->n_candidates;
+    const uint64_t np = ctl->stage_counts[n_stages - 1];
     const double denom = ctl->denom;
     const int g = 1 << p.log2g;
     const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
-    for (uint64_t t = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; t < n; t += nwarps) {
-        const uint64_t key = keys[t];
-        const int sz = shared_zero_count_warp(bits, p, key, lane);
+    for (uint64_t q = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; q < np; q += nwarps) {
+        const uint64_t sub = in_sub[q];
+        if (sub >> p.key_width) continue;           // warp-uniform
+        if (dh0_of(p, sub) != in_cl0[q]) continue;  // warp-uniform
+        const int sz = shared_zero_count_warp(bits, p, sub, lane);
         if (lane == 0) {
+            keys[atomicAdd(&ctl->n_candidates, 1ull)] = sub;  // < np <= max_candidates
             const double est = corrected_estimate(g, sz == 0 ? 1 : sz, denom);
-            if (est >= theta) {
-                const unsigned long long pos = atomicAdd(&ctl->n_reports, 1ull);
-                packed[pos] = pack_report(sz, denom, key);
-            }
+            if (est >= theta) packed[atomicAdd(&ctl->n_reports, 1ull)] = pack_report(sz, denom, sub);
         }
     }
 }
@@ -1322,28 +1337,33 @@ struct ReportOut {
     int32_t shared_zero_count;
 };
 
+// One packed report -> the row handed back to the caller (SuperPointReport, dhla.py:50-54).
+__device__ __forceinline__ ReportOut unpack_report(uint64_t w, int g, double denom)
+{
+    const uint64_t cls = w >> 33;
+    const int sat = (int)(w & 1ull);
+    ReportOut r;
+    r.host = (w >> 1) & 0xFFFFFFFFull;
+    r.saturated = sat;
+    if (cls == DHSA_ZERO_CLASS) {
+        r.estimate = 0.0;
+        r.shared_zero_count = -1;  // not recoverable from the zero class; unused by callers
+    } else {
+        r.estimate = corrected_estimate(g, (int)cls, denom);
+        r.shared_zero_count = sat ? 0 : (int)cls;
+    }
+    return r;
+}
+
+// Only for report lists too long for the single-CTA sorter, which emits its own rows.
 __global__ void __launch_bounds__(256) k_emit_reports(const uint64_t *__restrict__ packed, int g,
                                                       ReportOut *__restrict__ out, const Control *ctl)
 {
     const uint64_t n = ctl->n_reports;
     const double denom = ctl->denom;
     const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-    for (uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; t < n; t += stride) {
-        const uint64_t w = packed[t];
-        const uint64_t cls = w >> 33;
-        const int sat = (int)(w & 1ull);
-        ReportOut r;
-        r.host = (w >> 1) & 0xFFFFFFFFull;
-        r.saturated = sat;
-        if (cls == DHSA_ZERO_CLASS) {
-            r.estimate = 0.0;
-            r.shared_zero_count = -1;  // not recoverable from the zero class; unused by callers
-        } else {
-            r.estimate = corrected_estimate(g, (int)cls, denom);
-            r.shared_zero_count = sat ? 0 : (int)cls;
-        }
-        out[t] = r;
-    }
+    for (uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; t < n; t += stride)
+        out[t] = unpack_report(packed[t], g, denom);
 }
 
 // ------------------------------------------------------------------- sort --
@@ -1352,9 +1372,11 @@ __global__ void __launch_bounds__(256) k_emit_reports(const uint64_t *__restrict
 // beyond that the host drives the global bitonic passes below.
 #define DHSA_SORT_SMEM_MAX 8192
 
+// emit != nullptr: the sorted words are packed reports and their rows are written too
+// (sort + emit in one launch; the read-out chain is latency-bound, every launch is ~5 us).
 __global__ void __launch_bounds__(1024) k_sort_small(uint64_t *__restrict__ data,
                                                      const unsigned long long *__restrict__ n_ptr,
-                                                     Control *ctl)
+                                                     Control *ctl, ReportOut *__restrict__ emit, int g)
 {
     extern __shared__ uint64_t sm[];
     const uint64_t n = *n_ptr;
@@ -1380,6 +1402,10 @@ __global__ void __launch_bounds__(1024) k_sort_small(uint64_t *__restrict__ data
         }
     }
     for (uint32_t t = threadIdx.x; t < n; t += blockDim.x) data[t] = sm[t];
+    if (emit) {
+        const double denom = ctl->denom;
+        for (uint32_t t = threadIdx.x; t < n; t += blockDim.x) emit[t] = unpack_report(sm[t], g, denom);
+    }
     if (threadIdx.x == 0 && ctl) ctl->sorted = 1;
 }
 
