@@ -56,6 +56,9 @@ static int cuda_fail(cudaError_t e, const char *what)
 
 // ------------------------------------------------------------------ handle --
 
+#ifndef DHSA_READOUT_CTAS_PER_SM
+#define DHSA_READOUT_CTAS_PER_SM 4   // grid of the stage / verify / re-estimate kernels (grid-stride loops)
+#endif
 static const uint64_t kCounterBytes = 256;   // device counters kept behind the bit array
 static const uint64_t kPinnedReports = 256;
 static const uint32_t kPinnedBoundaries = 64;  // report rows copied back inside the read-out graph
@@ -1193,7 +1196,7 @@ static int launch_restore_stages(dhsa_sketch *s, uint64_t max_candidates, bool v
 {
     if (int rc = ensure_candidates(s, max_candidates)) return rc;
     const int r = s->params.r, n_stages = r - 2;
-    const int grid = s->sm_count * 4;
+    const int grid = s->sm_count * DHSA_READOUT_CTAS_PER_SM;
     k_stage_first<<<grid, 256, 0, s->stream>>>(s->lists, s->bitmaps, s->bitmap_words, s->dp, max_candidates,
                                                s->sub[0], s->cl0[0], s->ctl);
     int cur = 0;
@@ -1403,7 +1406,7 @@ static int enqueue_restore(dhsa_sketch *s, double theta, uint64_t max_candidates
     if (int rc = launch_estimate(s, theta)) return rc;
     int cur = 0;
     if (int rc = launch_restore_stages(s, max_candidates, false, &cur)) return rc;
-    const int grid = s->sm_count * 4;
+    const int grid = s->sm_count * DHSA_READOUT_CTAS_PER_SM;
     // verify + re-estimate, then sort + emit: two launches for what were four
     k_verify_reestimate<<<grid, 256, 0, s->stream>>>(s->params.r - 2, s->dp, max_candidates, s->sub[cur], s->cl0[cur],
                                                      s->bits, theta, s->keys, s->packed, s->ctl);
@@ -1498,7 +1501,7 @@ static int restore_end_locked(dhsa_sketch *s, dhsa_report_t *reports_host, uint6
         fill_info(s, info);
         return capacity_error(s, max_candidates);
     }
-    const int grid = s->sm_count * 4;
+    const int grid = s->sm_count * DHSA_READOUT_CTAS_PER_SM;
     const uint64_t n = s->ctl_host->n_reports;
     fill_info(s, info);
     // too small an output buffer: the read-out stays collectable, the caller retries with n_reports rows
