@@ -1,6 +1,6 @@
 """Randomised soak of the scan against the oracle: random window sizes, duplication, skew, scan
 modes, flow-cache sizes, batch splits and host/device inputs; bits must match every time.
-python tools/soak.py [seconds]"""
+python tests/checks/soak.py [seconds]"""
 import sys
 import time
 

@@ -1,6 +1,6 @@
 """Randomised soak of the record engine (row N1) against the oracle's restatement of the reference
 engine: random traces with out-of-order and far-future timestamps, window lengths, directions,
-chunk sizes, host and device inputs.  python tools/soak_engine.py [seconds]"""
+chunk sizes, host and device inputs.  python tests/checks/soak_engine.py [seconds]"""
 import sys
 import time
 

@@ -17,9 +17,9 @@ timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_sc
    python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu-baseline --no-parity --no-probe --no-records > gpurun_out/ncu_full.log 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_scan_vec4 -s 3 -c 1 -f -o gpurun_out/prof_vec4_${TAG} \
    python bench.py --steps 2 --warmup 3 --scan-mode test_agg --no-e2e --no-cpu-baseline --no-parity --no-probe --no-records > gpurun_out/ncu_full_vec4.log 2>&1
-timeout 900 python tools/contention.py > gpurun_out/config4_${TAG}.json 2> gpurun_out/config4.err
+timeout 900 python tests/checks/contention.py > gpurun_out/config4_${TAG}.json 2> gpurun_out/config4.err
 timeout 900 python tools/accuracy_sweep.py > gpurun_out/config5_${TAG}.json 2> gpurun_out/config5.err
-timeout 900 python tools/config3_window.py > gpurun_out/config3_${TAG}.json 2> gpurun_out/config3.err
+timeout 900 python tests/checks/config3_window.py > gpurun_out/config3_${TAG}.json 2> gpurun_out/config3.err
 PYTHONPATH=. timeout 600 python tools/tooling_timings.py > gpurun_out/tools_${TAG}.json 2> gpurun_out/tools.err
 tail -3 gpurun_out/pytest_gpu.log; tail -2 gpurun_out/smoke.log; cat gpurun_out/bench_${TAG}.json gpurun_out/bench_${TAG}_reference.json; tail -2 gpurun_out/ncu_full.log
 tail -3 gpurun_out/config3.err gpurun_out/config4.err gpurun_out/config5.err gpurun_out/tools.err; head -c 1500 gpurun_out/config3_${TAG}.json
