@@ -270,6 +270,8 @@ def run_ours(args, rank: int, local_rank: int, world: int) -> None:
         reports = step_device()
     parity = None
     if rank == 0 and not args.no_parity:
+        # the CPU leg as checker (never timed here, never on the product path): the oracle scans the
+        # window's distinct flows on the host and the GPU's bits / reports must equal its
         from oracle import oracle as O
         ora = O.OracleSketch()
         ora.update_batch(src, dst, threads=os.cpu_count() or 1)
