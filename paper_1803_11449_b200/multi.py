@@ -155,7 +155,13 @@ def peer_pointers(ops, dist, group=None) -> dict:
     if cache is None:
         world, rank = dist.get_world_size(group), dist.get_rank(group)
         handles: List[Optional[bytes]] = [None] * world
-        dist.all_gather_object(handles, ops.export_handle(), group=group)
+        try:
+            mine = ops.export_handle()
+        except Exception:
+            mine = None                    # still take part in the exchange: it is a collective
+        dist.all_gather_object(handles, mine, group=group)
+        if any(h is None for h in handles):
+            raise ConfigError("a rank could not export its sketch for peer mapping")
         cache = {q: ops.open_handle(handles[q]) for q in range(world) if q != rank}
         ops._peer_ptrs = cache
     return cache
@@ -259,23 +265,31 @@ class ShardedWindow:
         import torch
 
         dist = self._dist
-        if self._p2p_ok is not None:     # agreed once; the topology does not change between windows
-            if self._p2p_ok:
-                merge_p2p(self.ops, dist, self.group)
-            return self._p2p_ok
-        # agree up front whether every rank can map its peers (collective decision)
-        can = 1
-        try:
-            for q in range(torch.cuda.device_count()):
-                if q != self.sketch.device and not torch.cuda.can_device_access_peer(self.sketch.device, q):
-                    can = 0
-        except Exception:
-            can = 0
-        on_gpu = dist.get_backend(self.group) == "nccl"   # gloo rendezvous (tests) reduces on the host
-        flag = torch.tensor([can], dtype=torch.int32,
-                            device=f"cuda:{self.sketch.device}" if on_gpu else "cpu")
-        dist.all_reduce(flag, op=dist.ReduceOp.MIN, group=self.group)
-        self._p2p_ok = int(flag.item()) != 0
+        if self._p2p_ok is None:
+            # Agreed once (the topology does not change between windows): every rank exchanges its
+            # handle and tries to map every peer; one rank that cannot (no peer access, IPC refused
+            # by the container) sends everybody to the all-gather merge.
+            can = 1
+            try:
+                for q in range(torch.cuda.device_count()):
+                    if q != self.sketch.device and not torch.cuda.can_device_access_peer(self.sketch.device, q):
+                        can = 0
+            except Exception:
+                can = 0
+            try:
+                peer_pointers(self.ops, dist, self.group)      # collective exchange, local mapping
+            except Exception:
+                can = 0
+            on_gpu = dist.get_backend(self.group) == "nccl"   # gloo rendezvous (tests) reduces on the host
+            flag = torch.tensor([can], dtype=torch.int32,
+                                device=f"cuda:{self.sketch.device}" if on_gpu else "cpu")
+            dist.all_reduce(flag, op=dist.ReduceOp.MIN, group=self.group)
+            self._p2p_ok = int(flag.item()) != 0
+            if not self._p2p_ok:
+                try:
+                    release_peers(self.ops)
+                except Exception:
+                    pass
         if self._p2p_ok:
             merge_p2p(self.ops, dist, self.group)
         return self._p2p_ok
