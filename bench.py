@@ -1,7 +1,7 @@
 #!/usr/bin/env python
 """bench.py -- packets/s of one detection window (scan + estimate + restore + filter).
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config 2|3]
 
 Workload (BASELINE.json configs[1]): default DDH parameters (r=5, g=1024, k=14,
 alpha=6), theta 1024, a 100M-packet window per GPU: 150k uniform-address
@@ -10,14 +10,24 @@ scanners with 2048..8192 destinations (~3.8M distinct flows), every packet a
 uniform draw from the flow table (so ~26 packets per flow, shuffled).  A "step"
 is one whole window: reset the sketch, scan every packet, (N > 1: OR-merge the
 per-GPU sketches), estimate, restore and threshold-filter the super points.
+Both arms build the window with the same numpy code from the same seed
+(make_window), so they time the same packets.
 
 One JSON line on rank 0 (see the keys below).  `value` is device-resident
 throughput, windows pipelined the way a live detector runs them (window k's
 read-out is enqueued, window k+1's reset and scan are queued behind it, then
 window k's reports are collected; --no-pipeline waits per window instead); `e2e` pushes the same window from pinned HOST arrays through the
 public API (`Dhla.update_batch(numpy)` -> C ABI), host<->device copies inside
-the timed region.  `--impl reference` times the reference's own compiled CPU
-loops (oracle/_ref, or the oracle port when that is absent) on the host cores.
+the timed region; `e2e_dropin` feeds it the way the reference engine does --
+ordinary pageable numpy arrays, 65,536-pair batches, 1 and 8 feeder threads --
+through the reference's own unmodified WindowSession (baseline/_ref) holding the
+CUDA sketch.  `--impl reference` times the unmodified reference package on the
+host cores exactly as its own `dhsa bench` does (pkg/src/dhsa/cli.py:368-382:
+WindowSession(cfg, 0, "compiled", pool).feed_batch + seal, then restore).
+
+--config 3 (BASELINE.json configs[2]): ONE 1B-packet window split over the ranks
+by packet_slice, each rank generating only its slice on the device; strong
+scaling.  The default run is config 2, weak scaling at 100M packets per GPU.
 """
 from __future__ import annotations
 
@@ -38,6 +48,7 @@ if ROOT not in sys.path:
     sys.path.insert(0, ROOT)
 
 THETA = 1024
+CONTROL_BLOCK_BYTES = 1616   # sizeof(dhsa::Control), copied back with every read-out
 WORKLOAD = ("config2: 100M-packet window per GPU, default DDH (r5 g1024 k14 a6), 150k uniform background hosts "
             "(Zipf1.5 cardinality<=256) + 50 scanners (2048-8192), ~3.8M distinct flows, theta 1024")
 
@@ -60,6 +71,19 @@ def make_flows(seed: int, background_hosts: int = 150_000, scanners: int = 50):
     starts = np.repeat(np.cumsum(cards) - cards, cards).astype(np.uint64)
     dst = (np.repeat(bases, cards) + np.arange(len(src), dtype=np.uint64) - starts) & np.uint64(0xFFFFFFFF)
     return src.astype(np.uint32), dst.astype(np.uint32), hosts[background_hosts:].astype(np.uint32)
+
+
+def make_window(seed: int, n: int, rank: int = 0):
+    """(cand, opp, src, dst, scanners): the packets of one window -- n uniform draws from the flow
+    table, every flow at least once when n allows -- and the distinct flows they were drawn from.
+    Pure numpy from (seed, rank): the GPU arm and the reference arm time the same packets."""
+    src, dst, scanners = make_flows(seed)
+    flows = len(src)
+    rng = np.random.default_rng(seed * 1000 + rank + 1)
+    pick = rng.integers(0, flows, size=n, dtype=np.int64)
+    if rank == 0 and n >= flows:
+        pick[np.arange(flows, dtype=np.int64) * (n // flows)] = rng.permutation(flows)
+    return src[pick], dst[pick], src, dst, scanners
 
 
 def sha(a) -> str:
@@ -123,57 +147,88 @@ class ClockSampler:
 
 # ---------------------------------------------------------------- CPU baseline --
 
-def cpu_reference_window(cand: np.ndarray, opp: np.ndarray, threads: int):
-    """One window on the host cores with the reference's own compiled loops when
-    oracle/_ref holds them (kind "reference"), else the oracle's C port ("port").
-    Mirrors `dhsa bench` (/root/reference/pkg/src/dhsa/cli.py:371-382): batches of
-    65536 pairs handed to a thread pool sharing one sketch, seal, then restore."""
+REF_DIR = os.path.join(ROOT, "baseline", "_ref")
+
+
+def load_reference():
+    """The installed, unmodified reference package (baseline/install_reference.sh), or None."""
+    if not os.path.isdir(os.path.join(REF_DIR, "dhsa")):
+        return None
+    if REF_DIR not in sys.path:
+        sys.path.insert(0, REF_DIR)
+    try:
+        import dhsa
+        import dhsa.engine  # noqa: F401
+        from dhsa._kernels import available_backends
+        return dhsa if "compiled" in available_backends() else None
+    except Exception:
+        return None
+
+
+def reference_window(dhsa, cand: np.ndarray, opp: np.ndarray, threads: int):
+    """One window through the stock reference, as `dhsa bench` times it
+    (/root/reference/pkg/src/dhsa/cli.py:368-382): WindowSession(cfg, 0, "compiled", pool),
+    feed_batch (65,536-pair batches submitted to the pool) + seal, then restore (pure Python)."""
+    from dhsa.engine import WindowConfig, WindowSession
+
+    cfg = WindowConfig(workers=threads, theta=THETA)
+    pool = concurrent.futures.ThreadPoolExecutor(max_workers=threads) if threads > 1 else None
+    session = WindowSession(cfg, 0, "compiled", pool)
+    t0 = time.perf_counter()
+    session.feed_batch(cand, opp)
+    session.seal()
+    t_scan = time.perf_counter() - t0
+    if pool is not None:
+        pool.shutdown()
+    t1 = time.perf_counter()
+    reports = session.restore()
+    t_restore = time.perf_counter() - t1
+    return t_scan, t_scan + t_restore, reports
+
+
+def port_window(cand: np.ndarray, opp: np.ndarray, threads: int):
+    """Fallback when baseline/_ref did not travel: the oracle's C port of the same path."""
     from oracle import oracle as O
 
-    core = O.load_ref_core()
     ora = O.OracleSketch()
     t0 = time.perf_counter()
-    if core is not None:
-        kind = "reference"
-        mu = 65536  # engine.py:22 DEFAULT_BATCH_PAIRS
-        with concurrent.futures.ThreadPoolExecutor(max_workers=threads) as pool:
-            futs = [pool.submit(core.update_batch, ora.bits, ora.state_dh0, ora.state_h1, ora.k, ora.alpha,
-                                cand[s:s + mu], opp[s:s + mu]) for s in range(0, len(cand), mu)]
-            for f in futs:
-                f.result()
-    else:
-        kind = "port"
-        ora.update_batch(cand, opp, threads=threads)
+    ora.update_batch(cand, opp, threads=threads)
     t_scan = time.perf_counter() - t0
-    reports = ora.restore_superpoints(THETA)  # the reference's restore is pure Python: timed via the C port
-    t_all = time.perf_counter() - t0
-    return kind, t_scan, t_all, reports
+    reports = ora.restore_superpoints(THETA)
+    return t_scan, time.perf_counter() - t0, reports
+
+
+def cpu_window(cand, opp, threads):
+    dhsa = load_reference()
+    if dhsa is not None:
+        return ("reference",) + reference_window(dhsa, cand, opp, threads)
+    return ("port",) + port_window(cand, opp, threads)
 
 
 def run_reference(args, rank: int) -> None:
     if rank != 0:
         return
-    src, dst, _ = make_flows(args.seed)
+    n = args.packets
+    cand, opp, src, _, _ = make_window(args.seed, n, 0)
     threads = os.cpu_count() or 1
-    n = min(args.packets, args.cpu_sample)
-    rng = np.random.default_rng(args.seed + 1)
-    pick = rng.integers(0, len(src), size=n)
-    cand, opp = src[pick], dst[pick]
-    times = []
-    kind = "port"
+    times, kind, reports = [], "port", []
     for it in range(args.warmup + args.steps):
-        kind, _, t_all, _ = cpu_reference_window(cand, opp, threads)
+        kind, _, t_all, reports = cpu_window(cand, opp, threads)
         if it >= args.warmup:
             times.append(t_all)
     total = sum(times)
     mpps = n * len(times) / total / 1e6
-    sample = f"{n} packets drawn from the same flow table ({len(src)} flows), {threads} threads, batches of 65536"
+    sample = (f"the whole window: {n} packets over {len(src)} flows (the GPU arm's rank-0 window, same seed), "
+              f"{threads} threads, batches of 65536, "
+              + ("unmodified reference package from baseline/_ref: WindowSession.feed_batch + seal + restore"
+                 if kind == "reference" else "oracle C port (baseline/_ref absent)"))
     print(json.dumps({
         "impl": "reference", "metric": "packets/sec per detection window (scan+estimate+restore)",
         "value": mpps, "unit": "Mpps", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": 1e3 * total / len(times), "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "u32/u64 integer hashing + f64 estimates", "data": "synthetic",
-        "config": {"workload": WORKLOAD, "sample_packets": n, "theta": THETA},
+        "config": {"workload": WORKLOAD, "packets_per_gpu": n, "distinct_flows": len(src), "theta": THETA},
+        "n_superpoints": len(reports),
         "cpu_baseline": {"value": mpps, "unit": "Mpps", "cores": threads, "kind": kind, "sample": sample},
         "e2e": {"value": mpps, "unit": "Mpps", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }), flush=True)
@@ -208,6 +263,11 @@ def run_ours(args, rank: int, local_rank: int, world: int) -> None:
         if same_device:
             dist.init_process_group("gloo")
         else:
+            # NCCL's communicator lines stay on (stderr: stdout carries the JSON line), so a reader of the
+            # log can count the ranks that really joined
+            os.environ.setdefault("NCCL_DEBUG", "INFO")
+            os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+            os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
             dist.init_process_group("nccl", device_id=dev)
 
     def barrier():
@@ -215,19 +275,35 @@ def run_ours(args, rank: int, local_rank: int, world: int) -> None:
             dist.barrier()
         torch.cuda.synchronize()
 
-    n = args.packets
-    src, dst, scanners = make_flows(args.seed)
-    flows = len(src)
-    gen = torch.Generator(device=dev)
-    gen.manual_seed(args.seed * 1000 + rank)
-    src_d = torch.from_numpy(src.view(np.int32)).to(dev)
-    dst_d = torch.from_numpy(dst.view(np.int32)).to(dev)
-    pick = torch.randint(0, flows, (n,), device=dev, generator=gen)
-    if rank == 0 and n >= flows:
-        pick[:flows] = torch.arange(flows, device=dev)  # the window contains every flow at least once
-        pick = pick[torch.randperm(n, device=dev, generator=gen)]
-    cand_d, opp_d = src_d[pick].contiguous(), dst_d[pick].contiguous()
-    del pick
+    if args.config == 3:
+        # BASELINE config 3: ONE window of ~1B packets split over the ranks; each rank generates only
+        # its own packet slice, on the device (k_generate_trace), from the shared flow population
+        from paper_1803_11449_b200.multi import packet_slice
+        from paper_1803_11449_b200.traces import trace_population
+
+        base = P.GeneratorConfig(background_hosts=150_000, superpoints=50, duplicate_factor=1)
+        hosts, cards, bases = trace_population(base, args.seed)
+        src = np.repeat(hosts, cards)
+        ramp = (np.arange(len(src), dtype=np.int64) - np.repeat(np.cumsum(cards) - cards, cards)).astype(np.uint32)
+        dst = np.repeat(bases, cards) + ramp
+        scanners = hosts[cards >= 2048]
+        flows = len(src)
+        dup = max(1, round(args.window_packets / flows))
+        cfg3 = P.GeneratorConfig(background_hosts=150_000, superpoints=50, duplicate_factor=dup)
+        n_total = flows * dup
+        lo, hi = packet_slice(n_total, rank, world)
+        tr = P.generate_trace_device(cfg3, args.seed, device=local_rank, fmt="pairs", lo=lo, hi=hi)
+        cand_d, opp_d = tr["cand"], tr["opp"]
+        n = hi - lo
+        del tr
+    else:
+        n = args.packets
+        cand_np, opp_np, src, dst, scanners = make_window(args.seed, n, rank)
+        flows = len(src)
+        n_total = world * n
+        cand_d = torch.from_numpy(cand_np.view(np.int32)).to(dev)
+        opp_d = torch.from_numpy(opp_np.view(np.int32)).to(dev)
+        del cand_np, opp_np
     torch.cuda.synchronize()
 
     log(f"window generated: {n} packets over {flows} flows")
@@ -237,7 +313,7 @@ def run_ours(args, rank: int, local_rank: int, world: int) -> None:
     sk.set_flow_cache((args.flow_cache_mib << 20) // 32)
     stream = torch.cuda.Stream(dev)   # one stream for torch ops, the sketch's kernels and the timing events
     torch.cuda.set_stream(stream)
-    sk.use_stream(stream.cuda_stream)
+    sk.use_stream(stream)
 
     # -- roofline inputs measured here: random-address L2 rates (rank 0, N = 1 only)
     l2 = None
@@ -333,7 +409,7 @@ def run_ours(args, rank: int, local_rank: int, world: int) -> None:
     log(f"device-resident timing done: {ms_total / args.steps:.3f} ms per window")
     # -- timed: end to end from pinned host arrays through the public API
     e2e = None
-    if not args.no_e2e:
+    if not args.no_e2e and n <= 200_000_000:
         cand_h = torch.empty(n, dtype=torch.int32, pin_memory=True)
         opp_h = torch.empty(n, dtype=torch.int32, pin_memory=True)
         cand_h.copy_(cand_d)
@@ -360,11 +436,75 @@ def run_ours(args, rank: int, local_rank: int, world: int) -> None:
         e2e = (e2e_ms, len(reports_h))
         del cand_h, opp_h
 
+    # -- timed: the drop-in path.  The reference's own, unmodified WindowSession (baseline/_ref) with the
+    #    CUDA sketch in its seam, fed the way `dhsa bench` feeds it: ordinary
+    #    pageable numpy arrays, feed_batch cutting them into 65,536-pair batches that 1 or 8 pool
+    #    threads hand to update_batch, then seal and restore.  Wall clock around the whole window
+    #    (the device is idle before and drained after).
+    dropin = None
+    if world == 1 and not args.no_e2e and not args.no_dropin and n <= 200_000_000:
+        dhsa = load_reference()
+        cand_pg = cand_d.cpu().numpy().view(np.uint32).copy()      # pageable
+        opp_pg = opp_d.cpu().numpy().view(np.uint32).copy()
+        runs = []
+        for workers in (1, 8):
+            if dhsa is not None:
+                from dhsa.engine import WindowConfig as RefConfig, WindowSession as RefSession
+                import dhsa.engine as ref_engine
+                stock = ref_engine.Dhla
+                ref_engine.Dhla = lambda params, backend="auto", window_id=0: P.Dhla(params, backend="cuda",
+                                                                                     window_id=window_id, device=local_rank)
+                make = lambda pool: RefSession(RefConfig(workers=workers, theta=THETA), 0, "auto", pool)
+                engine = "reference WindowSession (baseline/_ref), unmodified"
+            else:
+                stock = None
+                make = lambda pool: P.WindowSession(P.WindowConfig(workers=workers, theta=THETA), 0, device=local_rank)
+                engine = "this package's WindowSession (baseline/_ref absent)"
+            try:
+                best, got = None, None
+                for rep in range(1 + max(1, min(args.steps, 3))):
+                    pool = concurrent.futures.ThreadPoolExecutor(max_workers=workers) if workers > 1 else None
+                    session = make(pool)
+                    session.sketch.set_scan_mode(args.scan_mode)
+                    torch.cuda.synchronize()
+                    t0 = time.perf_counter()
+                    if dhsa is not None or workers == 1:
+                        session.feed_batch(cand_pg, opp_pg)
+                    else:       # this package's session does not split: do what the reference's feed_batch does
+                        futs = [pool.submit(session.sketch.update_batch, cand_pg[q:q + 65536], opp_pg[q:q + 65536])
+                                for q in range(0, n, 65536)]
+                        for f in futs:
+                            f.result()
+                    session.seal()
+                    got = session.restore()
+                    dt = time.perf_counter() - t0
+                    if pool is not None:
+                        pool.shutdown()
+                    if rep and (best is None or dt < best):
+                        best = dt
+                ok = [(r.host, r.saturated) for r in got] == [(r.host, r.saturated) for r in reports]
+                runs.append({"feeder_threads": workers, "mpps": n / best / 1e6, "ms_per_window": best * 1e3,
+                             "reports_equal_device_run": bool(ok)})
+            finally:
+                if stock is not None:
+                    ref_engine.Dhla = stock
+        # what the engine's own hand-off costs with nothing behind it: the same number of pool.submit calls of
+        # a function that returns at once (CPython's executor + GIL; the library is not involved)
+        with concurrent.futures.ThreadPoolExecutor(max_workers=8) as pool:
+            t0 = time.perf_counter()
+            futs = [pool.submit(len, cand_pg[q:q + 65536]) for q in range(0, n, 65536)]
+            for f in futs:
+                f.result()
+            floor = time.perf_counter() - t0
+        dropin = {"engine": engine, "host_memory": "pageable numpy", "batch_pairs": 65536, "unit": "Mpps",
+                  "h2d_bytes_per_step": 8 * n, "runs": runs,
+                  "python_executor_floor_8_threads": {"us_per_batch": floor / len(futs) * 1e6, "mpps": n / floor / 1e6}}
+        del cand_pg, opp_pg
     log("end-to-end timing done")
     # -- row N1: the same window as raw 12-byte trace records through DetectionEngine (record decode,
     #    windowing, late drop and direction split fused into the scan).  Two windows, 1% late records.
     rec_stats = None
-    if world == 1 and not args.no_records:
+    if world == 1 and not args.no_records and args.config == 2:
         wsec = 300
         half = n // 2
         gen2 = torch.Generator(device=dev)
@@ -402,7 +542,7 @@ def run_ours(args, rank: int, local_rank: int, world: int) -> None:
         rec_stats = {"device_resident_mpps": n / (rec_ms * 1e-3) / 1e6, "ms_per_step": rec_ms,
                      "bytes_per_packet": 12, "windows": len(res), "late_dropped": n_late,
                      "counts_match": bool(ok), "superpoints_per_window": [len(r.reports) for r in res]}
-        if not args.no_e2e:
+        if not args.no_e2e and n <= 200_000_000:
             rec_h = torch.empty(n * 12, dtype=torch.uint8, pin_memory=True)
             rec_h.copy_(raw_dev)
             torch.cuda.synchronize()
@@ -456,62 +596,87 @@ def run_ours(args, rank: int, local_rank: int, world: int) -> None:
                     roofline["traffic"] = entry["dram_bytes_per_launch"]
                     roofline["traffic_source"] = "profiles/r01_traffic.json (ncu --set full)"
         if l2:
-            # The ceiling that actually binds (north star: the slower of HBM streaming and the sketch's
-            # L2 traffic): ncu shows the scan limited by one L1-miss request per clock per SM
-            # (l1tex__m_l1tex2xbar_req_cycles_active), which is what the random-address probe measures.
-            # Without the flow cache a packet needs 5 scattered sketch sectors (+0.25 packet-stream
-            # sectors); behind it a repeated flow needs 1 (+0.25).
             roofline["l2_probe"] = l2
-            roofline["hbm_ceiling_gpps"] = peak / 8.0
-            roofline["sketch_ceiling_gpps_5_accesses"] = l2["ld_gops"] / 5.25
-            roofline["red_ceiling_gpps_5_atomics"] = l2["red_gops"] / 5.0
-            req = 1.25 if args.scan_mode in ("flow_cache", "auto") else (5.0 if args.scan_mode == "red" else 5.25)
-            rate = l2["red_gops"] if args.scan_mode == "red" else l2["ld_gops"]
-            roofline["binding_ceiling_gpps"] = min(peak / 8.0, rate / req)
-            roofline["binding_requests_per_packet"] = req
+        # The ceiling that actually binds (north star: the slower of HBM streaming and the sketch's L2
+        # traffic).  ncu shows the scan limited by the SM's L1-miss request port -- one request per clock
+        # per SM -- not by DRAM.  Requests and REDs per packet come from the committed ncu capture of this
+        # kernel on this workload (profiles/r02_scan_counters.json, written by tools/ncu_counters.py from
+        # lts__t_requests_srcunit_tex / lts__t_sectors_srcunit_tex_op_red / sm__cycles_elapsed), never
+        # from a hand-set constant; the port rate is SMs x the SM clock sampled during this run.
+        roofline["hbm_ceiling_gpps"] = peak / 8.0
+        cpath = os.path.join(ROOT, "profiles", "r02_scan_counters.json")
+        ctr = json.load(open(cpath)).get(kernel) if os.path.exists(cpath) else None
+        clk = clocks.summary()
+        if ctr and n == ctr.get("packets_per_launch") and clk.get("sm_mhz"):
+            sms = torch.cuda.get_device_properties(dev).multi_processor_count
+            port = sms * clk["sm_mhz"] * 1e6 / 1e9                       # G requests/s the SMs can issue
+            req = ctr["l2_requests_per_packet"]
+            roofline["request_port_gps"] = port
+            roofline["l2_requests_per_packet"] = req
+            roofline["l2_red_per_packet"] = ctr["l2_red_per_packet"]
+            roofline["request_ceiling_gpps"] = port / req
+            if l2 and ctr["l2_red_per_packet"] > 0:
+                roofline["atomic_ceiling_gpps"] = l2["red_gops"] / ctr["l2_red_per_packet"]
+            ceilings = [roofline[k] for k in ("hbm_ceiling_gpps", "request_ceiling_gpps", "atomic_ceiling_gpps")
+                        if k in roofline]
+            roofline["binding_ceiling_gpps"] = min(ceilings)
             roofline["frac_of_binding_ceiling"] = roofline["scan_gpps"] / roofline["binding_ceiling_gpps"]
-        value = world * n * args.steps / (ms_total * 1e-3) / 1e6
+            roofline["ncu"] = {k: ctr[k] for k in ("request_port_busy_pct", "lts_throughput_pct", "dram_throughput_pct",
+                                                     "source") if k in ctr}
+        value = n_total * args.steps / (ms_total * 1e-3) / 1e6
+        workload = WORKLOAD if args.config == 2 else (
+            f"config3: ONE {n_total}-packet window (config 2's flow population, {n_total // flows} packets per flow) "
+            f"split over {world} GPU(s) by packet slices, generated on the device, OR-merged, theta 1024")
         line = {
             "metric": "packets/sec per detection window (scan+estimate+restore)",
             "value": value, "unit": "Mpps", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": ms_total / args.steps, "higher_is_better": True, "scaling": "weak",
+            "ms_per_step": ms_total / args.steps, "higher_is_better": True,
+            "scaling": "weak" if args.config == 2 else "strong",
             "vs_baseline": None, "dtype": "u32/u64 integer hashing + f64 estimates", "data": "synthetic",
-            "config": {"workload": WORKLOAD, "packets_per_gpu": n, "distinct_flows": flows, "theta": THETA,
-                       "scan_mode": args.scan_mode, "merge": win.merged_with,
+            "config": {"workload": workload, "packets_per_gpu": n, "window_packets": n_total if args.config == 3 else n,
+                       "distinct_flows": flows, "theta": THETA,
+                       "scan_mode": args.scan_mode, "scan_kernel_used": sk.scan_mode_used, "merge": win.merged_with,
                        "pipeline": ("none: every window waits for its reports (--no-pipeline)" if args.no_pipeline else
                                     "reports of window k collected after window k+1's reset+scan are queued "
                                     "(restore_begin/_end); every window's reports are read back"),
                        "flow_cache": ({"mib": args.flow_cache_mib,
                                        "hit_rate": (fc_hits / fc_lookups) if fc_lookups else None}
                                       if args.scan_mode in ("flow_cache", "auto") else None),
-                       "l2": "inputs (800 MB per GPU) larger than L2; sketch (10 MiB) L2-resident by design"},
+                       "l2": f"inputs ({8 * n / 1e6:.0f} MB per GPU) larger than L2; sketch (10 MiB) L2-resident by design"},
             "phase_ms": {"reset": reset_ms, "scan": scan_ms, "merge+estimate+restore+filter": readout_ms},
             "roofline": roofline,
             "gpu_launches": int(launches),
-            "clocks": clocks.summary(),
+            "clocks": clk,
         }
         if parity:
             line["parity"] = parity
         if rec_stats:
             line["records_path"] = rec_stats
         if e2e:
-            reports_bytes = 24 * e2e[1] + 1608  # dhsa_report_t rows + the 1608-byte control block read back per window
-            line["e2e"] = {"value": world * n * args.steps / (e2e_ms * 1e-3) / 1e6, "unit": "Mpps",
+            # dhsa_report_t rows + the control block + the window counters read back per window
+            reports_bytes = 24 * e2e[1] + CONTROL_BLOCK_BYTES + 48
+            line["e2e"] = {"value": n_total * args.steps / (e2e_ms * 1e-3) / 1e6, "unit": "Mpps",
                            "h2d_bytes_per_step": 8 * n, "d2h_bytes_per_step": reports_bytes,
                            "ms_per_step": e2e_ms / args.steps}
+        if dropin:
+            line["e2e_dropin"] = dropin
         if world == 1 and not args.no_cpu_baseline:
             m = min(n, args.cpu_sample)
             cand_s = cand_d[:m].cpu().numpy().view(np.uint32)
             opp_s = opp_d[:m].cpu().numpy().view(np.uint32)
             threads = os.cpu_count() or 1
-            cpu_reference_window(cand_s[: m // 4], opp_s[: m // 4], threads)  # page in, spin up the pool
-            kind, t_scan, t_all, _ = cpu_reference_window(cand_s, opp_s, threads)
+            cpu_window(cand_s[: m // 8], opp_s[: m // 8], threads)  # page in, spin up the pool
+            kind, t_scan, t_all, cpu_reports = cpu_window(cand_s, opp_s, threads)
             log("cpu baseline done")
             line["cpu_baseline"] = {
                 "value": m / t_all / 1e6, "unit": "Mpps", "cores": threads, "kind": kind,
-                "scan_only_mpps": m / t_scan / 1e6,
-                "sample": f"first {m} packets of the same window, {threads} threads sharing one sketch, "
-                          f"batches of 65536 (restore timed via the oracle's C port)"}
+                "scan_only_mpps": m / t_scan / 1e6, "restore_ms": (t_all - t_scan) * 1e3,
+                "sample": (f"{'the whole window' if m == n else 'first ' + str(m) + ' packets of the window'}, {threads} threads "
+                           f"sharing one sketch, batches of 65536; "
+                           + ("unmodified reference package (baseline/_ref): WindowSession.feed_batch + seal + restore, "
+                              "as pkg/src/dhsa/cli.py:368-382" if kind == "reference" else "oracle C port (baseline/_ref absent)")),
+                "reports_equal_gpu": [(r.host, r.saturated) for r in cpu_reports] == [(r.host, r.saturated) for r in reports]
+                if m == n else None}
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
@@ -528,7 +693,12 @@ def main() -> None:
     ap.add_argument("--scan-mode", default="auto", choices=["red", "test", "test_agg", "flow_cache", "auto"])
     ap.add_argument("--flow-cache-mib", type=int, default=32, help="flow cache size; flow_cache mode only")
     ap.add_argument("--merge", default="auto", choices=["auto", "p2p", "allgather"])
-    ap.add_argument("--cpu-sample", type=int, default=50_000_000)
+    ap.add_argument("--cpu-sample", type=int, default=100_000_000,
+                    help="packets of the window the in-run CPU baseline scans (default: the whole config-2 window)")
+    ap.add_argument("--config", type=int, default=2, choices=[2, 3],
+                    help="2: 100M packets per GPU, weak scaling (default); 3: one ~1B-packet window split over the ranks")
+    ap.add_argument("--window-packets", type=int, default=1_000_000_000, help="config 3: packets of the whole window")
+    ap.add_argument("--no-dropin", action="store_true", help="skip the reference-engine (pageable, 65,536-pair batches) leg")
     ap.add_argument("--traffic-bytes", type=float, default=None,
                     help="dram bytes per scan launch from the committed ncu capture (profiles/)")
     ap.add_argument("--no-e2e", action="store_true")

@@ -36,7 +36,7 @@
 extern "C" {
 #endif
 
-#define DHSA_ABI_VERSION 1
+#define DHSA_ABI_VERSION 2
 
 #define DHSA_OK 0
 #define DHSA_ECONFIG 2   /* ConfigError    pkg/src/dhsa/errors.py:12 */
@@ -48,8 +48,9 @@ extern "C" {
 #define DHSA_SCAN_TEST_RED 1      /* load the word, atomic only if the bit is still clear      */
 #define DHSA_SCAN_TEST_AGG_RED 2  /* as 1, and lanes of a warp hitting one word merge first    */
 #define DHSA_SCAN_FLOW_CACHE 3    /* as 2 behind an exact L2-resident cache of scanned pairs   */
-#define DHSA_SCAN_AUTO 4          /* default: 3, falling back to 2 for the rest of a window whose
-                                     flows do not repeat (cache hit rate below ~1/3)            */
+#define DHSA_SCAN_AUTO 4          /* default: 3; 2 for the rest of a window whose flows do not repeat
+                                     (cache hit rate below ~1/3); 1 while read-outs show at most
+                                     128 busy cells per array (a few candidates: words sit in L1) */
 
 typedef struct dhsa_sketch dhsa_sketch_t; /* opaque; replaces dhsa.dhla.Dhla, pkg/src/dhsa/dhla.py:57-68 */
 
@@ -88,6 +89,8 @@ typedef struct {
     uint64_t hot_counts[64];   /* |HE(i)|, dhla.py:111-119                                  */
     uint64_t stage_counts[64]; /* survivors after stage 1, 2, ... (r - 2 entries)           */
     int64_t zero_totals[64];   /* ZR(i), dhla.py:126                                        */
+    int32_t hot_cut;           /* hot <=> zc < g exp(-theta/g) <=> zc <= hot_cut (dhla.py:45-47,116) */
+    int32_t sz_cut;            /* reported <=> estimate >= theta <=> max(SZ, 1) <= sz_cut (dhla.py:183-192) */
 } dhsa_restore_info_t;
 
 int dhsa_abi_version(void);
@@ -99,7 +102,13 @@ const char *dhsa_last_error(void);
  * (pkg/src/dhsa/dhla.py:60-68).  Re-validates the DhgParams rules
  * (pkg/src/dhsa/dhg.py:78-105) -> DHSA_ECONFIG. */
 int dhsa_create(const dhsa_params_t *params, int device, dhsa_sketch_t **out);
+/* The reference builds one Dhla per window and drops it after the restore (engine.py:63,165-176);
+ * creating a device sketch, its first read-out and freeing it cost tens of milliseconds, so
+ * dhsa_destroy parks up to two sketches per (device, parameters) -- zeroed, in their initial
+ * state -- and dhsa_create hands a parked one out again.  dhsa_release_cached frees whatever is
+ * parked (and the page-locked / staging buffers kept for reuse). */
 int dhsa_destroy(dhsa_sketch_t *s);
+int dhsa_release_cached(void);
 /* Dhla.reset (pkg/src/dhsa/dhla.py:97-99). */
 int dhsa_reset(dhsa_sketch_t *s);
 /* Dhla.memory_bytes (pkg/src/dhsa/dhla.py:74-76). */
@@ -114,6 +123,9 @@ int dhsa_set_stream(dhsa_sketch_t *s, void *cuda_stream);
 int dhsa_set_own_stream(dhsa_sketch_t *s);
 int dhsa_get_stream(dhsa_sketch_t *s, void **cuda_stream);
 int dhsa_set_scan_mode(dhsa_sketch_t *s, int mode);
+/* The kernel variant (0..3) the last vectorised scan launch on this handle used: what
+ * DHSA_SCAN_AUTO resolved to. */
+int dhsa_scan_mode_used(const dhsa_sketch_t *s, int *mode);
 /* Flow cache of DHSA_SCAN_FLOW_CACHE: sets of 8 keys x 4 bytes = 32 bytes.  n_sets is rounded
  * down to a power of two and up to 2g (default 2^20 -> 32 MiB, allocated on first use;
  * 1024 <= n_sets <= 2^27).  The cache only ever skips a packet whose exact key (cand, h1(opp))
@@ -130,8 +142,19 @@ int dhsa_launch_count(const dhsa_sketch_t *s, uint64_t *n);
  *  (i, idx_i(cand[t])) of every array i. */
 int dhsa_update_device(dhsa_sketch_t *s, const uint32_t *cand_dev, const uint32_t *opp_dev,
                        uint64_t n);
+/* Host arrays.  Small batches -- the reference engine hands over 65,536 pairs at a time from a
+ * thread pool (pkg/src/dhsa/engine.py:22,78-86) -- are appended to page-locked accumulation slots
+ * by the calling threads, in parallel, and a slot is copied to the device and scanned when it is
+ * full or at the next barrier or read-out: the call returns once the caller's arrays have been
+ * read, every later read-out sees the batch.  Large page-locked arrays are DMA'd in place. */
 int dhsa_update_host(dhsa_sketch_t *s, const uint32_t *cand_host, const uint32_t *opp_host,
                      uint64_t n);
+/* dhsa_update_device for arrays produced on another stream than the sketch's (the caller's torch
+ * stream, say): ordered after what producer_stream has queued so far; producer_stream in turn
+ * waits for the scan, so the arrays may be released to it right after the call.  The sketch
+ * keeps its own launch stream. */
+int dhsa_update_device_from(dhsa_sketch_t *s, const uint32_t *cand_dev, const uint32_t *opp_dev,
+                            uint64_t n, void *producer_stream);
 /* WindowSession.seal's barrier (pkg/src/dhsa/engine.py:89-94): drain the stream. */
 int dhsa_seal(dhsa_sketch_t *s);
 
@@ -139,6 +162,10 @@ int dhsa_seal(dhsa_sketch_t *s);
  *      pkg/src/dhsa/dhla.py:372 and pkg/tests/test_dhla.py:88-90) ----------------- */
 int dhsa_download_bits(dhsa_sketch_t *s, uint8_t *bits_host, uint64_t nbytes);
 int dhsa_upload_bits(dhsa_sketch_t *s, const uint8_t *bits_host, uint64_t nbytes);
+/* The same for a byte range of the array: write_snapshot / read_snapshot (pkg/src/dhsa/dhla.py:321-373)
+ * stream the payload between the device and the file in pieces. */
+int dhsa_download_range(dhsa_sketch_t *s, uint64_t byte_lo, uint64_t nbytes, uint8_t *dst_host);
+int dhsa_upload_range(dhsa_sketch_t *s, uint64_t byte_lo, uint64_t nbytes, const uint8_t *src_host);
 /* Dhla.estimator(i, j) (pkg/src/dhsa/dhla.py:107-109): the g/8 bytes of one cell (a copy). */
 int dhsa_download_cell(dhsa_sketch_t *s, int32_t array, uint64_t index, uint8_t *cell_host,
                        uint64_t nbytes);
@@ -149,6 +176,11 @@ int dhsa_download_cell(dhsa_sketch_t *s, int32_t array, uint64_t index, uint8_t 
  * pkg/src/dhsa/dhla.py:103-105): zc_host = int64 (r, 2^k); zr_host (optional) =
  * per-array totals ZR(i) (pkg/src/dhsa/dhla.py:126). */
 int dhsa_zero_counts(dhsa_sketch_t *s, int64_t *zc_host, int64_t *zr_host);
+/* The zero_counts= argument of Dhla.hot_sets / estimate_flow_count / _candidate_hosts
+ * (pkg/src/dhsa/dhla.py:111-128,198-207): the next one of dhsa_hot_sets / dhsa_estimate /
+ * dhsa_candidate_hosts on this handle starts from zc_host (int64 (r, 2^k), each in [0, g])
+ * instead of counting the bits. */
+int dhsa_use_zero_counts(dhsa_sketch_t *s, const int64_t *zc_host);
 /* Dhla.hot_sets (pkg/src/dhsa/dhla.py:111-119, hot_threshold :45-47): row i of
  * lists_host (r x 2^k u64) holds counts_host[i] ascending indices. */
 int dhsa_hot_sets(dhsa_sketch_t *s, double theta, uint64_t *lists_host, uint64_t *counts_host);
@@ -179,6 +211,19 @@ int dhsa_restore(dhsa_sketch_t *s, double theta, uint64_t max_candidates,
 int dhsa_restore_begin(dhsa_sketch_t *s, double theta, uint64_t max_candidates);
 int dhsa_restore_end(dhsa_sketch_t *s, dhsa_report_t *reports_host, uint64_t reports_cap,
                      dhsa_restore_info_t *info);
+
+/* ---- the hash group, forward and inverse (stateless: parameters in, no sketch) ---------------
+ * dhg.forward_many (pkg/src/dhsa/dhg.py:203-210): indices_host = (n, r) u64, row t the r estimator
+ * indices of keys_host[t].
+ * dhg.reconstruct_key / reconstruct_many (pkg/src/dhsa/dhg.py:161-185, 213-233): tuples_host =
+ * (n, r) u64 index tuples; keys_host[t] = the rebuilt key (meaningless where rejected, as in the
+ * reference), ok_host[t] = 1 iff neighbouring blocks agree on their k - alpha overlapping bits, no
+ * bit lies above key_width and dh0(key) reproduces index 0 -- the accept predicate the restore
+ * stages apply incrementally. */
+int dhsa_forward_many(const dhsa_params_t *params, int device, const uint64_t *keys_host, uint64_t n,
+                      uint64_t *indices_host);
+int dhsa_reconstruct_many(const dhsa_params_t *params, int device, const uint64_t *tuples_host,
+                          uint64_t n, uint64_t *keys_host, uint8_t *ok_host);
 
 /* ---- record streams: the window engine's per-record work, fused into the scan --------
  * Records are the reference's 12-byte IPPR trace records (pkg/src/dhsa/ingest.py:20): u32

@@ -37,11 +37,13 @@ class RestoreInfo(C.Structure):
         ("flow_count", C.c_double), ("psi", C.c_double), ("denom", C.c_double),
         ("hot_counts", C.c_uint64 * 64), ("stage_counts", C.c_uint64 * 64),
         ("zero_totals", C.c_int64 * 64),
+        ("hot_cut", C.c_int32), ("sz_cut", C.c_int32),
     ]
 
 
 _vp = C.c_void_p
 _u64 = C.c_uint64
+ABI_VERSION = 2   # DHSA_ABI_VERSION of include/dhsa_b200.h
 
 # name -> argtypes; every symbol include/dhsa_b200.h declares (tests check the two agree)
 SIGNATURES = {
@@ -49,6 +51,7 @@ SIGNATURES = {
     "dhsa_last_error": [],
     "dhsa_create": [C.POINTER(Params), C.c_int, C.POINTER(_vp)],
     "dhsa_destroy": [_vp],
+    "dhsa_release_cached": [],
     "dhsa_reset": [_vp],
     "dhsa_sketch_bytes": [_vp, C.POINTER(_u64)],
     "dhsa_bits_device_ptr": [_vp, C.POINTER(_vp)],
@@ -56,16 +59,21 @@ SIGNATURES = {
     "dhsa_set_own_stream": [_vp],
     "dhsa_get_stream": [_vp, C.POINTER(_vp)],
     "dhsa_set_scan_mode": [_vp, C.c_int],
+    "dhsa_scan_mode_used": [_vp, C.POINTER(C.c_int)],
     "dhsa_set_flow_cache": [_vp, _u64],
     "dhsa_flow_cache_stats": [_vp, C.POINTER(_u64), C.POINTER(_u64)],
     "dhsa_launch_count": [_vp, C.POINTER(_u64)],
     "dhsa_update_device": [_vp, _vp, _vp, _u64],
     "dhsa_update_host": [_vp, _vp, _vp, _u64],
+    "dhsa_update_device_from": [_vp, _vp, _vp, _u64, _vp],
     "dhsa_seal": [_vp],
     "dhsa_download_bits": [_vp, _vp, _u64],
     "dhsa_upload_bits": [_vp, _vp, _u64],
+    "dhsa_download_range": [_vp, _u64, _u64, _vp],
+    "dhsa_upload_range": [_vp, _u64, _u64, _vp],
     "dhsa_download_cell": [_vp, C.c_int32, _u64, _vp, _u64],
     "dhsa_zero_counts": [_vp, _vp, _vp],
+    "dhsa_use_zero_counts": [_vp, _vp],
     "dhsa_hot_sets": [_vp, C.c_double, _vp, _vp],
     "dhsa_estimate": [_vp, C.c_double, C.POINTER(RestoreInfo)],
     "dhsa_candidate_hosts": [_vp, C.c_double, _u64, _vp, _u64, C.POINTER(RestoreInfo)],
@@ -73,6 +81,8 @@ SIGNATURES = {
     "dhsa_restore": [_vp, C.c_double, _u64, _vp, _u64, C.POINTER(RestoreInfo)],
     "dhsa_restore_begin": [_vp, C.c_double, _u64],
     "dhsa_restore_end": [_vp, _vp, _u64, C.POINTER(RestoreInfo)],
+    "dhsa_forward_many": [C.POINTER(Params), C.c_int, _vp, _u64, _vp],
+    "dhsa_reconstruct_many": [C.POINTER(Params), C.c_int, _vp, _u64, _vp, _vp],
     "dhsa_plan_windows": [_vp, _vp, _u64, C.c_uint32, C.c_int64, _vp, C.c_uint32, C.POINTER(C.c_uint32)],
     "dhsa_update_records_device": [_vp, _vp, _u64, _u64, _u64, C.c_uint32, C.c_uint32, C.c_int],
     "dhsa_record_tally": [_vp, C.POINTER(_u64), C.POINTER(_u64)],
@@ -119,8 +129,8 @@ def lib() -> C.CDLL:
                     fn.argtypes = argtypes
                     fn.restype = C.c_int
                 L.dhsa_last_error.restype = C.c_char_p
-                if L.dhsa_abi_version() != 1:
-                    raise ConfigError(f"libdhsa_b200.so ABI {L.dhsa_abi_version()} != 1")
+                if L.dhsa_abi_version() != ABI_VERSION:
+                    raise ConfigError(f"libdhsa_b200.so ABI {L.dhsa_abi_version()} != {ABI_VERSION}")
                 _lib = L
     return _lib
 

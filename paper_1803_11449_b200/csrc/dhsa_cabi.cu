@@ -15,8 +15,9 @@
 #include <stdlib.h>
 #include <string.h>
 
+#include <atomic>
+#include <chrono>
 #include <condition_variable>
-#include <deque>
 #include <mutex>
 #include <new>
 #include <thread>
@@ -64,13 +65,22 @@ static const uint64_t kPinnedReports = 256;
 static const uint32_t kPinnedBoundaries = 64;  // report rows copied back inside the read-out graph
 static const int kStageBufs = 3;            // staging buffers of the host-input pipeline
 static const uint64_t kStagePackets = 1ull << 22;  // packets per staged chunk (16 MiB per array)
-static const int kHostSlots = 4;                    // pinned bounce slots for pageable host input
+static const int kHostSlots = 6;                    // pinned accumulation slots for host input
 static const uint64_t kHostSlotPackets = 1ull << 20;  // packets per slot (4 MiB per array)
 
+// Host batches are appended into pinned slots and a slot is copied to the device and scanned once
+// it is full (or at the next barrier / read-out): the reference engine hands over 65,536-pair
+// batches (pkg/src/dhsa/engine.py:22,78-86), and one H2D copy + one kernel launch per batch is
+// launch-latency-bound at ~1 Gpps.  Callers on several threads reserve disjoint ranges of a slot
+// under a short lock and fill them in parallel outside it.
 struct HostSlot {
     uint32_t *cand, *opp;  // pinned
     cudaEvent_t dma_done;  // the last copy out of this slot has finished
-    bool busy, used;
+    bool dma_pending;      // ... and was queued: wait for it before refilling
+    int state;             // 0 free, 1 open (accepting reservations), 2 closed (writers may still be copying)
+    bool submitting;       // a thread holding the sketch lock is queueing this slot
+    uint64_t reserved;     // packets handed out to writers
+    uint64_t copied;       // packets whose memcpy has finished
 };
 
 struct dhsa_sketch {
@@ -79,6 +89,7 @@ struct dhsa_sketch {
     int device;
     int sm_count;
     int scan_mode;
+    int last_mode_used;     // kernel variant of the last vectorised scan launch (what auto resolved to)
     uint64_t nbytes;        // exact payload, r * 2^k * g/8
     uint64_t alloc_bytes;   // padded to 16 B
     uint8_t *bits;
@@ -86,21 +97,27 @@ struct dhsa_sketch {
     cudaStream_t copy_stream;
     std::mutex mu;
     uint64_t launches;
+    cudaEvent_t bridge_ev;  // orders a foreign producer stream with the launch stream (dhsa_update_device_from)
+    int occ[5][2];          // resident CTAs per SM of the scan kernel of [mode][packet source] (0 = not asked yet)
+    bool fc_opted_in[2];    // the flow-cache kernel's >48 KB dynamic shared memory was granted on this device
+    uint64_t mutation_seq;  // bumped by every call that can change the bits
 
     // flow cache of scan mode 3
     unsigned long long *fcache;
-    unsigned long long *fc_stats;  // device: lookups, hits
+    unsigned long long *fc_stats;  // device: flow-cache lookups, hits; test-first kernel packets, REDs (auto policy)
     uint32_t fc_sets;              // requested size in sets; the table is allocated on first use
     bool fc_dirty;                 // holds entries since the last clear
     unsigned long long *fc_stats_host;  // pinned snapshot of fc_stats for the auto policy
     cudaEvent_t fc_stats_ev;
     bool fc_stats_pending;
     bool auto_fell_back;           // auto mode: this window's flows do not repeat, use the 5-access kernel
+    bool regime_few_keys;          // auto mode: the traffic's keys sit in a handful of hot words (see the auto policy)
 
     // read-out workspaces
     Control *ctl;           // device
     Control *ctl_host;      // pinned mirror
     int32_t *zc;            // ncell
+    bool zc_given;          // s->zc holds counts handed in by the caller for the next read-out call
     uint32_t *lists;        // r * 2^k
     uint32_t *bitmaps;      // r * bitmap_words
     uint64_t bitmap_words;  // per array
@@ -108,12 +125,15 @@ struct dhsa_sketch {
     uint64_t *sub[2];
     uint32_t *cl0[2];
     uint64_t *keys;         // verified keys, then sorted candidates
+    int32_t *cand_sz;       // SZ of each verified key (k_verify_reestimate), kept for k_refilter
     uint64_t *packed;       // packed reports (padded to a power of two for the big sorter)
     uint64_t packed_cap;
     ReportOut *reports;
     uint64_t *hosts_in;     // shared_zero_counts input
     int32_t *sz_out;
     uint64_t hosts_in_cap;
+    void *host_tmp;         // pinned scratch of the array-returning read-out calls (grown on demand)
+    uint64_t host_tmp_bytes;
 
     // the read-out chain as a CUDA graph (captured once per theta / max_candidates / workspace)
     cudaGraphExec_t restore_graph;
@@ -124,9 +144,12 @@ struct dhsa_sketch {
     bool graph_disabled;
     ReportOut *reports_pinned;      // the first kPinnedReports rows land here with the control block
     cudaEvent_t restore_ev;         // read-out enqueued by dhsa_restore_begin has landed in the pinned mirrors
-    unsigned long long *tally_pinned;  // record tally as of the last read-out (copied with the control block)
+    unsigned long long *tally_pinned;  // the 6 window counters (record tally, flow cache, test kernel) as of the last read-out
     bool restore_pending;
     uint64_t restore_max_candidates;
+    double restore_theta;
+    uint64_t restore_seq;           // mutation_seq when the pending read-out was queued
+    int restore_last_buf;           // ping-pong buffer holding the last stage's partial keys
 
     // record streams
     unsigned long long *tally;      // device: records fed, records dropped
@@ -145,13 +168,44 @@ struct dhsa_sketch {
     bool staging_ready;
     uint64_t stage_seq;
 
-    // pageable host input: pinned bounce slots filled by the calling threads (in parallel, outside mu)
+    // host input: pinned accumulation slots filled by the calling threads (in parallel, outside mu)
     HostSlot hslots[kHostSlots];
     bool hslots_ready;
-    unsigned hslot_next;
-    std::mutex hmu;
+    unsigned hcur;            // slot taking reservations
+    std::mutex hmu;           // lock order: mu before hmu; never wait for mu while holding hmu
     std::condition_variable hcv;
 };
+
+// ---- per-device cache of the expensive-to-create pieces of a sketch ---------------------------
+// The reference creates one Dhla per window (pkg/src/dhsa/engine.py:63).  Page-locking 48 MB of
+// host memory, allocating the device staging ring and the flow-cache table cost tens of
+// milliseconds -- more than scanning a 100M-packet window -- so a destroyed sketch hands them to
+// the next one created on the same device instead of freeing them (at most kCachedSets of each).
+struct HostRingRes {
+    uint32_t *cand[kHostSlots], *opp[kHostSlots];
+    cudaEvent_t dma_done[kHostSlots];
+};
+struct StagingRes {
+    uint32_t *cand[kStageBufs], *opp[kStageBufs];
+    cudaEvent_t copied[kStageBufs], scanned[kStageBufs];
+};
+struct FlowCacheRes {
+    unsigned long long *table;
+    uint32_t sets;
+};
+static const size_t kCachedSets = 2;
+struct DeviceCache {
+    std::mutex mu;
+    std::vector<HostRingRes> rings;
+    std::vector<StagingRes> stagings;
+    std::vector<FlowCacheRes> tables;
+};
+static DeviceCache g_cache[64];
+static DeviceCache *cache_of(int device) { return device >= 0 && device < 64 ? &g_cache[device] : nullptr; }
+
+static const unsigned long long kPolicyMinSample = 1ull << 22;  // packets before the auto policy trusts a counter
+static void consume_policy_snapshots(dhsa_sketch *s, bool window_ends);
+static int flush_host_locked(dhsa_sketch *s);
 
 static int use_device(const dhsa_sketch *s)
 {
@@ -211,29 +265,19 @@ static void free_workspaces(dhsa_sketch *s)
         cudaFree(s->cl0[b]);
     }
     cudaFree(s->keys);
+    cudaFree(s->cand_sz);
     cudaFree(s->packed);
     cudaFree(s->reports);
     cudaFree(s->hosts_in);
     cudaFree(s->sz_out);
-    s->zc = nullptr, s->lists = nullptr, s->bitmaps = nullptr, s->keys = nullptr, s->packed = nullptr;
+    s->zc = nullptr, s->lists = nullptr, s->bitmaps = nullptr, s->keys = nullptr, s->packed = nullptr, s->cand_sz = nullptr;
     s->reports = nullptr, s->hosts_in = nullptr, s->sz_out = nullptr;
     s->sub[0] = s->sub[1] = nullptr, s->cl0[0] = s->cl0[1] = nullptr;
     s->cand_cap = s->packed_cap = s->hosts_in_cap = 0;
 }
 
-extern "C" int dhsa_create(const dhsa_params_t *params, int device, dhsa_sketch_t **out)
+static int create_locked(dhsa_sketch *s, const dhsa_params_t *params, int device)
 {
-    NEED(params);
-    NEED(out);
-    *out = nullptr;
-    int rc = validate(params);
-    if (rc) return rc;
-    int ndev = 0;
-    CU(cudaGetDeviceCount(&ndev));
-    if (device < 0 || device >= ndev) return fail(DHSA_ECONFIG, "device %d out of range (%d visible)", device, ndev);
-    CU(cudaSetDevice(device));
-    dhsa_sketch *s = new (std::nothrow) dhsa_sketch();
-    if (!s) return fail(-1, "out of host memory");
     s->params = *params;
     s->device = device;
     CU(cudaDeviceGetAttribute(&s->sm_count, cudaDevAttrMultiProcessorCount, device));
@@ -253,11 +297,7 @@ extern "C" int dhsa_create(const dhsa_params_t *params, int device, dhsa_sketch_
     s->bitmap_words = m >= 32 ? m / 32 : 1;
     // the window's counters (record tally, flow-cache statistics) sit right behind the
     // bit array, so a window reset is ONE memset
-    cudaError_t e = cudaMalloc(&s->bits, s->alloc_bytes + kCounterBytes);
-    if (e != cudaSuccess) {
-        delete s;
-        return cuda_fail(e, "cudaMalloc(bits)");
-    }
+    CU(cudaMalloc(&s->bits, s->alloc_bytes + kCounterBytes));
     CU(cudaStreamCreateWithFlags(&s->own_stream, cudaStreamNonBlocking));
     CU(cudaStreamCreateWithFlags(&s->copy_stream, cudaStreamNonBlocking));
     s->stream = s->own_stream;
@@ -267,14 +307,119 @@ extern "C" int dhsa_create(const dhsa_params_t *params, int device, dhsa_sketch_
     CU(cudaMallocHost(&s->ctl_host, sizeof(Control)));
     CU(cudaMallocHost(&s->reports_pinned, kPinnedReports * sizeof(ReportOut)));
     CU(cudaEventCreateWithFlags(&s->restore_ev, cudaEventDisableTiming));
-    CU(cudaMallocHost(&s->tally_pinned, 2 * sizeof(unsigned long long)));
-    s->tally_pinned[0] = s->tally_pinned[1] = 0;
+    CU(cudaEventCreateWithFlags(&s->bridge_ev, cudaEventDisableTiming));
+    CU(cudaMallocHost(&s->tally_pinned, 6 * sizeof(unsigned long long)));
+    memset(s->tally_pinned, 0, 6 * sizeof(unsigned long long));
     s->graph_disabled = getenv("DHSA_NO_GRAPH") != nullptr;
     CU(cudaMemsetAsync(s->bits, 0, s->alloc_bytes + kCounterBytes, s->stream));
     CU(cudaMemsetAsync(s->ctl, 0, sizeof(Control), s->stream));
     CU(cudaStreamSynchronize(s->stream));
     CU(cudaFuncSetAttribute(k_sort_small, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             DHSA_SORT_SMEM_MAX * (int)sizeof(uint64_t)));
+    return DHSA_OK;
+}
+
+// ---- parked sketches --------------------------------------------------------------------------
+// The reference builds a new Dhla for every window and drops it after the restore
+// (pkg/src/dhsa/engine.py:63,165-176).  On the device that is the expensive way round: creating a
+// sketch, its first read-out (64 MB of stage workspaces, the captured read-out graph) and freeing
+// it all again cost 40-80 ms -- several times the scan of a 100M-packet window.  So dhsa_destroy
+// parks up to kParkedPerKey sketches per (device, parameters) and kParkedTotal overall, zeroed and back in their initial
+// state, and dhsa_create hands a parked one out again.  dhsa_release_cached() frees them.
+static const size_t kParkedPerKey = 2;
+static const size_t kParkedTotal = 6;
+static std::mutex g_parked_mu;
+static std::vector<dhsa_sketch *> g_parked;
+
+static int clear_flow_cache_locked(dhsa_sketch *s, bool clear_stats);
+
+static bool same_key(const dhsa_sketch *s, const dhsa_params_t *p, int device)
+{
+    const dhsa_params_t &x = s->params;
+    return s->device == device && x.r == p->r && x.g == p->g && x.k == p->k && x.alpha == p->alpha &&
+           x.key_width == p->key_width && x.state_dh0 == p->state_dh0 && x.state_h1 == p->state_h1;
+}
+
+static int destroy_for_real(dhsa_sketch *s);
+
+// back to the state dhsa_create leaves a sketch in (its stream is drained)
+static int scrub_for_parking(dhsa_sketch *s)
+{
+    std::lock_guard<std::mutex> lk(s->mu);
+    if (s->hslots_ready) {  // batches nobody read are dropped with the window they belonged to
+        std::lock_guard<std::mutex> hl(s->hmu);
+        for (int i = 0; i < kHostSlots; i++) {
+            if (s->hslots[i].submitting || (s->hslots[i].state != 0 && s->hslots[i].copied != s->hslots[i].reserved))
+                return -1;  // a writer is still inside: not a sketch to recycle
+            s->hslots[i].state = 0, s->hslots[i].reserved = s->hslots[i].copied = 0;
+        }
+    }
+    s->stream = s->own_stream;
+    s->scan_mode = DHSA_SCAN_AUTO;
+    s->fc_sets = 1u << 20;
+    s->launches = 0;
+    s->restore_pending = false;
+    s->zc_given = false;
+    s->regime_few_keys = false;
+    CU(cudaMemsetAsync(s->bits, 0, s->alloc_bytes + kCounterBytes, s->stream));
+    if (int rc = clear_flow_cache_locked(s, false)) return rc;
+    CU(cudaStreamSynchronize(s->stream));
+    return DHSA_OK;
+}
+
+extern "C" int dhsa_release_cached(void)
+{
+    std::vector<dhsa_sketch *> victims;
+    {
+        std::lock_guard<std::mutex> lk(g_parked_mu);
+        victims.swap(g_parked);
+    }
+    for (dhsa_sketch *s : victims) destroy_for_real(s);
+    for (int d = 0; d < 64; d++) {
+        DeviceCache &dc = g_cache[d];
+        std::lock_guard<std::mutex> lk(dc.mu);
+        if (dc.rings.empty() && dc.stagings.empty() && dc.tables.empty()) continue;
+        cudaSetDevice(d);
+        for (auto &r : dc.rings)
+            for (int i = 0; i < kHostSlots; i++) cudaFreeHost(r.cand[i]), cudaFreeHost(r.opp[i]), cudaEventDestroy(r.dma_done[i]);
+        for (auto &r : dc.stagings)
+            for (int b = 0; b < kStageBufs; b++)
+                cudaFree(r.cand[b]), cudaFree(r.opp[b]), cudaEventDestroy(r.copied[b]), cudaEventDestroy(r.scanned[b]);
+        for (auto &r : dc.tables) cudaFree(r.table);
+        dc.rings.clear(), dc.stagings.clear(), dc.tables.clear();
+    }
+    (void)cudaGetLastError();
+    return DHSA_OK;
+}
+
+extern "C" int dhsa_create(const dhsa_params_t *params, int device, dhsa_sketch_t **out)
+{
+    NEED(params);
+    NEED(out);
+    *out = nullptr;
+    int rc = validate(params);
+    if (rc) return rc;
+    int ndev = 0;
+    CU(cudaGetDeviceCount(&ndev));
+    if (device < 0 || device >= ndev) return fail(DHSA_ECONFIG, "device %d out of range (%d visible)", device, ndev);
+    CU(cudaSetDevice(device));
+    {
+        std::lock_guard<std::mutex> lk(g_parked_mu);
+        for (size_t i = 0; i < g_parked.size(); i++)
+            if (same_key(g_parked[i], params, device)) {
+                *out = g_parked[i];
+                g_parked.erase(g_parked.begin() + i);
+                return DHSA_OK;
+            }
+    }
+    dhsa_sketch *s = new (std::nothrow) dhsa_sketch();  // value-initialised: every pointer null, every flag false
+    if (!s) return fail(-1, "out of host memory");
+    rc = create_locked(s, params, device);
+    if (rc != DHSA_OK) {  // whatever was allocated before the failing call goes back (the message is kept)
+        s->device = device;
+        destroy_for_real(s);
+        return rc;
+    }
     *out = s;
     return DHSA_OK;
 }
@@ -283,23 +428,80 @@ extern "C" int dhsa_destroy(dhsa_sketch_t *s)
 {
     if (!s) return DHSA_OK;
     cudaSetDevice(s->device);
-    cudaStreamSynchronize(s->stream);
-    cudaStreamSynchronize(s->copy_stream);
-    free_workspaces(s);
-    if (s->staging_ready) {
-        for (int b = 0; b < kStageBufs; b++) {
-            cudaFree(s->stage_cand[b]);
-            cudaFree(s->stage_opp[b]);
-            cudaEventDestroy(s->ev_copied[b]);
-            cudaEventDestroy(s->ev_scanned[b]);
+    if (s->stream) cudaStreamSynchronize(s->stream);
+    if (s->copy_stream) cudaStreamSynchronize(s->copy_stream);
+    if (getenv("DHSA_NO_SKETCH_CACHE") == nullptr && s->bits && s->own_stream) {
+        size_t same = 0;
+        {
+            std::lock_guard<std::mutex> lk(g_parked_mu);
+            for (dhsa_sketch *q : g_parked) same += same_key(q, &s->params, s->device);
         }
+        if (same < kParkedPerKey && scrub_for_parking(s) == DHSA_OK) {
+            dhsa_sketch *evicted = nullptr;
+            {
+                std::lock_guard<std::mutex> lk(g_parked_mu);
+                if (g_parked.size() >= kParkedTotal) {  // the oldest makes room
+                    evicted = g_parked.front();
+                    g_parked.erase(g_parked.begin());
+                }
+                g_parked.push_back(s);
+            }
+            if (evicted) destroy_for_real(evicted);
+            return DHSA_OK;
+        }
+        (void)cudaGetLastError();
     }
-    if (s->hslots_ready)
-        for (int i = 0; i < kHostSlots; i++) {
-            cudaFreeHost(s->hslots[i].cand);
-            cudaFreeHost(s->hslots[i].opp);
-            cudaEventDestroy(s->hslots[i].dma_done);
+    return destroy_for_real(s);
+}
+
+static int destroy_for_real(dhsa_sketch *s)
+{
+    cudaSetDevice(s->device);
+    if (s->stream) cudaStreamSynchronize(s->stream);
+    if (s->copy_stream) cudaStreamSynchronize(s->copy_stream);
+    free_workspaces(s);
+    DeviceCache *dc = cache_of(s->device);
+    if (s->staging_ready) {
+        StagingRes r;
+        for (int b = 0; b < kStageBufs; b++)
+            r.cand[b] = s->stage_cand[b], r.opp[b] = s->stage_opp[b], r.copied[b] = s->ev_copied[b], r.scanned[b] = s->ev_scanned[b];
+        bool kept = false;
+        if (dc) {
+            std::lock_guard<std::mutex> lk(dc->mu);
+            if (dc->stagings.size() < kCachedSets) dc->stagings.push_back(r), kept = true;
         }
+        if (!kept)
+            for (int b = 0; b < kStageBufs; b++) {
+                cudaFree(r.cand[b]);
+                cudaFree(r.opp[b]);
+                cudaEventDestroy(r.copied[b]);
+                cudaEventDestroy(r.scanned[b]);
+            }
+    }
+    if (s->hslots_ready) {
+        HostRingRes r;
+        for (int i = 0; i < kHostSlots; i++)
+            r.cand[i] = s->hslots[i].cand, r.opp[i] = s->hslots[i].opp, r.dma_done[i] = s->hslots[i].dma_done;
+        bool kept = false;
+        if (dc) {
+            std::lock_guard<std::mutex> lk(dc->mu);
+            if (dc->rings.size() < kCachedSets) dc->rings.push_back(r), kept = true;
+        }
+        if (!kept)
+            for (int i = 0; i < kHostSlots; i++) {
+                cudaFreeHost(r.cand[i]);
+                cudaFreeHost(r.opp[i]);
+                cudaEventDestroy(r.dma_done[i]);
+            }
+    }
+    if (s->fcache) {
+        bool kept = false;
+        if (dc) {
+            std::lock_guard<std::mutex> lk(dc->mu);
+            if (dc->tables.size() < kCachedSets) dc->tables.push_back(FlowCacheRes{s->fcache, s->dp.fc_sets}), kept = true;
+        }
+        if (kept) s->fcache = nullptr;
+    }
     cudaFree(s->bits);
     cudaFree(s->plan_block_max);
     cudaFree(s->plan_carry);
@@ -313,21 +515,29 @@ extern "C" int dhsa_destroy(dhsa_sketch_t *s)
         cudaEventDestroy(s->fc_stats_ev);
     }
     cudaFree(s->ctl);
-    cudaFreeHost(s->ctl_host);
-    cudaFreeHost(s->reports_pinned);
-    cudaEventDestroy(s->restore_ev);
-    cudaFreeHost(s->tally_pinned);
+    if (s->ctl_host) cudaFreeHost(s->ctl_host);
+    if (s->reports_pinned) cudaFreeHost(s->reports_pinned);
+    if (s->host_tmp) cudaFreeHost(s->host_tmp);
+    if (s->restore_ev) cudaEventDestroy(s->restore_ev);
+    if (s->bridge_ev) cudaEventDestroy(s->bridge_ev);
+    if (s->tally_pinned) cudaFreeHost(s->tally_pinned);
     if (s->restore_graph) cudaGraphExecDestroy(s->restore_graph);
-    cudaStreamDestroy(s->own_stream);
-    cudaStreamDestroy(s->copy_stream);
+    if (s->own_stream) cudaStreamDestroy(s->own_stream);
+    if (s->copy_stream) cudaStreamDestroy(s->copy_stream);
+    (void)cudaGetLastError();
     delete s;
     return DHSA_OK;
 }
 
 // The flow cache asserts "this key's bits are in the sketch": it must be emptied
 // whenever bits can disappear (reset, upload).  Stream-ordered with the scans.
-static int clear_flow_cache_locked(dhsa_sketch *s, bool clear_stats = true)
+static int clear_flow_cache_locked(dhsa_sketch *s, bool clear_stats)
 {
+    // a hit-rate snapshot still in flight belongs to the window that ends here: the auto policy must not
+    // judge the next window by it (the copy may still land in fc_stats_host; nothing reads it unasked)
+    consume_policy_snapshots(s, true);
+    s->fc_stats_pending = false;
+    s->auto_fell_back = false;  // a new window may repeat flows again
     if (!s->fcache || !s->fc_dirty) return DHSA_OK;
     // entries carry the epoch they were written in: bumping it empties the table without touching it
     const uint32_t epoch_max = (uint32_t)((1ull << (32 - s->dp.fc_tag_bits)) - 1);
@@ -337,9 +547,8 @@ static int clear_flow_cache_locked(dhsa_sketch *s, bool clear_stats = true)
     } else {
         s->dp.fc_epoch++;
     }
-    if (clear_stats) CU(cudaMemsetAsync(s->fc_stats, 0, 2 * sizeof(unsigned long long), s->stream));
+    if (clear_stats) CU(cudaMemsetAsync(s->fc_stats, 0, 4 * sizeof(unsigned long long), s->stream));
     s->fc_dirty = false;
-    s->auto_fell_back = false;  // a new window may repeat flows again
     return DHSA_OK;
 }
 
@@ -363,12 +572,16 @@ static int ensure_flow_cache_locked(dhsa_sketch *s)
     CU(cudaStreamSynchronize(s->stream));
     cudaFree(s->fcache);
     s->fcache = nullptr;
-    if (!s->fc_stats_host) {
-        CU(cudaMallocHost(&s->fc_stats_host, 2 * sizeof(unsigned long long)));
-        CU(cudaEventCreateWithFlags(&s->fc_stats_ev, cudaEventDisableTiming));
-        s->fc_stats_host[0] = s->fc_stats_host[1] = 0;
+    if (DeviceCache *dc = cache_of(s->device)) {  // a table a destroyed sketch left behind (cleared below: epoch restart)
+        std::lock_guard<std::mutex> lk(dc->mu);
+        for (size_t i = 0; i < dc->tables.size(); i++)
+            if (dc->tables[i].sets == sets) {
+                s->fcache = dc->tables[i].table;
+                dc->tables.erase(dc->tables.begin() + i);
+                break;
+            }
     }
-    CU(cudaMalloc(&s->fcache, (size_t)32 * sets));
+    if (!s->fcache) CU(cudaMalloc(&s->fcache, (size_t)32 * sets));
     s->dp.fc_sets = sets;
     s->dp.fc_shift = 32 - flow_cache_log2_sets(s);
     s->dp.fc_tag_bits = s->dp.fc_shift + s->dp.log2g;  // <= 31: the table has at least 2g sets
@@ -376,7 +589,7 @@ static int ensure_flow_cache_locked(dhsa_sketch *s)
     s->dp.fcache = s->fcache;
     s->dp.fc_stats = s->fc_stats;
     s->fc_dirty = true;
-    return clear_flow_cache_locked(s);
+    return clear_flow_cache_locked(s, true);
 }
 
 extern "C" int dhsa_set_flow_cache(dhsa_sketch_t *s, uint64_t n_sets)
@@ -398,6 +611,7 @@ extern "C" int dhsa_flow_cache_stats(dhsa_sketch_t *s, uint64_t *lookups, uint64
     *lookups = *hits = 0;
     std::lock_guard<std::mutex> lk(s->mu);
     if (int rc = use_device(s)) return rc;
+    if (int rc = flush_host_locked(s)) return rc;
     unsigned long long v[2];
     CU(cudaMemcpyAsync(v, s->fc_stats, sizeof v, cudaMemcpyDeviceToHost, s->stream));
     CU(cudaStreamSynchronize(s->stream));
@@ -410,6 +624,8 @@ extern "C" int dhsa_reset(dhsa_sketch_t *s)
     NEED(s);
     std::lock_guard<std::mutex> lk(s->mu);
     if (int rc = use_device(s)) return rc;
+    if (int rc = flush_host_locked(s)) return rc;  // batches handed over before the reset belong to the old window
+    s->mutation_seq++;
     CU(cudaMemsetAsync(s->bits, 0, s->alloc_bytes + kCounterBytes, s->stream));  // bits and every counter
     return clear_flow_cache_locked(s, false);
 }
@@ -475,6 +691,14 @@ extern "C" int dhsa_set_scan_mode(dhsa_sketch_t *s, int mode)
     return DHSA_OK;
 }
 
+extern "C" int dhsa_scan_mode_used(const dhsa_sketch_t *s, int *mode)
+{
+    NEED(s);
+    NEED(mode);
+    *mode = s->last_mode_used;
+    return DHSA_OK;
+}
+
 extern "C" int dhsa_launch_count(const dhsa_sketch_t *s, uint64_t *n)
 {
     NEED(s);
@@ -485,17 +709,30 @@ extern "C" int dhsa_launch_count(const dhsa_sketch_t *s, uint64_t *n)
 
 // -------------------------------------------------------------------- scan --
 
+template <typename SRC> struct SrcKind;
+template <> struct SrcKind<SoaSource> { static const int value = 0; };
+template <> struct SrcKind<RecordSource> { static const int value = 1; };
+
+// resident CTAs per SM of `kernel`, asked once per sketch and (mode, packet source)
+template <typename K>
+static int resident_ctas(dhsa_sketch *s, int mode, int kind, K kernel, int smem, int fallback)
+{
+    int &occ = s->occ[mode][kind];
+    if (!occ && (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kernel, 256, smem) != cudaSuccess || occ < 1))
+        occ = fallback;
+    return occ;
+}
+
 template <int R, typename SRC>
 static void launch_scan_src(dhsa_sketch *s, int mode, const SRC &src)
 {
     uint32_t *w = reinterpret_cast<uint32_t *>(s->bits);
     const uint64_t nvec = src.vectors();
+    const int kind = SrcKind<SRC>::value;
     // persistent grid: SMs x resident CTAs of the chosen kernel
 #define LAUNCH(KERNEL, FALLBACK_OCC)                                                                       \
     do {                                                                                                   \
-        static int occ = 0;                                                                                \
-        if (!occ && (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, KERNEL, 256, 0) != cudaSuccess || occ < 1)) \
-            occ = FALLBACK_OCC;                                                                            \
+        const int occ = resident_ctas(s, mode, kind, KERNEL, 0, FALLBACK_OCC);                             \
         KERNEL<<<grid_for(s, nvec, 256, occ), 256, 0, s->stream>>>(src, w, s->dp);                         \
     } while (0)
     switch (mode) {
@@ -507,17 +744,14 @@ static void launch_scan_src(dhsa_sketch *s, int mode, const SRC &src)
     // packet stream by TMA was 2-3% faster than register prefetch and is the only form kept
     default: {
         // flow cache: dynamic shared memory (TMA stage rings + miss queues), 3 CTAs per SM.
-        // The opt-in to more than 48 KB is per device, the occupancy is the same on every B200.
-        static int occ = 0;
-        static bool opted_in[64] = {false};
+        // The opt-in to more than 48 KB is per device, hence per sketch.
         auto kernel = k_scan_flowcache<R, SRC>;
         const int smem = FcSmem<SRC>::kBytes;
-        if (s->device < 64 && !opted_in[s->device]) {
+        if (!s->fc_opted_in[kind]) {
             cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-            opted_in[s->device] = true;
+            s->fc_opted_in[kind] = true;
         }
-        if (!occ && (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kernel, 256, smem) != cudaSuccess || occ < 1))
-            occ = 3;
+        const int occ = resident_ctas(s, DHSA_SCAN_FLOW_CACHE, kind, kernel, smem, 3);
         kernel<<<grid_for(s, nvec, 256, occ), 256, smem, s->stream>>>(src, w, s->dp);
         break;
     }
@@ -537,21 +771,42 @@ static void launch_scan_any_r(dhsa_sketch *s, int mode, const SRC &src)
     }
 }
 
-// Which fast kernel this launch uses (lock held).  Auto: scan behind the flow cache, watch its
-// hit rate through an asynchronous snapshot (never a sync), and fall back to the 5-access kernel
-// for the rest of the window when flows do not repeat.  Break-even is a hit rate of about 1/3:
-// 1 + 11 (1 - h) requests per packet with the cache against 5 + 5 (1 - h) without.
+// ---- the auto policy ------------------------------------------------------------------------
+// Decided per launch from counters the scan kernels leave behind the bit array, read through
+// asynchronous pinned snapshots (never a synchronisation):
+//   * flows that do not repeat (cache hit rate under 0.3 after >= 4M lookups): the rest of the
+//     WINDOW goes to the 5-access kernel.  Break-even is a hit rate of about 1/3: 1 + 11 (1 - h)
+//     requests per packet with the cache against 5 + 5 (1 - h) without.
+//   * a handful of candidate hosts (a DDoS window with the victims as candidates -- BASELINE
+//     config 4 -- where every packet lands in the same few cells): those cells' words sit in L1, so
+//     the plain test-first kernel needs no L2 access at all while a cache lookup is still one L2
+//     request per packet.  The signal is exact and free: every read-out counts the non-empty cells
+//     of array 0 (k_hot_sets), i.e. the distinct dh0 values seen.  At most kFewCells of them after a
+//     window of >= 4M packets switches the REGIME, which persists across resets (it is a property
+//     of the traffic, known one read-out late); more than that, or -- inside a window -- a test
+//     kernel that still issues a RED for more than 1 packet in 64, switches it back.
+static const unsigned long long kFewCells = 128;   // 5 x 128 cells x 128 B = 80 KB of sketch words
+
+static void consume_policy_snapshots(dhsa_sketch *s, bool window_ends)
+{
+    if (s->fc_stats_pending && cudaEventQuery(s->fc_stats_ev) == cudaSuccess) {
+        s->fc_stats_pending = false;
+        const unsigned long long lookups = s->fc_stats_host[0], hits = s->fc_stats_host[1];
+        const unsigned long long packets = s->fc_stats_host[2], reds = s->fc_stats_host[3];
+        if (lookups >= kPolicyMinSample && !window_ends && hits * 10 < lookups * 3) s->auto_fell_back = true;
+        if (packets >= kPolicyMinSample && reds * 64 > packets) s->regime_few_keys = false;
+    }
+    (void)cudaGetLastError();
+}
+
+// Which fast kernel this launch uses (lock held).
 static int pick_scan_mode_locked(dhsa_sketch *s)
 {
     int mode = s->scan_mode;
     if (mode == DHSA_SCAN_AUTO) {
-        if (s->fc_stats_pending && cudaEventQuery(s->fc_stats_ev) == cudaSuccess) {
-            s->fc_stats_pending = false;
-            const unsigned long long lookups = s->fc_stats_host[0], hits = s->fc_stats_host[1];
-            if (lookups >= (1ull << 22) && hits * 10 < lookups * 3) s->auto_fell_back = true;
-        }
-        (void)cudaGetLastError();
-        mode = s->auto_fell_back ? DHSA_SCAN_TEST_AGG_RED : DHSA_SCAN_FLOW_CACHE;
+        consume_policy_snapshots(s, false);
+        mode = s->regime_few_keys ? DHSA_SCAN_TEST_RED
+                                  : (s->auto_fell_back ? DHSA_SCAN_TEST_AGG_RED : DHSA_SCAN_FLOW_CACHE);
     }
     if (mode == DHSA_SCAN_FLOW_CACHE && !flow_cache_supported(s)) mode = DHSA_SCAN_TEST_AGG_RED;
     return mode;
@@ -559,17 +814,26 @@ static int pick_scan_mode_locked(dhsa_sketch *s)
 
 static int before_fast_scan_locked(dhsa_sketch *s, int mode)
 {
+    s->last_mode_used = mode;
     if (mode == DHSA_SCAN_FLOW_CACHE) {
         if (int rc = ensure_flow_cache_locked(s)) return rc;
         s->fc_dirty = true;
     }
+    // the test-first kernel counts packets and REDs only while the policy listens
+    s->dp.test_stats = (s->scan_mode == DHSA_SCAN_AUTO && mode == DHSA_SCAN_TEST_RED) ? s->fc_stats + 2 : nullptr;
     return DHSA_OK;
 }
 
 static int after_fast_scan_locked(dhsa_sketch *s, int mode)
 {
-    if (s->scan_mode == DHSA_SCAN_AUTO && mode == DHSA_SCAN_FLOW_CACHE && !s->fc_stats_pending) {
-        CU(cudaMemcpyAsync(s->fc_stats_host, s->fc_stats, 2 * sizeof(unsigned long long), cudaMemcpyDeviceToHost,
+    if (s->scan_mode == DHSA_SCAN_AUTO && (mode == DHSA_SCAN_FLOW_CACHE || mode == DHSA_SCAN_TEST_RED) &&
+        !s->fc_stats_pending) {
+        if (!s->fc_stats_host) {
+            CU(cudaMallocHost(&s->fc_stats_host, 4 * sizeof(unsigned long long)));
+            CU(cudaEventCreateWithFlags(&s->fc_stats_ev, cudaEventDisableTiming));
+            memset(s->fc_stats_host, 0, 4 * sizeof(unsigned long long));
+        }
+        CU(cudaMemcpyAsync(s->fc_stats_host, s->fc_stats, 4 * sizeof(unsigned long long), cudaMemcpyDeviceToHost,
                            s->stream));
         CU(cudaEventRecord(s->fc_stats_ev, s->stream));
         s->fc_stats_pending = true;
@@ -674,6 +938,7 @@ extern "C" int dhsa_update_records_device(dhsa_sketch_t *s, const void *records_
     if ((uintptr_t)records_dev & 3u) return fail(DHSA_ECONFIG, "record buffer must be 4-byte aligned");
     std::lock_guard<std::mutex> lk(s->mu);
     if (int rc = use_device(s)) return rc;
+    s->mutation_seq++;
     const uint8_t *rec = static_cast<const uint8_t *>(records_dev);
     // "both" feeds each record in both orientations (engine.py:191-192): two passes over the segment.
     // Late records are tallied once, by the first pass.
@@ -712,53 +977,84 @@ extern "C" int dhsa_record_tally_at_restore(dhsa_sketch_t *s, uint64_t *records_
 
 // ---- parallel memcpy for pageable host input ---------------------------------------------
 // A pageable cudaMemcpyAsync is a single-threaded copy into the driver's bounce buffer
-// (measured 1.4 Gpps = 11 GB/s); PCIe takes 55 GB/s.  So pageable arrays are copied into pinned
-// slots by several host threads -- a small process-wide pool plus the caller -- and DMA'd from there.
+// (measured 1.4 Gpps = 11 GB/s); PCIe takes 55 GB/s.  So host arrays are copied into pinned
+// slots by several host threads -- a small process-wide pool plus the caller -- and DMA'd from
+// there.  The reference engine hands over 65,536-pair batches (512 KB), so a job lasts tens of
+// microseconds: helpers poll for about 100 us after their last job before they go to sleep, and
+// a caller that finds the pool busy with another caller's job simply copies alone.
 class CopyPool {
 public:
+    struct Piece {
+        void *dst;
+        const void *src;
+        size_t bytes;
+    };
     static CopyPool &get()
     {
         static CopyPool *pool = new CopyPool();  // leaked on purpose: no destructor races at exit
         return *pool;
     }
-    // dst <- src, split over the pool and the calling thread; returns when every byte is copied
-    void copy(void *dst, const void *src, size_t bytes)
+    // dst <- src for both arrays, split into pieces over the pool and the calling thread;
+    // returns when every byte is copied
+    void copy2(void *d0, const void *s0, void *d1, const void *s1, size_t bytes_each)
     {
-        const size_t piece_min = 1u << 19;
-        size_t pieces = bytes / piece_min;
-        if (pieces > workers_.size() + 1) pieces = workers_.size() + 1;
-        if (pieces <= 1) {
-            memcpy(dst, src, bytes);
+        const size_t kPiece = 32u << 10;  // 16 pieces for a 65,536-pair batch: late helpers still find work
+        const size_t per_array = (bytes_each + kPiece - 1) / kPiece;
+        if (n_helpers_ == 0 || per_array * 2 < 4 || !job_mu_.try_lock()) {
+            memcpy(d0, s0, bytes_each);
+            memcpy(d1, s1, bytes_each);
             return;
         }
-        const size_t per = ((bytes / pieces) + 63) & ~(size_t)63;
-        Job job;
-        job.pending = (int)pieces - 1;
-        {
-            std::lock_guard<std::mutex> lk(mu_);
-            for (size_t i = 1; i < pieces; i++) {
-                const size_t lo = i * per, hi = (i + 1 == pieces) ? bytes : (i + 1) * per;
-                tasks_.push_back(Task{(char *)dst + lo, (const char *)src + lo, hi - lo, &job});
-            }
+        // at most kMaxPieces pieces: larger pieces for larger jobs
+        size_t piece = kPiece;
+        while ((bytes_each + piece - 1) / piece * 2 > kMaxPieces) piece <<= 1;
+        uint32_t n = 0;
+        for (int a = 0; a < 2; a++) {
+            char *d = (char *)(a ? d1 : d0);
+            const char *src = (const char *)(a ? s1 : s0);
+            for (size_t lo = 0; lo < bytes_each; lo += piece)
+                pieces_[n++] = Piece{d + lo, src + lo, bytes_each - lo < piece ? bytes_each - lo : piece};
         }
-        cv_.notify_all();
-        memcpy(dst, src, per);
-        std::unique_lock<std::mutex> lk(job.mu);
-        job.cv.wait(lk, [&] { return job.pending == 0; });
+        n_pieces_.store(n, std::memory_order_relaxed);
+        done_.store(0, std::memory_order_relaxed);
+        const uint64_t gen = (ticket_.load(std::memory_order_relaxed) >> 32) + 1;
+        ticket_.store(gen << 32, std::memory_order_release);  // publishes pieces_ / n_pieces_
+        if (sleepers_.load(std::memory_order_acquire) > 0) {
+            { std::lock_guard<std::mutex> lk(cv_mu_); }
+            cv_.notify_all();
+        }
+        work(gen);
+        while (done_.load(std::memory_order_acquire) != n) cpu_relax();
+        // close the job: a helper that still holds an old ticket value can no longer claim a piece
+        // index once pieces_ is rewritten for the next job (its compare-exchange fails)
+        ticket_.store((gen << 32) | 0xFFFFFFFFull, std::memory_order_release);
+        job_mu_.unlock();
     }
 
 private:
-    struct Job {
-        std::mutex mu;
-        std::condition_variable cv;
-        int pending;
-    };
-    struct Task {
-        char *dst;
-        const char *src;
-        size_t bytes;
-        Job *job;
-    };
+    static const uint32_t kMaxPieces = 256;
+    static void cpu_relax()
+    {
+#if defined(__x86_64__) || defined(__i386__)
+        __builtin_ia32_pause();
+#else
+        std::this_thread::yield();
+#endif
+    }
+    // take pieces of job `gen` until none is left (or the job is over)
+    void work(uint64_t gen)
+    {
+        for (;;) {
+            uint64_t t = ticket_.load(std::memory_order_acquire);
+            if ((t >> 32) != gen) return;
+            const uint32_t idx = (uint32_t)t;
+            if (idx >= n_pieces_.load(std::memory_order_relaxed)) return;
+            if (!ticket_.compare_exchange_weak(t, t + 1, std::memory_order_acq_rel)) continue;
+            const Piece pc = pieces_[idx];
+            memcpy(pc.dst, pc.src, pc.bytes);
+            done_.fetch_add(1, std::memory_order_acq_rel);
+        }
+    }
     CopyPool()
     {
         // helper threads: DHSA_COPY_THREADS, else up to 6 while leaving two cores to the application
@@ -768,30 +1064,43 @@ private:
             const long v = strtol(env, nullptr, 10);
             if (v >= 0 && v <= 64) n = (unsigned)v;
         }
+        n_helpers_ = n;
         for (unsigned i = 0; i < n; i++) {
-            workers_.emplace_back([this] { run(); });
-            workers_.back().detach();
+            std::thread th([this] { run(); });
+            th.detach();
         }
     }
     void run()
     {
+        uint64_t seen = 0;
+        auto last = std::chrono::steady_clock::now();
         for (;;) {
-            Task t;
-            {
-                std::unique_lock<std::mutex> lk(mu_);
-                cv_.wait(lk, [&] { return !tasks_.empty(); });
-                t = tasks_.front();
-                tasks_.pop_front();
+            const uint64_t gen = ticket_.load(std::memory_order_acquire) >> 32;
+            if (gen != seen) {
+                seen = gen;
+                work(gen);
+                last = std::chrono::steady_clock::now();
+                continue;
             }
-            memcpy(t.dst, t.src, t.bytes);
-            std::lock_guard<std::mutex> lk(t.job->mu);
-            if (--t.job->pending == 0) t.job->cv.notify_one();
+            if (std::chrono::steady_clock::now() - last < std::chrono::microseconds(100)) {
+                cpu_relax();
+                continue;
+            }
+            std::unique_lock<std::mutex> lk(cv_mu_);
+            sleepers_.fetch_add(1, std::memory_order_acq_rel);
+            cv_.wait(lk, [&] { return (ticket_.load(std::memory_order_acquire) >> 32) != seen; });
+            sleepers_.fetch_sub(1, std::memory_order_acq_rel);
         }
     }
-    std::mutex mu_;
+    std::mutex job_mu_;  // one job at a time
+    Piece pieces_[kMaxPieces];
+    std::atomic<uint32_t> n_pieces_{0};
+    std::atomic<uint64_t> ticket_{0};  // job generation << 32 | next piece
+    std::atomic<uint32_t> done_{0};
+    std::atomic<int> sleepers_{0};
+    std::mutex cv_mu_;
     std::condition_variable cv_;
-    std::deque<Task> tasks_;
-    std::vector<std::thread> workers_;
+    unsigned n_helpers_ = 0;
 };
 
 static bool is_pageable(const void *p)
@@ -844,7 +1153,12 @@ extern "C" int dhsa_copy_to_device_async(int device, void *dst_dev, const void *
         const uint64_t cnt = nbytes - off < kBounceBytes ? nbytes - off : kBounceBytes;
         const int i = (int)(r.next++ % kBounceSlots);
         if (r.used[i]) CU(cudaEventSynchronize(r.done[i]));
-        CopyPool::get().copy(r.buf[i], (const uint8_t *)src_host + off, cnt);
+        {   // two halves so the pool's two-array entry point serves a single buffer too
+            const uint64_t half = (cnt / 2) & ~63ull;
+            if (half) CopyPool::get().copy2(r.buf[i], (const uint8_t *)src_host + off, r.buf[i] + half,
+                                            (const uint8_t *)src_host + off + half, half);
+            if (cnt > 2 * half) memcpy(r.buf[i] + 2 * half, (const uint8_t *)src_host + off + 2 * half, cnt - 2 * half);
+        }
         CU(cudaMemcpyAsync((uint8_t *)dst_dev + off, r.buf[i], cnt, cudaMemcpyHostToDevice, stream));
         CU(cudaEventRecord(r.done[i], stream));
         r.used[i] = true;
@@ -937,12 +1251,49 @@ extern "C" int dhsa_update_device(dhsa_sketch_t *s, const uint32_t *cand_dev, co
     NEED(opp_dev);
     std::lock_guard<std::mutex> lk(s->mu);
     if (int rc = use_device(s)) return rc;
+    s->mutation_seq++;
     return scan_locked(s, cand_dev, opp_dev, n);
+}
+
+// The same scan for arrays produced on ANOTHER stream (torch's current stream, say): the launch
+// stream waits for what that stream has queued so far, and that stream waits for the scan before
+// it runs anything queued later -- so the producer may free or overwrite the arrays right after
+// the call, and the sketch keeps launching on its own stream.
+extern "C" int dhsa_update_device_from(dhsa_sketch_t *s, const uint32_t *cand_dev, const uint32_t *opp_dev, uint64_t n,
+                                       void *producer_stream)
+{
+    NEED(s);
+    if (n == 0) return DHSA_OK;
+    NEED(cand_dev);
+    NEED(opp_dev);
+    std::lock_guard<std::mutex> lk(s->mu);
+    if (int rc = use_device(s)) return rc;
+    s->mutation_seq++;
+    cudaStream_t ps = (cudaStream_t)producer_stream;
+    if (ps == s->stream) return scan_locked(s, cand_dev, opp_dev, n);
+    CU(cudaEventRecord(s->bridge_ev, ps));
+    CU(cudaStreamWaitEvent(s->stream, s->bridge_ev, 0));
+    if (int rc = scan_locked(s, cand_dev, opp_dev, n)) return rc;
+    CU(cudaEventRecord(s->bridge_ev, s->stream));
+    CU(cudaStreamWaitEvent(ps, s->bridge_ev, 0));
+    return DHSA_OK;
 }
 
 static int ensure_staging(dhsa_sketch *s)
 {
     if (s->staging_ready) return DHSA_OK;
+    if (DeviceCache *dc = cache_of(s->device)) {
+        std::lock_guard<std::mutex> lk(dc->mu);
+        if (!dc->stagings.empty()) {
+            const StagingRes r = dc->stagings.back();
+            dc->stagings.pop_back();
+            for (int b = 0; b < kStageBufs; b++)
+                s->stage_cand[b] = r.cand[b], s->stage_opp[b] = r.opp[b], s->ev_copied[b] = r.copied[b], s->ev_scanned[b] = r.scanned[b];
+            s->staging_ready = true;
+            s->stage_seq = 0;
+            return DHSA_OK;
+        }
+    }
     for (int b = 0; b < kStageBufs; b++) {
         CU(cudaMalloc(&s->stage_cand[b], kStagePackets * 4));
         CU(cudaMalloc(&s->stage_opp[b], kStagePackets * 4));
@@ -958,18 +1309,35 @@ static int ensure_host_slots(dhsa_sketch *s)
 {
     std::lock_guard<std::mutex> lk(s->hmu);
     if (s->hslots_ready) return DHSA_OK;
-    for (int i = 0; i < kHostSlots; i++) {
-        CU(cudaMallocHost(&s->hslots[i].cand, kHostSlotPackets * 4));
-        CU(cudaMallocHost(&s->hslots[i].opp, kHostSlotPackets * 4));
-        CU(cudaEventCreateWithFlags(&s->hslots[i].dma_done, cudaEventDisableTiming));
-        s->hslots[i].busy = s->hslots[i].used = false;
+    HostRingRes cached;
+    bool have = false;
+    if (DeviceCache *dc = cache_of(s->device)) {
+        std::lock_guard<std::mutex> cl(dc->mu);
+        if (!dc->rings.empty()) {
+            cached = dc->rings.back();
+            dc->rings.pop_back();
+            have = true;
+        }
     }
+    for (int i = 0; i < kHostSlots; i++) {
+        if (have) {
+            s->hslots[i].cand = cached.cand[i], s->hslots[i].opp = cached.opp[i], s->hslots[i].dma_done = cached.dma_done[i];
+        } else {
+            CU(cudaMallocHost(&s->hslots[i].cand, kHostSlotPackets * 4));
+            CU(cudaMallocHost(&s->hslots[i].opp, kHostSlotPackets * 4));
+            CU(cudaEventCreateWithFlags(&s->hslots[i].dma_done, cudaEventDisableTiming));
+        }
+        s->hslots[i].dma_pending = s->hslots[i].submitting = false;
+        s->hslots[i].state = 0;
+        s->hslots[i].reserved = s->hslots[i].copied = 0;
+    }
+    s->hcur = 0;
     s->hslots_ready = true;
     return DHSA_OK;
 }
 
-// One staged chunk: H2D from `cand`/`opp` (pinned, or pageable through the driver) into the device
-// ring on the copy stream, then its scan on the launch stream.  Lock held.
+// One staged chunk: H2D from `cand`/`opp` (pinned) into the device ring on the copy stream, then
+// its scan on the launch stream.  Lock held.
 static int stage_and_scan_locked(dhsa_sketch *s, const uint32_t *cand, const uint32_t *opp, uint64_t cnt,
                                  cudaEvent_t also_record, int *buf_out)
 {
@@ -987,56 +1355,123 @@ static int stage_and_scan_locked(dhsa_sketch *s, const uint32_t *cand, const uin
     return DHSA_OK;
 }
 
-// Pageable arrays: every chunk is copied into a pinned slot by this thread (and the copy pool)
-// with no sketch lock held -- callers on several threads, as the reference's pool submits them
-// (pkg/src/dhsa/engine.py:81-86), fill different slots at once -- then queued under the lock.
-// The caller's arrays are no longer needed once the last chunk sits in its slot.
-static int update_host_pageable(dhsa_sketch *s, const uint32_t *cand_host, const uint32_t *opp_host, uint64_t n)
+// Queue one closed, completely filled slot: H2D + scan.  mu held, h.submitting set by the caller.
+static int submit_slot_locked(dhsa_sketch *s, HostSlot &h)
+{
+    int rc = ensure_staging(s);
+    if (rc == DHSA_OK) rc = stage_and_scan_locked(s, h.cand, h.opp, h.reserved, h.dma_done, nullptr);
+    {
+        std::lock_guard<std::mutex> lk(s->hmu);
+        h.state = 0;
+        h.dma_pending = rc == DHSA_OK;
+        h.submitting = false;
+        h.reserved = h.copied = 0;
+    }
+    s->hcv.notify_all();
+    return rc;
+}
+
+// Everything host callers have handed over so far is queued on the launch stream when this
+// returns (mu held).  Closes the partly filled slot, waits for writers still copying into closed
+// slots -- they need no sketch lock for that -- and queues every slot that is ready.
+static int flush_host_locked(dhsa_sketch *s)
+{
+    if (!s->hslots_ready) return DHSA_OK;
+    std::unique_lock<std::mutex> lk(s->hmu);
+    HostSlot &cur = s->hslots[s->hcur];
+    if (cur.state == 1) {
+        if (cur.reserved > 0) {
+            cur.state = 2;
+            s->hcur = (s->hcur + 1) % kHostSlots;
+        } else {
+            cur.state = 0;
+        }
+    }
+    int rc = DHSA_OK;
+    for (;;) {
+        bool waiting = false;
+        for (int i = 0; i < kHostSlots; i++) {
+            HostSlot &h = s->hslots[i];
+            if (h.state != 2) continue;
+            if (h.copied == h.reserved && !h.submitting) {
+                h.submitting = true;
+                lk.unlock();
+                const int r2 = submit_slot_locked(s, h);
+                if (rc == DHSA_OK) rc = r2;
+                lk.lock();
+            } else {
+                waiting = true;
+            }
+        }
+        if (!waiting) break;
+        s->hcv.wait(lk);
+    }
+    return rc;
+}
+
+// Host arrays through the accumulation slots.  The caller's arrays are no longer needed once
+// their last byte sits in a slot; the scan itself is queued when the slot fills up or at the
+// next barrier / read-out (flush_host_locked).  Called without the sketch lock, from any number
+// of threads (pkg/src/dhsa/engine.py:81-86 submits batches from a pool onto one sketch).
+static int update_host_ring(dhsa_sketch *s, const uint32_t *cand_host, const uint32_t *opp_host, uint64_t n)
 {
     if (int rc = ensure_host_slots(s)) return rc;
-    for (uint64_t off = 0; off < n; off += kHostSlotPackets) {
-        const uint64_t cnt = (n - off < kHostSlotPackets) ? (n - off) : kHostSlotPackets;
-        int slot = -1;
+    for (uint64_t off = 0; off < n;) {
+        HostSlot *hp = nullptr;
+        uint64_t at = 0, take = 0;
         {
             std::unique_lock<std::mutex> lk(s->hmu);
-            s->hcv.wait(lk, [&] {
-                for (int i = 0; i < kHostSlots; i++)
-                    if (!s->hslots[i].busy) return true;
-                return false;
-            });
-            // round robin: the slot whose last DMA is oldest, so filling it never waits for a copy in flight
-            for (int k = 0; k < kHostSlots && slot < 0; k++) {
-                const int i = (int)((s->hslot_next + k) % kHostSlots);
-                if (!s->hslots[i].busy) slot = i;
+            for (;;) {
+                HostSlot &h = s->hslots[s->hcur];
+                if (h.state == 0 && !h.submitting) {
+                    if (h.dma_pending) {  // the copy out of this slot (kHostSlots - 1 slots ago) must be over
+                        if (cudaEventSynchronize(h.dma_done) != cudaSuccess) return cuda_fail(cudaGetLastError(), "host slot wait");
+                        h.dma_pending = false;
+                    }
+                    h.state = 1;
+                    h.reserved = h.copied = 0;
+                }
+                if (h.state == 1) break;
+                s->hcv.wait(lk);  // the ring is full: wait for a slot to be queued
             }
-            s->hslot_next = (unsigned)slot + 1u;
-            s->hslots[slot].busy = true;
+            hp = &s->hslots[s->hcur];
+            at = hp->reserved;
+            take = n - off < kHostSlotPackets - at ? n - off : kHostSlotPackets - at;
+            hp->reserved += take;
+            if (hp->reserved == kHostSlotPackets) {
+                hp->state = 2;
+                s->hcur = (s->hcur + 1) % kHostSlots;
+            }
         }
-        HostSlot &h = s->hslots[slot];
-        int rc = DHSA_OK;
-        if (h.used && cudaEventSynchronize(h.dma_done) != cudaSuccess) rc = cuda_fail(cudaGetLastError(), "host slot wait");
-        if (rc == DHSA_OK) {
-            CopyPool::get().copy(h.cand, cand_host + off, cnt * 4);
-            CopyPool::get().copy(h.opp, opp_host + off, cnt * 4);
-            std::lock_guard<std::mutex> lk(s->mu);
-            rc = ensure_staging(s);
-            if (rc == DHSA_OK) rc = stage_and_scan_locked(s, h.cand, h.opp, cnt, h.dma_done, nullptr);
-            h.used = true;
-        }
+        CopyPool::get().copy2(hp->cand + at, cand_host + off, hp->opp + at, opp_host + off, take * 4);
+        bool ready;
         {
             std::lock_guard<std::mutex> lk(s->hmu);
-            h.busy = false;
+            hp->copied += take;
+            ready = hp->state == 2 && hp->copied == hp->reserved && !hp->submitting;
         }
-        s->hcv.notify_one();
-        if (rc != DHSA_OK) return rc;
+        s->hcv.notify_all();
+        off += take;
+        if (ready) {  // the writer that completes a closed slot queues it
+            std::lock_guard<std::mutex> lk(s->mu);
+            {
+                std::lock_guard<std::mutex> hl(s->hmu);
+                ready = hp->state == 2 && hp->copied == hp->reserved && !hp->submitting && hp->reserved > 0;
+                if (ready) hp->submitting = true;
+            }
+            if (ready) {
+                s->mutation_seq++;
+                if (int rc = submit_slot_locked(s, *hp)) return rc;
+            }
+        }
     }
     return DHSA_OK;
 }
 
-// Host packets -> HBM staging ring -> scan.  Copies run on their own stream and
-// overlap the scan of the previous chunk; pinned sources are DMA'd in place,
-// pageable ones through pinned slots filled by several host threads.  Returns once
-// the last byte of the caller's arrays has been read.
+// Host packets -> pinned slots / pinned caller memory -> HBM staging ring -> scan.  Copies run on
+// their own stream and overlap the scan of the previous chunk.  Large page-locked arrays are DMA'd
+// in place (the call returns once their last byte has been read); everything else -- ordinary
+// numpy arrays, small batches -- is appended to the accumulation slots.
 extern "C" int dhsa_update_host(dhsa_sketch_t *s, const uint32_t *cand_host, const uint32_t *opp_host, uint64_t n)
 {
     NEED(s);
@@ -1044,8 +1479,10 @@ extern "C" int dhsa_update_host(dhsa_sketch_t *s, const uint32_t *cand_host, con
     NEED(cand_host);
     NEED(opp_host);
     if (int rc = use_device(s)) return rc;
-    if (is_pageable(cand_host) || is_pageable(opp_host)) return update_host_pageable(s, cand_host, opp_host, n);
+    if (n < kHostSlotPackets || is_pageable(cand_host) || is_pageable(opp_host))
+        return update_host_ring(s, cand_host, opp_host, n);
     std::lock_guard<std::mutex> lk(s->mu);
+    s->mutation_seq++;
     if (int rc = ensure_staging(s)) return rc;
     int last = -1;
     for (uint64_t off = 0; off < n; off += kStagePackets) {
@@ -1061,6 +1498,7 @@ extern "C" int dhsa_seal(dhsa_sketch_t *s)
     NEED(s);
     std::lock_guard<std::mutex> lk(s->mu);
     if (int rc = use_device(s)) return rc;
+    if (int rc = flush_host_locked(s)) return rc;
     CU(cudaStreamSynchronize(s->stream));
     return DHSA_OK;
 }
@@ -1073,7 +1511,44 @@ extern "C" int dhsa_download_bits(dhsa_sketch_t *s, uint8_t *bits_host, uint64_t
                                          (unsigned long long)nbytes, (unsigned long long)s->nbytes);
     std::lock_guard<std::mutex> lk(s->mu);
     if (int rc = use_device(s)) return rc;
+    if (int rc = flush_host_locked(s)) return rc;
     CU(cudaMemcpyAsync(bits_host, s->bits, nbytes, cudaMemcpyDeviceToHost, s->stream));
+    CU(cudaStreamSynchronize(s->stream));
+    return DHSA_OK;
+}
+
+// A byte range of the bit array, for callers that stream a sketch to or from a file in pieces
+// (snapshots) instead of holding a second whole copy on the host.
+extern "C" int dhsa_download_range(dhsa_sketch_t *s, uint64_t byte_lo, uint64_t nbytes, uint8_t *dst_host)
+{
+    NEED(s);
+    if (nbytes == 0) return DHSA_OK;
+    NEED(dst_host);
+    if (byte_lo > s->nbytes || nbytes > s->nbytes - byte_lo)
+        return fail(DHSA_EDATA, "range [%llu, +%llu) outside the sketch's %llu bytes", (unsigned long long)byte_lo,
+                    (unsigned long long)nbytes, (unsigned long long)s->nbytes);
+    std::lock_guard<std::mutex> lk(s->mu);
+    if (int rc = use_device(s)) return rc;
+    if (int rc = flush_host_locked(s)) return rc;
+    CU(cudaMemcpyAsync(dst_host, s->bits + byte_lo, nbytes, cudaMemcpyDeviceToHost, s->stream));
+    CU(cudaStreamSynchronize(s->stream));
+    return DHSA_OK;
+}
+
+extern "C" int dhsa_upload_range(dhsa_sketch_t *s, uint64_t byte_lo, uint64_t nbytes, const uint8_t *src_host)
+{
+    NEED(s);
+    if (nbytes == 0) return DHSA_OK;
+    NEED(src_host);
+    if (byte_lo > s->nbytes || nbytes > s->nbytes - byte_lo)
+        return fail(DHSA_EDATA, "range [%llu, +%llu) outside the sketch's %llu bytes", (unsigned long long)byte_lo,
+                    (unsigned long long)nbytes, (unsigned long long)s->nbytes);
+    std::lock_guard<std::mutex> lk(s->mu);
+    if (int rc = use_device(s)) return rc;
+    if (int rc = flush_host_locked(s)) return rc;
+    s->mutation_seq++;
+    CU(cudaMemcpyAsync(s->bits + byte_lo, src_host, nbytes, cudaMemcpyHostToDevice, s->stream));
+    if (int rc = clear_flow_cache_locked(s, true)) return rc;  // bits may have disappeared
     CU(cudaStreamSynchronize(s->stream));
     return DHSA_OK;
 }
@@ -1090,6 +1565,7 @@ extern "C" int dhsa_download_cell(dhsa_sketch_t *s, int32_t array, uint64_t inde
                                           (unsigned long long)nbytes, (unsigned long long)cell_bytes);
     std::lock_guard<std::mutex> lk(s->mu);
     if (int rc = use_device(s)) return rc;
+    if (int rc = flush_host_locked(s)) return rc;
     const uint64_t off = (((uint64_t)array << s->params.k) + index) * cell_bytes;
     CU(cudaMemcpyAsync(cell_host, s->bits + off, cell_bytes, cudaMemcpyDeviceToHost, s->stream));
     CU(cudaStreamSynchronize(s->stream));
@@ -1104,8 +1580,10 @@ extern "C" int dhsa_upload_bits(dhsa_sketch_t *s, const uint8_t *bits_host, uint
                                          (unsigned long long)nbytes, (unsigned long long)s->nbytes);
     std::lock_guard<std::mutex> lk(s->mu);
     if (int rc = use_device(s)) return rc;
+    if (int rc = flush_host_locked(s)) return rc;
+    s->mutation_seq++;
     CU(cudaMemcpyAsync(s->bits, bits_host, nbytes, cudaMemcpyHostToDevice, s->stream));
-    if (int rc = clear_flow_cache_locked(s)) return rc;
+    if (int rc = clear_flow_cache_locked(s, true)) return rc;
     CU(cudaStreamSynchronize(s->stream));
     return DHSA_OK;
 }
@@ -1115,11 +1593,19 @@ extern "C" int dhsa_upload_bits(dhsa_sketch_t *s, const uint8_t *bits_host, uint
 static int ensure_readout(dhsa_sketch *s)
 {
     if (s->zc) return DHSA_OK;
-    const uint64_t m = 1ull << s->params.k;
     CU(cudaMalloc(&s->zc, s->dp.ncell * sizeof(int32_t)));
     CU(cudaMalloc(&s->lists, s->dp.ncell * sizeof(uint32_t)));
     CU(cudaMalloc(&s->bitmaps, (uint64_t)s->params.r * s->bitmap_words * sizeof(uint32_t)));
-    (void)m;
+    return DHSA_OK;
+}
+
+static int ensure_host_tmp(dhsa_sketch *s, uint64_t bytes)
+{
+    if (bytes <= s->host_tmp_bytes) return DHSA_OK;
+    if (s->host_tmp) cudaFreeHost(s->host_tmp);
+    s->host_tmp = nullptr, s->host_tmp_bytes = 0;
+    CU(cudaMallocHost(&s->host_tmp, bytes));
+    s->host_tmp_bytes = bytes;
     return DHSA_OK;
 }
 
@@ -1130,9 +1616,14 @@ static uint64_t pow2_at_least(uint64_t v)
     return l;
 }
 
-static int ensure_candidates(dhsa_sketch *s, uint64_t max_candidates)
+// Workspaces of the stage chain: 64 bytes per partial key.  max_candidates is only a bound in the
+// reference (pkg/src/dhsa/dhla.py:34,269-273), and callers pass huge values for "unlimited", so the
+// buffers start at the default bound and grow when a stage needs more (restore_collect).
+static const uint64_t kInitialCandidates = 1ull << 20;  // DEFAULT_MAX_CANDIDATES, dhla.py:34
+
+static int ensure_candidates(dhsa_sketch *s, uint64_t want)
 {
-    const uint64_t want = max_candidates < 1 ? 1 : max_candidates;
+    if (want < 1) want = 1;
     if (want <= s->cand_cap) return DHSA_OK;
     CU(cudaStreamSynchronize(s->stream));
     for (int b = 0; b < 2; b++) {
@@ -1141,9 +1632,10 @@ static int ensure_candidates(dhsa_sketch *s, uint64_t max_candidates)
         s->sub[b] = nullptr, s->cl0[b] = nullptr;
     }
     cudaFree(s->keys);
+    cudaFree(s->cand_sz);
     cudaFree(s->packed);
     cudaFree(s->reports);
-    s->keys = nullptr, s->packed = nullptr, s->reports = nullptr;
+    s->keys = nullptr, s->packed = nullptr, s->reports = nullptr, s->cand_sz = nullptr;
     s->cand_cap = 0;
     for (int b = 0; b < 2; b++) {
         CU(cudaMalloc(&s->sub[b], want * sizeof(uint64_t)));
@@ -1151,10 +1643,23 @@ static int ensure_candidates(dhsa_sketch *s, uint64_t max_candidates)
     }
     s->packed_cap = pow2_at_least(want);
     CU(cudaMalloc(&s->keys, s->packed_cap * sizeof(uint64_t)));
+    CU(cudaMalloc(&s->cand_sz, want * sizeof(int32_t)));
     CU(cudaMalloc(&s->packed, s->packed_cap * sizeof(uint64_t)));
     CU(cudaMalloc(&s->reports, want * sizeof(ReportOut)));
     s->cand_cap = want;
     return DHSA_OK;
+}
+
+// entries the stage buffers hold for a read-out bounded by max_candidates
+static uint64_t buffer_cap(const dhsa_sketch *s, uint64_t max_candidates)
+{
+    return max_candidates < s->cand_cap ? max_candidates : s->cand_cap;
+}
+
+static int ensure_candidates_for(dhsa_sketch *s, uint64_t max_candidates)
+{
+    if (s->cand_cap >= max_candidates || s->cand_cap >= kInitialCandidates) return DHSA_OK;
+    return ensure_candidates(s, max_candidates < kInitialCandidates ? max_candidates : kInitialCandidates);
 }
 
 // K2: zero counts of every cell.
@@ -1178,14 +1683,101 @@ static int launch_zero_counts(dhsa_sketch *s)
 
 static int refuse_if_restore_pending(const dhsa_sketch *s);
 
+// ---- the read-out's floating point, on the host -----------------------------------------------
+// Every number the reference derives with float64 math is derived here with the same formula and
+// the host's libm, as the reference does (math.log / math.exp / ** on Python floats):
+//   zmin        = g exp(-theta / g)                                  dhla.py:45-47
+//   flow count  = mean_i( -C ln(ZR(i)/C) ), ZR == 0 -> 1, saturated  estimator.py:26-34, dhla.py:121-128
+//   psi         = 1 - exp(-flow / C)                                 dhla.py:130-134
+//   denom       = g (1 - psi^r)                                      dhla.py:184
+//   estimate    = -g ln(SZ'/denom), 0.0 when SZ' >= denom            dhla.py:183-189
+// and the two threshold decisions become integer compares the kernels apply exactly:
+//   hot   <=> zc < zmin          <=> zc <= zc_cut    (zc_cut = the largest integer below zmin)
+//   keep  <=> estimate >= theta  <=> SZ' <= sz_cut   (the estimate is non-increasing in SZ')
+// zc_cut is known before the read-out is queued.  sz_cut needs psi, i.e. the zero totals the device
+// is about to count, so the device bisects its own cut (report_cut) to keep the chain free of host
+// round trips, and the host recomputes it here from the zero totals that came back: if the two ever
+// differ, the reports are re-filtered on the device with the host's cut (restore_collect).
+static int hot_cut(const dhsa_sketch *s, double theta)
+{
+    const double g = (double)s->params.g;
+    const double zmin = g * exp(-theta / g);
+    if (!(zmin > 0.0)) return -1;                     // nothing is below zero (also NaN)
+    if (zmin > g) return s->params.g;                 // theta < 0: every cell is hot
+    long long c = (long long)ceil(zmin) - 1;          // largest integer strictly below zmin
+    while ((double)(c + 1) < zmin) c++;
+    while (c >= 0 && !((double)c < zmin)) c--;
+    return (int)c;
+}
+
+struct HostScalars {
+    double flow, psi, denom;
+    int flow_saturated;
+    int sz_cut;
+};
+
+static double host_estimate(int g, long long sz_clamped, double denom)
+{
+    if ((double)sz_clamped >= denom) return 0.0;
+    return -(double)g * log((double)sz_clamped / denom);
+}
+
+static HostScalars host_scalars(const dhsa_sketch *s, const long long *zero_totals, double theta)
+{
+    HostScalars h;
+    const int r = s->params.r, g = s->params.g;
+    const double cap = (double)g * (double)(1ull << s->params.k);
+    // sum(e.value for e in per_array) (dhla.py:127): the interpreter this reference runs on (CPython >= 3.12)
+    // adds floats with Neumaier's compensated summation, so the mean is formed the same way here --
+    // the last bit of the flow count would otherwise differ from the live reference's
+    double acc = 0.0, comp = 0.0;
+    h.flow_saturated = 0;
+    for (int i = 0; i < r; i++) {
+        long long z = zero_totals[i];
+        if (z == 0) {
+            h.flow_saturated = 1;
+            z = 1;
+        }
+        const double x = -cap * log((double)z / cap);
+        const double t = acc + x;
+        comp += fabs(acc) >= fabs(x) ? (acc - t) + x : (x - t) + acc;
+        acc = t;
+    }
+    if (comp != 0.0 && isfinite(comp)) acc += comp;
+    h.flow = acc / r;
+    h.psi = 1.0 - exp(-h.flow / cap);
+    h.denom = g * (1.0 - pow(h.psi, (double)r));
+    // largest SZ' in [1, g] whose estimate reaches theta (0 = none): bisection, then a walk over the
+    // neighbours so that a non-monotone last bit of log() cannot leave the boundary one step off
+    int cut = 0;
+    if (host_estimate(g, 1, h.denom) >= theta) {
+        int lo = 1, hi = g;
+        if (host_estimate(g, hi, h.denom) >= theta) {
+            lo = hi;
+        } else {
+            while (hi - lo > 1) {
+                const int mid = lo + ((hi - lo) >> 1);
+                if (host_estimate(g, mid, h.denom) >= theta) lo = mid; else hi = mid;
+            }
+        }
+        while (lo < g && host_estimate(g, lo + 1, h.denom) >= theta) lo++;
+        cut = lo;
+    }
+    h.sz_cut = cut;
+    return h;
+}
+
 // K2 + hot sets + scalars, stream-ordered.
 static int launch_estimate(dhsa_sketch *s, double theta)
 {
     if (int rc = ensure_readout(s)) return rc;
-    if (int rc = launch_zero_counts(s)) return rc;
-    const double zmin = (double)s->params.g * exp(-theta / (double)s->params.g);  // dhla.py:45-47
-    k_hot_sets<<<s->params.r, 1024, 0, s->stream>>>(s->zc, zmin, s->params.r, s->params.k, s->params.g, s->lists,
-                                                   s->bitmaps, s->bitmap_words, s->ctl);
+    if (s->zc_given) {
+        s->zc_given = false;  // the caller's zero counts are already in s->zc (dhsa_use_zero_counts)
+    } else if (int rc = launch_zero_counts(s)) {
+        return rc;
+    }
+    k_hot_sets<<<s->params.r, 1024, 0, s->stream>>>(s->zc, hot_cut(s, theta), theta, s->params.r, s->params.k,
+                                                   s->params.g, s->lists, s->bitmaps, s->bitmap_words, s->ctl);
     s->launches += 1;
     CU(cudaGetLastError());
     return DHSA_OK;
@@ -1194,19 +1786,19 @@ static int launch_estimate(dhsa_sketch *s, double theta)
 // K3: stage chain -> verified keys in s->keys, count in ctl->n_candidates.
 static int launch_restore_stages(dhsa_sketch *s, uint64_t max_candidates, bool verify, int *last_buf)
 {
-    if (int rc = ensure_candidates(s, max_candidates)) return rc;
+    const uint64_t cap = buffer_cap(s, max_candidates);
     const int r = s->params.r, n_stages = r - 2;
     const int grid = s->sm_count * DHSA_READOUT_CTAS_PER_SM;
-    k_stage_first<<<grid, 256, 0, s->stream>>>(s->lists, s->bitmaps, s->bitmap_words, s->dp, max_candidates,
-                                               s->sub[0], s->cl0[0], s->ctl);
+    k_stage_first<<<grid, 256, 0, s->stream>>>(s->lists, s->bitmaps, s->bitmap_words, s->dp, cap, s->sub[0], s->cl0[0],
+                                               s->ctl);
     int cur = 0;
     for (int i = 3; i < r; i++) {
-        k_stage_next<<<grid, 256, 0, s->stream>>>(i, s->lists, s->bitmaps, s->bitmap_words, s->dp, max_candidates,
-                                                  s->sub[cur], s->cl0[cur], s->sub[cur ^ 1], s->cl0[cur ^ 1], s->ctl);
+        k_stage_next<<<grid, 256, 0, s->stream>>>(i, s->lists, s->bitmaps, s->bitmap_words, s->dp, cap, s->sub[cur],
+                                                  s->cl0[cur], s->sub[cur ^ 1], s->cl0[cur ^ 1], s->ctl);
         cur ^= 1;
     }
     if (verify)
-        k_verify_keys<<<grid, 256, 0, s->stream>>>(n_stages, s->dp, max_candidates, s->sub[cur], s->cl0[cur], s->keys,
+        k_verify_keys<<<grid, 256, 0, s->stream>>>(n_stages, s->dp, cap, max_candidates, s->sub[cur], s->cl0[cur], s->keys,
                                                    s->ctl);
     if (last_buf) *last_buf = cur;
     s->launches += (uint64_t)n_stages + (verify ? 1 : 0);
@@ -1237,24 +1829,36 @@ static int sort_large(dhsa_sketch *s, uint64_t *data, uint64_t n)
     return DHSA_OK;
 }
 
-static void fill_info(const dhsa_sketch *s, dhsa_restore_info_t *info)
+// *info from the control block that came back, with the float64 scalars from the host's formulas.
+static void fill_info(const dhsa_sketch *s, double theta, dhsa_restore_info_t *info)
 {
     if (!info) return;
     const Control *c = s->ctl_host;
     memset(info, 0, sizeof *info);
+    const HostScalars h = host_scalars(s, c->zero_totals, theta);
     info->n_candidates = c->n_candidates;
     info->n_reports = c->n_reports;
     info->fail_stage = c->fail_stage;
     info->fail_count = c->fail_count;
-    info->flow_saturated = c->flow_saturated;
-    info->flow_count = c->flow_count;
-    info->psi = c->psi;
-    info->denom = c->denom;
+    info->flow_saturated = h.flow_saturated;
+    info->flow_count = h.flow;
+    info->psi = h.psi;
+    info->denom = h.denom;
+    info->sz_cut = h.sz_cut;
+    info->hot_cut = hot_cut(s, theta);
     for (int i = 0; i < 64; i++) {
         info->hot_counts[i] = c->hot_counts[i];
         info->stage_counts[i] = c->stage_counts[i];
         info->zero_totals[i] = c->zero_totals[i];
     }
+}
+
+// a window's read-out came back: what it says about the traffic (the auto policy's regime)
+static void note_traffic_regime(dhsa_sketch *s)
+{
+    const unsigned long long *w = s->tally_pinned;  // [0..1] record tally, [2..3] flow cache, [4..5] test kernel
+    const unsigned long long seen = w[2] + w[4];
+    if (seen >= kPolicyMinSample) s->regime_few_keys = s->ctl_host->busy_cells <= kFewCells;
 }
 
 extern "C" int dhsa_zero_counts(dhsa_sketch_t *s, int64_t *zc_host, int64_t *zr_host)
@@ -1264,21 +1868,44 @@ extern "C" int dhsa_zero_counts(dhsa_sketch_t *s, int64_t *zc_host, int64_t *zr_
     std::lock_guard<std::mutex> lk(s->mu);
     if (int rc = use_device(s)) return rc;
     if (int rc = refuse_if_restore_pending(s)) return rc;
+    if (int rc = flush_host_locked(s)) return rc;
+    s->zc_given = false;
     if (int rc = launch_estimate(s, 0.0)) return rc;
     // widen on the host side of the copy: device keeps int32, the reference API is int64
-    int32_t *tmp = nullptr;
-    CU(cudaMallocHost(&tmp, s->dp.ncell * sizeof(int32_t)));
-    cudaError_t e = cudaMemcpyAsync(tmp, s->zc, s->dp.ncell * sizeof(int32_t), cudaMemcpyDeviceToHost, s->stream);
-    if (e == cudaSuccess) e = cudaMemcpyAsync(s->ctl_host, s->ctl, sizeof(Control), cudaMemcpyDeviceToHost, s->stream);
-    if (e == cudaSuccess) e = cudaStreamSynchronize(s->stream);
-    if (e != cudaSuccess) {
-        cudaFreeHost(tmp);
-        return cuda_fail(e, "zero_counts readback");
-    }
+    if (int rc = ensure_host_tmp(s, s->dp.ncell * sizeof(int32_t))) return rc;
+    int32_t *tmp = static_cast<int32_t *>(s->host_tmp);
+    CU(cudaMemcpyAsync(tmp, s->zc, s->dp.ncell * sizeof(int32_t), cudaMemcpyDeviceToHost, s->stream));
+    CU(cudaMemcpyAsync(s->ctl_host, s->ctl, sizeof(Control), cudaMemcpyDeviceToHost, s->stream));
+    CU(cudaStreamSynchronize(s->stream));
     for (uint64_t c = 0; c < s->dp.ncell; c++) zc_host[c] = tmp[c];
-    cudaFreeHost(tmp);
     if (zr_host)
         for (int i = 0; i < s->params.r; i++) zr_host[i] = s->ctl_host->zero_totals[i];
+    return DHSA_OK;
+}
+
+// The reference's read-out methods take an optional zero_counts= array and use it in place of
+// counting the bits (hot_sets dhla.py:111-119, estimate_flow_count :121-128, _candidate_hosts
+// :198-207).  One-shot: the next dhsa_hot_sets / dhsa_estimate / dhsa_candidate_hosts on this handle
+// starts from these counts.
+extern "C" int dhsa_use_zero_counts(dhsa_sketch_t *s, const int64_t *zc_host)
+{
+    NEED(s);
+    NEED(zc_host);
+    std::lock_guard<std::mutex> lk(s->mu);
+    if (int rc = use_device(s)) return rc;
+    if (int rc = refuse_if_restore_pending(s)) return rc;
+    if (int rc = ensure_readout(s)) return rc;
+    if (int rc = ensure_host_tmp(s, s->dp.ncell * sizeof(int32_t))) return rc;
+    int32_t *tmp = static_cast<int32_t *>(s->host_tmp);
+    for (uint64_t c = 0; c < s->dp.ncell; c++) {
+        if (zc_host[c] < 0 || zc_host[c] > s->params.g)
+            return fail(DHSA_EDATA, "zero count %lld of cell %llu outside [0, g=%d]", (long long)zc_host[c],
+                        (unsigned long long)c, s->params.g);
+        tmp[c] = (int32_t)zc_host[c];
+    }
+    CU(cudaMemcpyAsync(s->zc, tmp, s->dp.ncell * sizeof(int32_t), cudaMemcpyHostToDevice, s->stream));
+    CU(cudaStreamSynchronize(s->stream));  // host_tmp is reused by the read-out that follows
+    s->zc_given = true;
     return DHSA_OK;
 }
 
@@ -1290,26 +1917,18 @@ extern "C" int dhsa_hot_sets(dhsa_sketch_t *s, double theta, uint64_t *lists_hos
     std::lock_guard<std::mutex> lk(s->mu);
     if (int rc = use_device(s)) return rc;
     if (int rc = refuse_if_restore_pending(s)) return rc;
+    if (int rc = flush_host_locked(s)) return rc;
     if (int rc = launch_estimate(s, theta)) return rc;
+    if (int rc = ensure_host_tmp(s, s->dp.ncell * sizeof(uint32_t))) return rc;
+    uint32_t *tmp = static_cast<uint32_t *>(s->host_tmp);
+    CU(cudaMemcpyAsync(tmp, s->lists, s->dp.ncell * sizeof(uint32_t), cudaMemcpyDeviceToHost, s->stream));
     if (int rc = read_control(s)) return rc;
     const uint64_t m = 1ull << s->params.k;
-    uint32_t *tmp = nullptr;
-    CU(cudaMallocHost(&tmp, m * sizeof(uint32_t)));
     for (int i = 0; i < s->params.r; i++) {
         const uint64_t n = s->ctl_host->hot_counts[i];
         counts_host[i] = n;
-        if (n) {
-            cudaError_t e = cudaMemcpyAsync(tmp, s->lists + (uint64_t)i * m, n * sizeof(uint32_t),
-                                            cudaMemcpyDeviceToHost, s->stream);
-            if (e == cudaSuccess) e = cudaStreamSynchronize(s->stream);
-            if (e != cudaSuccess) {
-                cudaFreeHost(tmp);
-                return cuda_fail(e, "hot_sets readback");
-            }
-            for (uint64_t q = 0; q < n; q++) lists_host[(uint64_t)i * m + q] = tmp[q];
-        }
+        for (uint64_t q = 0; q < n; q++) lists_host[(uint64_t)i * m + q] = tmp[(uint64_t)i * m + q];
     }
-    cudaFreeHost(tmp);
     return DHSA_OK;
 }
 
@@ -1320,9 +1939,10 @@ extern "C" int dhsa_estimate(dhsa_sketch_t *s, double theta, dhsa_restore_info_t
     std::lock_guard<std::mutex> lk(s->mu);
     if (int rc = use_device(s)) return rc;
     if (int rc = refuse_if_restore_pending(s)) return rc;
+    if (int rc = flush_host_locked(s)) return rc;
     if (int rc = launch_estimate(s, theta)) return rc;
     if (int rc = read_control(s)) return rc;
-    fill_info(s, info);
+    fill_info(s, theta, info);
     return DHSA_OK;
 }
 
@@ -1334,6 +1954,21 @@ static int capacity_error(const dhsa_sketch *s, uint64_t max_candidates)
                 (unsigned long long)max_candidates);
 }
 
+// The stage buffers were too small for a stage that max_candidates allows: how many entries the
+// rerun needs (0 = the buffers were large enough).  ctl_host holds the control block of the run.
+static uint64_t regrow_target(const dhsa_sketch *s, uint64_t max_candidates)
+{
+    const Control *c = s->ctl_host;
+    if (c->fail_stage || c->any_empty) return 0;
+    const uint64_t cap = buffer_cap(s, max_candidates);
+    for (int st = 0; st < s->params.r - 2; st++)
+        if (c->stage_counts[st] > cap) {
+            uint64_t want = pow2_at_least(c->stage_counts[st]);
+            return want < max_candidates ? want : max_candidates;
+        }
+    return 0;
+}
+
 extern "C" int dhsa_candidate_hosts(dhsa_sketch_t *s, double theta, uint64_t max_candidates, uint64_t *hosts_host,
                                     uint64_t hosts_cap, dhsa_restore_info_t *info)
 {
@@ -1341,14 +1976,22 @@ extern "C" int dhsa_candidate_hosts(dhsa_sketch_t *s, double theta, uint64_t max
     std::lock_guard<std::mutex> lk(s->mu);
     if (int rc = use_device(s)) return rc;
     if (int rc = refuse_if_restore_pending(s)) return rc;
-    if (int rc = launch_estimate(s, theta)) return rc;
-    if (int rc = launch_restore_stages(s, max_candidates, true, nullptr)) return rc;
-    k_sort_small<<<1, 1024, DHSA_SORT_SMEM_MAX * sizeof(uint64_t), s->stream>>>(s->keys, &s->ctl->n_candidates, s->ctl,
-                                                                                 nullptr, 0);
-    s->launches++;
-    CU(cudaGetLastError());
-    if (int rc = read_control(s)) return rc;
-    fill_info(s, info);
+    if (int rc = flush_host_locked(s)) return rc;
+    if (int rc = ensure_readout(s)) return rc;
+    if (int rc = ensure_candidates_for(s, max_candidates)) return rc;
+    for (;;) {
+        if (int rc = launch_estimate(s, theta)) return rc;
+        if (int rc = launch_restore_stages(s, max_candidates, true, nullptr)) return rc;
+        k_sort_small<<<1, 1024, DHSA_SORT_SMEM_MAX * sizeof(uint64_t), s->stream>>>(s->keys, &s->ctl->n_candidates, s->ctl,
+                                                                                     nullptr, 0);
+        s->launches++;
+        CU(cudaGetLastError());
+        if (int rc = read_control(s)) return rc;
+        const uint64_t want = regrow_target(s, max_candidates);
+        if (!want) break;
+        if (int rc = ensure_candidates(s, want)) return rc;  // the bits are untouched: run the chain again
+    }
+    fill_info(s, theta, info);
     if (s->ctl_host->fail_stage) return capacity_error(s, max_candidates);
     const uint64_t n = s->ctl_host->n_candidates;
     if (n > DHSA_SORT_SMEM_MAX)
@@ -1371,6 +2014,7 @@ extern "C" int dhsa_shared_zero_counts(dhsa_sketch_t *s, const uint64_t *hosts_h
     NEED(sz_host);
     std::lock_guard<std::mutex> lk(s->mu);
     if (int rc = use_device(s)) return rc;
+    if (int rc = flush_host_locked(s)) return rc;
     if (n > s->hosts_in_cap) {
         CU(cudaStreamSynchronize(s->stream));
         cudaFree(s->hosts_in);
@@ -1406,10 +2050,12 @@ static int enqueue_restore(dhsa_sketch *s, double theta, uint64_t max_candidates
     if (int rc = launch_estimate(s, theta)) return rc;
     int cur = 0;
     if (int rc = launch_restore_stages(s, max_candidates, false, &cur)) return rc;
+    s->restore_last_buf = cur;
     const int grid = s->sm_count * DHSA_READOUT_CTAS_PER_SM;
     // verify + re-estimate, then sort + emit: two launches for what were four
-    k_verify_reestimate<<<grid, 256, 0, s->stream>>>(s->params.r - 2, s->dp, max_candidates, s->sub[cur], s->cl0[cur],
-                                                     s->bits, theta, s->keys, s->packed, s->ctl);
+    k_verify_reestimate<<<grid, 256, 0, s->stream>>>(s->params.r - 2, s->dp, buffer_cap(s, max_candidates), max_candidates,
+                                                     s->sub[cur], s->cl0[cur], s->bits, s->keys, s->cand_sz, s->packed,
+                                                     s->ctl);
     k_sort_small<<<1, 1024, DHSA_SORT_SMEM_MAX * sizeof(uint64_t), s->stream>>>(s->packed, &s->ctl->n_reports, s->ctl,
                                                                                  s->reports, s->params.g);
     s->launches += 2;
@@ -1417,7 +2063,8 @@ static int enqueue_restore(dhsa_sketch *s, double theta, uint64_t max_candidates
     CU(cudaMemcpyAsync(s->ctl_host, s->ctl, sizeof(Control), cudaMemcpyDeviceToHost, s->stream));
     const uint64_t rows = s->cand_cap < kPinnedReports ? s->cand_cap : kPinnedReports;
     CU(cudaMemcpyAsync(s->reports_pinned, s->reports, rows * sizeof(ReportOut), cudaMemcpyDeviceToHost, s->stream));
-    CU(cudaMemcpyAsync(s->tally_pinned, s->tally, 2 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s->stream));
+    // record tally + the scan kernels' counters (6 words behind the bit array) as they stand at this read-out
+    CU(cudaMemcpyAsync(s->tally_pinned, s->tally, 6 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s->stream));
     return DHSA_OK;
 }
 
@@ -1427,7 +2074,7 @@ static int enqueue_restore(dhsa_sketch *s, double theta, uint64_t max_candidates
 static int run_restore(dhsa_sketch *s, double theta, uint64_t max_candidates)
 {
     if (int rc = ensure_readout(s)) return rc;
-    if (int rc = ensure_candidates(s, max_candidates)) return rc;
+    if (int rc = ensure_candidates_for(s, max_candidates)) return rc;
     if (!s->graph_disabled) {
         const bool fresh = s->restore_graph && s->graph_theta == theta &&
                            s->graph_max_candidates == max_candidates && s->graph_cand_cap == s->cand_cap;
@@ -1483,11 +2130,37 @@ static int refuse_if_restore_pending(const dhsa_sketch *s)
 static int restore_begin_locked(dhsa_sketch *s, double theta, uint64_t max_candidates)
 {
     if (int rc = refuse_if_restore_pending(s)) return rc;
+    if (int rc = flush_host_locked(s)) return rc;
+    s->zc_given = false;  // restore_superpoints always counts the bits itself (dhla.py:176)
     if (int rc = run_restore(s, theta, max_candidates)) return rc;
     CU(cudaEventRecord(s->restore_ev, s->stream));
     s->restore_pending = true;
     s->restore_max_candidates = max_candidates;
+    s->restore_theta = theta;
+    s->restore_seq = s->mutation_seq;
     return DHSA_OK;
+}
+
+// The filter and the sort again with the host's scalars (denom, sz_cut) in the device control
+// block -- taken when the device's own libm put the cut, or the zero-estimate class, one step away
+// from where the host's formulas put it.  Uses only what the read-out left in the workspaces (the
+// verified keys and their SZ), not the bits: the next window may already be in them.
+static int refilter_with_host_cut(dhsa_sketch *s, const HostScalars &h)
+{
+    Control *c = s->ctl_host;
+    c->denom = h.denom, c->psi = h.psi, c->flow_count = h.flow;
+    c->n_reports = 0;
+    c->sorted = 0;
+    CU(cudaMemcpyAsync(s->ctl, c, sizeof(Control), cudaMemcpyHostToDevice, s->stream));
+    const int grid = s->sm_count * DHSA_READOUT_CTAS_PER_SM;
+    k_refilter<<<grid, 256, 0, s->stream>>>(s->keys, s->cand_sz, h.sz_cut, s->packed, s->ctl);
+    k_sort_small<<<1, 1024, DHSA_SORT_SMEM_MAX * sizeof(uint64_t), s->stream>>>(s->packed, &s->ctl->n_reports, s->ctl,
+                                                                                 s->reports, s->params.g);
+    s->launches += 2;
+    CU(cudaGetLastError());
+    const uint64_t rows = s->cand_cap < kPinnedReports ? s->cand_cap : kPinnedReports;
+    CU(cudaMemcpyAsync(s->reports_pinned, s->reports, rows * sizeof(ReportOut), cudaMemcpyDeviceToHost, s->stream));
+    return read_control(s);
 }
 
 static int restore_end_locked(dhsa_sketch *s, dhsa_report_t *reports_host, uint64_t reports_cap,
@@ -1496,14 +2169,34 @@ static int restore_end_locked(dhsa_sketch *s, dhsa_report_t *reports_host, uint6
     if (!s->restore_pending) return fail(DHSA_ECONFIG, "dhsa_restore_end without dhsa_restore_begin");
     CU(cudaEventSynchronize(s->restore_ev));
     const uint64_t max_candidates = s->restore_max_candidates;
+    const double theta = s->restore_theta;
+    // a stage needed more room than the workspaces had (and max_candidates allows it): grow, run again
+    for (uint64_t want; (want = regrow_target(s, max_candidates)) != 0;) {
+        if (s->restore_seq != s->mutation_seq) {
+            s->restore_pending = false;
+            return fail(DHSA_ECONFIG, "restore needs room for %llu partial keys (workspace %llu) but the sketch was modified "
+                        "after dhsa_restore_begin; use dhsa_restore, or collect before the next window is fed",
+                        (unsigned long long)want, (unsigned long long)s->cand_cap);
+        }
+        if (int rc = ensure_candidates(s, want)) return rc;
+        if (int rc = run_restore(s, theta, max_candidates)) return rc;
+        CU(cudaStreamSynchronize(s->stream));
+    }
+    note_traffic_regime(s);
     if (s->ctl_host->fail_stage) {
         s->restore_pending = false;
-        fill_info(s, info);
+        fill_info(s, theta, info);
         return capacity_error(s, max_candidates);
+    }
+    // the threshold decision belongs to the host's formulas (see host_scalars)
+    const HostScalars h = host_scalars(s, s->ctl_host->zero_totals, theta);
+    if (!s->ctl_host->any_empty && s->ctl_host->n_candidates &&
+        (h.sz_cut != s->ctl_host->sz_cut || ceil(h.denom) != ceil(s->ctl_host->denom))) {
+        if (int rc = refilter_with_host_cut(s, h)) return rc;
     }
     const int grid = s->sm_count * DHSA_READOUT_CTAS_PER_SM;
     const uint64_t n = s->ctl_host->n_reports;
-    fill_info(s, info);
+    fill_info(s, theta, info);
     // too small an output buffer: the read-out stays collectable, the caller retries with n_reports rows
     if (n > reports_cap) return fail(DHSA_EDATA, "%llu reports exceed the output capacity %llu",
                                      (unsigned long long)n, (unsigned long long)reports_cap);
@@ -1524,6 +2217,11 @@ static int restore_end_locked(dhsa_sketch *s, dhsa_report_t *reports_host, uint6
         } else {
             CU(cudaMemcpyAsync(reports_host, s->reports, n * sizeof(ReportOut), cudaMemcpyDeviceToHost, s->stream));
             CU(cudaStreamSynchronize(s->stream));
+        }
+        // estimates from the integer SZ with the host's formula (the device rows carry its own libm's value)
+        for (uint64_t t = 0; t < n; t++) {
+            const int32_t sz = reports_host[t].shared_zero_count;
+            reports_host[t].estimate = sz < 0 ? 0.0 : host_estimate(s->params.g, sz == 0 ? 1 : sz, h.denom);
         }
     }
     return DHSA_OK;
@@ -1556,6 +2254,75 @@ extern "C" int dhsa_restore_end(dhsa_sketch_t *s, dhsa_report_t *reports_host, u
     std::lock_guard<std::mutex> lk(s->mu);
     if (int rc = use_device(s)) return rc;
     return restore_end_locked(s, reports_host, reports_cap, info);
+}
+
+// ------------------------------------------------------- hash group, stateless --
+
+static int dev_params_from(const dhsa_params_t *params, DevParams *d)
+{
+    if (int rc = validate(params)) return rc;
+    memset(d, 0, sizeof *d);
+    const uint64_t m = 1ull << params->k;
+    d->r = params->r, d->k = params->k, d->alpha = params->alpha, d->key_width = params->key_width;
+    d->log2g = ilog2_exact(params->g);
+    d->kmask = (uint32_t)(m - 1);
+    d->gmask = (uint32_t)(params->g - 1);
+    d->state_dh0 = params->state_dh0, d->state_h1 = params->state_h1;
+    d->ncell = (uint64_t)params->r * m;
+    return DHSA_OK;
+}
+
+// shared body of the two calls below: `in` (n x in_width u64) -> out0 (n x out_width u64) [+ ok bytes]
+static int hash_group_call(const dhsa_params_t *params, int device, bool inverse, const uint64_t *in_host, uint64_t n,
+                           uint64_t *out_host, uint8_t *ok_host)
+{
+    NEED(params);
+    DevParams d;
+    if (int rc = dev_params_from(params, &d)) return rc;
+    if (n == 0) return DHSA_OK;
+    NEED(in_host);
+    NEED(out_host);
+    if (inverse) NEED(ok_host);
+    CU(cudaSetDevice(device));
+    const uint64_t in_w = inverse ? (uint64_t)d.r : 1, out_w = inverse ? 1 : (uint64_t)d.r;
+    uint64_t *in_dev = nullptr, *out_dev = nullptr;
+    uint8_t *ok_dev = nullptr;
+    cudaStream_t st = nullptr;
+    cudaError_t e = cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaMalloc(&in_dev, n * in_w * 8);
+    if (e == cudaSuccess) e = cudaMalloc(&out_dev, n * out_w * 8);
+    if (e == cudaSuccess && inverse) e = cudaMalloc(&ok_dev, n);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(in_dev, in_host, n * in_w * 8, cudaMemcpyHostToDevice, st);
+    if (e == cudaSuccess) {
+        int sms = 1;
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+        uint64_t want = (n + 255) / 256, cap = (uint64_t)sms * 8;
+        const int grid = (int)(want < cap ? want : cap);
+        if (inverse)
+            k_reconstruct_many<<<grid, 256, 0, st>>>(d, in_dev, n, out_dev, ok_dev);
+        else
+            k_forward_many<<<grid, 256, 0, st>>>(d, in_dev, n, out_dev);
+        e = cudaGetLastError();
+    }
+    if (e == cudaSuccess) e = cudaMemcpyAsync(out_host, out_dev, n * out_w * 8, cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess && inverse) e = cudaMemcpyAsync(ok_host, ok_dev, n, cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+    cudaFree(in_dev), cudaFree(out_dev), cudaFree(ok_dev);
+    if (st) cudaStreamDestroy(st);
+    if (e != cudaSuccess) return cuda_fail(e, inverse ? "reconstruct_many" : "forward_many");
+    return DHSA_OK;
+}
+
+extern "C" int dhsa_forward_many(const dhsa_params_t *params, int device, const uint64_t *keys_host, uint64_t n,
+                                 uint64_t *indices_host)
+{
+    return hash_group_call(params, device, false, keys_host, n, indices_host, nullptr);
+}
+
+extern "C" int dhsa_reconstruct_many(const dhsa_params_t *params, int device, const uint64_t *tuples_host, uint64_t n,
+                                     uint64_t *keys_host, uint8_t *ok_host)
+{
+    return hash_group_call(params, device, true, tuples_host, n, keys_host, ok_host);
 }
 
 // ------------------------------------------------------------------- merge --
@@ -1597,10 +2364,13 @@ extern "C" int dhsa_or_merge(dhsa_sketch_t *dst, dhsa_sketch_t *src)
     {
         std::lock_guard<std::mutex> lk(src->mu);
         if (int rc = use_device(src)) return rc;
+        if (int rc = flush_host_locked(src)) return rc;
         CU(cudaStreamSynchronize(src->stream));
     }
     std::lock_guard<std::mutex> lk(dst->mu);
     if (int rc = use_device(dst)) return rc;
+    if (int rc = flush_host_locked(dst)) return rc;
+    dst->mutation_seq++;
     if (src->device != dst->device) {
         int can = 0;
         CU(cudaDeviceCanAccessPeer(&can, dst->device, src->device));
@@ -1620,6 +2390,8 @@ extern "C" int dhsa_or_merge_peers(dhsa_sketch_t *dst, const void *const *peer_b
     NEED(peer_bits_dev);
     std::lock_guard<std::mutex> lk(dst->mu);
     if (int rc = use_device(dst)) return rc;
+    if (int rc = flush_host_locked(dst)) return rc;
+    dst->mutation_seq++;
     return merge_range_locked(dst, peer_bits_dev, n_peers, byte_lo, byte_hi);
 }
 
@@ -1633,6 +2405,8 @@ extern "C" int dhsa_copy_slice_from_peer(dhsa_sketch_t *dst, const void *peer_bi
     if (byte_lo == byte_hi) return DHSA_OK;
     std::lock_guard<std::mutex> lk(dst->mu);
     if (int rc = use_device(dst)) return rc;
+    if (int rc = flush_host_locked(dst)) return rc;
+    dst->mutation_seq++;
     const uint64_t lo = byte_lo / 16, hi = byte_hi / 16;
     const int grid = grid_for(dst, hi - lo, 256, 8);
     k_copy_slice<<<grid, 256, 0, dst->stream>>>(reinterpret_cast<uint4 *>(dst->bits),
@@ -1651,6 +2425,8 @@ extern "C" int dhsa_or_merge_buffer(dhsa_sketch_t *dst, const void *bits_dev, ui
     if ((uintptr_t)bits_dev & 15u) return fail(DHSA_ECONFIG, "buffer must be 16-byte aligned");
     std::lock_guard<std::mutex> lk(dst->mu);
     if (int rc = use_device(dst)) return rc;
+    if (int rc = flush_host_locked(dst)) return rc;
+    dst->mutation_seq++;
     const void *peers[1] = {bits_dev};
     // whole 16-byte vectors, then the (at most 15-byte) tail of odd-sized toy sketches byte-wise via a padded view:
     // the allocation is padded and zero beyond nbytes on both sides only when the source is itself padded, so

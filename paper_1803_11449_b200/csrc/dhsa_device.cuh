@@ -32,6 +32,7 @@ struct DevParams {
     int fc_tag_bits;               // fc_shift + log2(g): key bits an entry stores
     uint32_t fc_epoch;             // entries of other epochs count as empty: a window reset is epoch + 1
     unsigned long long *fc_stats;  // [0] lookups, [1] hits
+    unsigned long long *test_stats;  // k_scan_vec4<.,1>: [0] packets, [1] REDs issued; null = do not count
 };
 
 // Device-resident control block of one read-out: every stage kernel reads its
@@ -48,8 +49,9 @@ struct Control {
     int any_empty;  // some hot set is empty -> no candidates (dhla.py:208-209)
     int sorted;     // reports/candidates were sorted on the device by the single-CTA sorter
     unsigned int blocks_done;  // k_hot_sets: CTAs finished (the last one computes the scalars)
-    unsigned int pad_;
+    int sz_cut;  // report filter as an integer: a candidate passes iff max(SZ, 1) <= sz_cut (see plan_readout)
     double flow_count, psi, denom;
+    unsigned long long busy_cells;  // non-empty cells of array 0 = distinct dh0 values seen (the auto policy's signal)
 };
 
 // ------------------------------------------------------------------ hashing --
@@ -454,6 +456,7 @@ __global__ void __launch_bounds__(256) k_scan_vec4(SRC src, uint32_t *__restrict
     const int wshift = p.log2g - 5;
     const uint64_t pol = policy_evict_first();
     uint32_t on_time = 0, late = 0;
+    uint32_t n_red = 0, n_pkt = 0;  // MODE 1 under the auto policy: new bits per packet (p.test_stats)
 
     for (uint64_t base = warp0 * 32; base < nvec; base += nwarps * 32) {
         const uint64_t v = base + lane;
@@ -462,6 +465,7 @@ __global__ void __launch_bounds__(256) k_scan_vec4(SRC src, uint32_t *__restrict
         uint32_t cs[4], os[4];
         bool ok[4];
         src.unpack(raw, v, cs, os, ok, on_time, late);
+        if (MODE == 1) n_pkt += (uint32_t)ok[0] + (uint32_t)ok[1] + (uint32_t)ok[2] + (uint32_t)ok[3];
 
         uint32_t widx[4][R];
         uint32_t mask[4];
@@ -492,12 +496,26 @@ __global__ void __launch_bounds__(256) k_scan_vec4(SRC src, uint32_t *__restrict
                 for (int i = 0; i < R; i++) {
                     const bool need = (w[j][i] & mask[j]) == 0;
                     if (MODE == 1) {
-                        if (need) red_or(words + widx[j][i], mask[j]);
+                        if (need) {
+                            red_or(words + widx[j][i], mask[j]);
+                            n_red++;
+                        }
                     } else {
                         red_or_aggregated(words, widx[j][i], mask[j], need, lane);
                     }
                 }
             }
+        }
+    }
+    if (MODE == 1 && p.test_stats != nullptr) {
+        unsigned long long pk = n_pkt, rd = n_red;
+        for (int d = 16; d > 0; d >>= 1) {
+            pk += __shfl_xor_sync(0xFFFFFFFFu, pk, d);
+            rd += __shfl_xor_sync(0xFFFFFFFFu, rd, d);
+        }
+        if (lane == 0 && pk) {
+            atomicAdd(p.test_stats + 0, pk);
+            atomicAdd(p.test_stats + 1, rd);
         }
     }
     flush_tally(src, on_time, late, lane);
@@ -943,7 +961,33 @@ __global__ void __launch_bounds__(256) k_zero_counts_small(const uint8_t *__rest
 //   psi         = 1 - exp(-flow / C)                          (dhla.py:130-134)
 //   denom       = g (1 - psi^r)                               (dhla.py:184)
 // and the "any hot set empty -> no candidates" rule (dhla.py:208-209).
-__device__ __forceinline__ void plan_readout(Control *ctl, int r, int k, int g)
+// Sharing-corrected estimate (pkg/src/dhsa/dhla.py:183-189):
+//   SZ == 0 -> saturated, evaluate at 1;  SZ >= denom -> 0.0;  else -g ln(SZ/denom).
+__device__ __forceinline__ double corrected_estimate(int g, int sz_clamped, double denom)
+{
+    if ((double)sz_clamped >= denom) return 0.0;
+    return -(double)g * log((double)sz_clamped / denom);
+}
+
+// The threshold filter `estimate >= theta` (dhla.py:190-194) as an integer cut on the clamped
+// SZ: the estimate is non-increasing in SZ, so the passing values are a prefix [1, sz_cut] of
+// [1, g] (0 = nothing passes).  Found by bisection here so the chain stays on the device; the
+// host re-derives the cut with its own libm from the same zero totals when it collects the
+// read-out (dhsa_cabi.cu: host_scalars) and re-filters in the -- never yet observed -- case that
+// the two disagree, so the decision is the host formula's, not this libm's.
+__device__ __forceinline__ int report_cut(int g, double denom, double theta)
+{
+    if (!(corrected_estimate(g, 1, denom) >= theta)) return 0;
+    int lo = 1, hi = g;  // invariant: lo passes
+    if (corrected_estimate(g, hi, denom) >= theta) return hi;
+    while (hi - lo > 1) {
+        const int mid = lo + ((hi - lo) >> 1);
+        if (corrected_estimate(g, mid, denom) >= theta) lo = mid; else hi = mid;
+    }
+    return lo;
+}
+
+__device__ __forceinline__ void plan_readout(Control *ctl, int r, int k, int g, double theta)
 {
     const double cap = (double)g * (double)(1ull << k);
     double acc = 0.0;
@@ -963,6 +1007,7 @@ __device__ __forceinline__ void plan_readout(Control *ctl, int r, int k, int g)
     ctl->flow_saturated = sat;
     ctl->psi = psi;
     ctl->denom = g * (1.0 - pow(psi, (double)r));
+    ctl->sz_cut = report_cut(g, ctl->denom, theta);
     ctl->any_empty = empty;
     for (int i = 0; i < 64; i++) ctl->stage_counts[i] = 0;
     ctl->n_candidates = 0;
@@ -973,13 +1018,14 @@ __device__ __forceinline__ void plan_readout(Control *ctl, int r, int k, int g)
 }
 
 // Dhla.hot_sets (pkg/src/dhsa/dhla.py:111-119): HE(i) = { j : zc[i][j] < zmin },
-// ascending; plus the 2^k-bit hot bitmap of each array and ZR(i) = sum_j zc[i][j]
+// ascending -- as the integer compare zc <= zc_cut, zc_cut = the largest integer below zmin,
+// derived on the host from the reference's own float64 formula (dhla.py:45-47); plus the 2^k-bit hot bitmap of each array and ZR(i) = sum_j zc[i][j]
 // (dhla.py:126).  One 1024-thread CTA per array; each thread owns 16 consecutive
 // cells (64 contiguous bytes of zero counts), so the default 2^14-cell array is
 // one pass: thread-local 16-bit hot mask, one block scan, in-order list writes.
 // The last CTA to finish computes the scalars above (no extra launch).
 #define DHSA_HOT_CPT 16
-__global__ void __launch_bounds__(1024) k_hot_sets(const int32_t *__restrict__ zc, double zmin, int r, int k, int g,
+__global__ void __launch_bounds__(1024) k_hot_sets(const int32_t *__restrict__ zc, int zc_cut, double theta, int r, int k, int g,
                                                    uint32_t *__restrict__ lists,
                                                    uint32_t *__restrict__ bitmaps,
                                                    uint64_t bitmap_words_per_array, Control *ctl)
@@ -996,6 +1042,7 @@ __global__ void __launch_bounds__(1024) k_hot_sets(const int32_t *__restrict__ z
     uint32_t *list = lists + (uint64_t)arr * m;
     uint32_t *bmp = bitmaps + (uint64_t)arr * bitmap_words_per_array;
     unsigned long long base = 0, total = 0;
+    uint32_t busy = 0;  // cells of this thread with at least one bit set
     for (uint64_t c0 = 0; c0 < m; c0 += 1024ull * DHSA_HOT_CPT) {
         const uint64_t j0 = c0 + (uint64_t)threadIdx.x * DHSA_HOT_CPT;
         uint32_t hot = 0;
@@ -1005,19 +1052,21 @@ __global__ void __launch_bounds__(1024) k_hot_sets(const int32_t *__restrict__ z
 #pragma unroll
             for (int q = 0; q < DHSA_HOT_CPT / 4; q++) {
                 const int4 z = v[q];
-                hot |= (uint32_t)((double)z.x < zmin) << (4 * q + 0);
-                hot |= (uint32_t)((double)z.y < zmin) << (4 * q + 1);
-                hot |= (uint32_t)((double)z.z < zmin) << (4 * q + 2);
-                hot |= (uint32_t)((double)z.w < zmin) << (4 * q + 3);
+                hot |= (uint32_t)(z.x <= zc_cut) << (4 * q + 0);
+                hot |= (uint32_t)(z.y <= zc_cut) << (4 * q + 1);
+                hot |= (uint32_t)(z.z <= zc_cut) << (4 * q + 2);
+                hot |= (uint32_t)(z.w <= zc_cut) << (4 * q + 3);
                 zs += (unsigned long long)z.x + (unsigned long long)z.y + (unsigned long long)z.z +
                       (unsigned long long)z.w;
+                busy += (uint32_t)(z.x < g) + (uint32_t)(z.y < g) + (uint32_t)(z.z < g) + (uint32_t)(z.w < g);
             }
         } else {
             for (int q = 0; q < DHSA_HOT_CPT; q++)
                 if (j0 + q < m) {
                     const int32_t z = row[j0 + q];
-                    hot |= (uint32_t)((double)z < zmin) << q;
+                    hot |= (uint32_t)(z <= zc_cut) << q;
                     zs += (unsigned long long)z;
+                    busy += (uint32_t)(z < g);
                 }
         }
         // bitmap: two threads share a 32-bit word
@@ -1055,6 +1104,16 @@ __global__ void __launch_bounds__(1024) k_hot_sets(const int32_t *__restrict__ z
         total += chunk_sum_s;
         __syncthreads();
     }
+    if (arr == 0) {  // block sum of the busy-cell counts (warp_count is free again after the loop's last barrier)
+        for (int d = 16; d > 0; d >>= 1) busy += __shfl_xor_sync(0xFFFFFFFFu, busy, d);
+        if (lane == 0) warp_count[wid] = busy;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            unsigned long long tot = 0;
+            for (int w = 0; w < 32; w++) tot += warp_count[w];
+            ctl->busy_cells = tot;
+        }
+    }
     if (threadIdx.x == 0) {
         ctl->hot_counts[arr] = base;
         ctl->zero_totals[arr] = (long long)total;
@@ -1064,7 +1123,7 @@ __global__ void __launch_bounds__(1024) k_hot_sets(const int32_t *__restrict__ z
     __syncthreads();
     if (is_last_s && threadIdx.x == 0) {
         __threadfence();
-        plan_readout(ctl, r, k, g);
+        plan_readout(ctl, r, k, g, theta);
         ctl->blocks_done = 0;
     }
 }
@@ -1086,15 +1145,21 @@ __device__ __forceinline__ bool bitmap_test(const uint32_t *bmp, uint32_t idx)
     return (bmp[idx >> 5] >> (idx & 31u)) & 1u;
 }
 
+// Two bounds travel through the stage kernels.  max_candidates is the reference's bound: a stage
+// that produces more partial keys raises CapacityError (dhla.py:269-273, 294-298).  buf_cap
+// (<= max_candidates) is what the workspaces hold right now: the library sizes them for the
+// default bound and grows them when a stage needs more (dhsa_cabi.cu: restore_collect), so a huge
+// "unlimited" max_candidates does not allocate 64 bytes per entry up front.  Every stage counts
+// all its survivors either way, so the counts -- and the error they trigger -- are exact.
 __device__ __forceinline__ bool stage_blocked(const Control *ctl, int stage_index,
-                                              unsigned long long max_candidates)
+                                              unsigned long long buf_cap)
 {
     // stage_index = number of stages already run.  Blocked when some hot set is
-    // empty, or an earlier stage overflowed (then nothing after it runs, like the
-    // exception in the reference).
+    // empty, or an earlier stage overflowed the buffers (then nothing after it runs:
+    // either the reference would have raised there, or the host grows the buffers and reruns).
     if (ctl->any_empty) return true;
     for (int s = 0; s < stage_index; s++)
-        if (ctl->stage_counts[s] > max_candidates) return true;
+        if (ctl->stage_counts[s] > buf_cap) return true;
     return false;
 }
 
@@ -1104,11 +1169,11 @@ __device__ __forceinline__ bool stage_blocked(const Control *ctl, int stage_inde
 __global__ void __launch_bounds__(256) k_stage_first(const uint32_t *__restrict__ lists,
                                                      const uint32_t *__restrict__ bitmaps,
                                                      uint64_t bitmap_words_per_array, DevParams p,
-                                                     unsigned long long max_candidates,
+                                                     unsigned long long buf_cap,
                                                      uint64_t *__restrict__ out_sub,
                                                      uint32_t *__restrict__ out_cl0, Control *ctl)
 {
-    if (stage_blocked(ctl, 0, max_candidates)) return;
+    if (stage_blocked(ctl, 0, buf_cap)) return;
     const uint64_t m = 1ull << p.k;
     const uint64_t n0 = ctl->hot_counts[0], n1 = ctl->hot_counts[1], n2 = ctl->hot_counts[2];
     const uint64_t next = 1ull << p.alpha;
@@ -1135,7 +1200,7 @@ __global__ void __launch_bounds__(256) k_stage_first(const uint32_t *__restrict_
         }
         if (ok) {
             const unsigned long long pos = atomicAdd(&ctl->stage_counts[0], 1ull);
-            if (pos < max_candidates) {
+            if (pos < buf_cap) {
                 out_sub[pos] = (uint64_t)b1 | ((uint64_t)(b2 >> top) << p.k);
                 out_cl0[pos] = cl0;
             }
@@ -1149,14 +1214,14 @@ __global__ void __launch_bounds__(256) k_stage_first(const uint32_t *__restrict_
 __global__ void __launch_bounds__(256) k_stage_next(int i, const uint32_t *__restrict__ lists,
                                                     const uint32_t *__restrict__ bitmaps,
                                                     uint64_t bitmap_words_per_array, DevParams p,
-                                                    unsigned long long max_candidates,
+                                                    unsigned long long buf_cap,
                                                     const uint64_t *__restrict__ in_sub,
                                                     const uint32_t *__restrict__ in_cl0,
                                                     uint64_t *__restrict__ out_sub,
                                                     uint32_t *__restrict__ out_cl0, Control *ctl)
 {
     const int s = i - 2;  // stages already run
-    if (stage_blocked(ctl, s, max_candidates)) return;
+    if (stage_blocked(ctl, s, buf_cap)) return;
     const uint64_t m = 1ull << p.k;
     const uint64_t np = ctl->stage_counts[s - 1], ni = ctl->hot_counts[i];
     const uint64_t next = 1ull << p.alpha;
@@ -1185,7 +1250,7 @@ __global__ void __launch_bounds__(256) k_stage_next(int i, const uint32_t *__res
         }
         if (ok) {
             const unsigned long long pos = atomicAdd(&ctl->stage_counts[s], 1ull);
-            if (pos < max_candidates) {
+            if (pos < buf_cap) {
                 out_sub[pos] = sp | ((uint64_t)(blk >> top) << sh_put);
                 out_cl0[pos] = cl0;
             }
@@ -1196,23 +1261,31 @@ __global__ void __launch_bounds__(256) k_stage_next(int i, const uint32_t *__res
 // Tail of _candidate_hosts (pkg/src/dhsa/dhla.py:213-216): drop partials with bits
 // above key_width, keep those whose dh0 reproduces cl0.  A key determines cl0 and
 // the tuple <-> (sub, cl0) map is one-to-one, so survivors are already distinct.
-__global__ void __launch_bounds__(256) k_verify_keys(int n_stages, DevParams p,
+// The first stage whose survivor count exceeds max_candidates: the numbers of the CapacityError
+// text (stage 1, then i - 1 for array i; dhla.py:269-273, 294-298).  A stage that only overflowed
+// the buffers (<= max_candidates) stops the scan: later counts are not final until the rerun.
+__device__ __forceinline__ void record_capacity_failure(Control *ctl, int n_stages, unsigned long long buf_cap,
+                                                        unsigned long long max_candidates)
+{
+    if (ctl->any_empty) return;
+    for (int st = 0; st < n_stages; st++) {
+        if (ctl->stage_counts[st] > max_candidates) {
+            ctl->fail_stage = st + 1;
+            ctl->fail_count = ctl->stage_counts[st];
+            return;
+        }
+        if (ctl->stage_counts[st] > buf_cap) return;
+    }
+}
+
+__global__ void __launch_bounds__(256) k_verify_keys(int n_stages, DevParams p, unsigned long long buf_cap,
                                                      unsigned long long max_candidates,
                                                      const uint64_t *__restrict__ in_sub,
                                                      const uint32_t *__restrict__ in_cl0,
                                                      uint64_t *__restrict__ keys, Control *ctl)
 {
-    if (blockIdx.x == 0 && threadIdx.x == 0 && !ctl->any_empty) {
-        // record the first overflowing stage: the numbers of the CapacityError text
-        // (stage 1, then i - 1 for array i; dhla.py:269-273, 294-298)
-        for (int st = 0; st < n_stages; st++)
-            if (ctl->stage_counts[st] > max_candidates) {
-                ctl->fail_stage = st + 1;
-                ctl->fail_count = ctl->stage_counts[st];
-                break;
-            }
-    }
-    if (stage_blocked(ctl, n_stages, max_candidates)) return;
+    if (blockIdx.x == 0 && threadIdx.x == 0) record_capacity_failure(ctl, n_stages, buf_cap, max_candidates);
+    if (stage_blocked(ctl, n_stages, buf_cap)) return;
     const uint64_t np = ctl->stage_counts[n_stages - 1];
     const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
     for (uint64_t q = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; q < np; q += stride) {
@@ -1220,7 +1293,7 @@ __global__ void __launch_bounds__(256) k_verify_keys(int n_stages, DevParams p,
         if (sub >> p.key_width) continue;
         if (dh0_of(p, sub) != in_cl0[q]) continue;
         const unsigned long long pos = atomicAdd(&ctl->n_candidates, 1ull);
-        keys[pos] = sub;  // pos < np <= max_candidates
+        keys[pos] = sub;  // pos < np <= buf_cap
     }
 }
 
@@ -1271,14 +1344,6 @@ __global__ void __launch_bounds__(256) k_shared_zero_counts(const uint8_t *__res
     }
 }
 
-// Sharing-corrected estimate (pkg/src/dhsa/dhla.py:183-189):
-//   SZ == 0 -> saturated, evaluate at 1;  SZ >= denom -> 0.0;  else -g ln(SZ/denom).
-__device__ __forceinline__ double corrected_estimate(int g, int sz_clamped, double denom)
-{
-    if ((double)sz_clamped >= denom) return 0.0;
-    return -(double)g * log((double)sz_clamped / denom);
-}
-
 // Sort key of one report.  The reference orders by (-estimate, host)
 // (dhla.py:195); the estimate is strictly decreasing in the clamped SZ below
 // denom and 0.0 from denom on, so (class, host) with class = clamped SZ, or one
@@ -1294,28 +1359,23 @@ __device__ __forceinline__ uint64_t pack_report(int sz, double denom, uint64_t h
 
 // Verify + re-estimate in one launch: one warp per partial key of the last stage -- key-width
 // cut, dh0(key) == cl0 (dhla.py:213-216; k_verify_keys is the stand-alone form behind
-// _candidate_hosts), then SZ, the estimate and the threshold filter (dhla.py:183-194).
-__global__ void __launch_bounds__(256) k_verify_reestimate(int n_stages, DevParams p,
+// _candidate_hosts), then SZ and the threshold filter (dhla.py:183-194) as the integer compare
+// max(SZ, 1) <= ctl->sz_cut.  Every verified key is kept with its SZ (keys[], cand_sz[]) so the
+// filter can be re-applied with another cut without touching the bits again (k_refilter).
+__global__ void __launch_bounds__(256) k_verify_reestimate(int n_stages, DevParams p, unsigned long long buf_cap,
                                                            unsigned long long max_candidates,
                                                            const uint64_t *__restrict__ in_sub,
                                                            const uint32_t *__restrict__ in_cl0,
-                                                           const uint8_t *__restrict__ bits, double theta,
-                                                           uint64_t *__restrict__ keys,
+                                                           const uint8_t *__restrict__ bits,
+                                                           uint64_t *__restrict__ keys, int32_t *__restrict__ cand_sz,
                                                            uint64_t *__restrict__ packed, Control *ctl)
 {
-    if (blockIdx.x == 0 && threadIdx.x == 0 && !ctl->any_empty) {
-        for (int st = 0; st < n_stages; st++)  // the numbers of the CapacityError text, as in k_verify_keys
-            if (ctl->stage_counts[st] > max_candidates) {
-                ctl->fail_stage = st + 1;
-                ctl->fail_count = ctl->stage_counts[st];
-                break;
-            }
-    }
-    if (stage_blocked(ctl, n_stages, max_candidates)) return;
+    if (blockIdx.x == 0 && threadIdx.x == 0) record_capacity_failure(ctl, n_stages, buf_cap, max_candidates);
+    if (stage_blocked(ctl, n_stages, buf_cap)) return;
     const uint32_t lane = threadIdx.x & 31u;
     const uint64_t np = ctl->stage_counts[n_stages - 1];
     const double denom = ctl->denom;
-    const int g = 1 << p.log2g;
+    const int cut = ctl->sz_cut;
     const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
     for (uint64_t q = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; q < np; q += nwarps) {
         const uint64_t sub = in_sub[q];
@@ -1323,11 +1383,27 @@ __global__ void __launch_bounds__(256) k_verify_reestimate(int n_stages, DevPara
         if (dh0_of(p, sub) != in_cl0[q]) continue;  // warp-uniform
         const int sz = shared_zero_count_warp(bits, p, sub, lane);
         if (lane == 0) {
-            keys[atomicAdd(&ctl->n_candidates, 1ull)] = sub;  // < np <= max_candidates
-            const double est = corrected_estimate(g, sz == 0 ? 1 : sz, denom);
-            if (est >= theta) packed[atomicAdd(&ctl->n_reports, 1ull)] = pack_report(sz, denom, sub);
+            const unsigned long long pos = atomicAdd(&ctl->n_candidates, 1ull);  // < np <= buf_cap
+            keys[pos] = sub;
+            cand_sz[pos] = sz;
+            if ((sz == 0 ? 1 : sz) <= cut) packed[atomicAdd(&ctl->n_reports, 1ull)] = pack_report(sz, denom, sub);
         }
     }
+}
+
+// The filter again, over the verified keys and their SZ, with a cut handed in by the host
+// (n_reports was zeroed by the caller).
+__global__ void __launch_bounds__(256) k_refilter(const uint64_t *__restrict__ keys, const int32_t *__restrict__ cand_sz,
+                                                  int cut, uint64_t *__restrict__ packed, Control *ctl)
+{
+    const uint64_t n = ctl->n_candidates;
+    const double denom = ctl->denom;
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; t < n; t += stride) {
+        const int sz = cand_sz[t];
+        if ((sz == 0 ? 1 : sz) <= cut) packed[atomicAdd(&ctl->n_reports, 1ull)] = pack_report(sz, denom, keys[t]);
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) ctl->sz_cut = cut;
 }
 
 struct ReportOut {
@@ -1671,6 +1747,50 @@ __global__ void __launch_bounds__(256) k_generate_trace(TraceSpec t, uint64_t p_
         }
         if (cand_out) cand_out[q] = src;
         if (opp_out) opp_out[q] = dst;
+    }
+}
+
+// ------------------------------------------- hash group, forward and inverse --
+// dhg.forward_many (pkg/src/dhsa/dhg.py:203-210): the r estimator indices of each key.
+__global__ void __launch_bounds__(256) k_forward_many(DevParams p, const uint64_t *__restrict__ keys, uint64_t n,
+                                                      uint64_t *__restrict__ indices)
+{
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; t < n; t += stride) {
+        const uint64_t a = keys[t];
+        const uint32_t d0 = dh0_of(p, a);
+        for (int i = 0; i < p.r; i++) indices[t * p.r + i] = index_of(p, a, d0, i);
+    }
+}
+
+// dhg.reconstruct_key / reconstruct_many (pkg/src/dhsa/dhg.py:161-185, 213-233): rebuild the key
+// of one full r-tuple of indices; accepted iff every pair of neighbouring blocks agrees on its
+// k - alpha overlapping bits, no bit lies above key_width and dh0(key) reproduces index 0 -- the
+// predicate the stage kernels apply incrementally (k_stage_first / _next / k_verify_keys).
+// keys[t] is written either way (the reference returns "garbage where not ok" too, the same
+// garbage: the OR of the shifted blocks).
+__global__ void __launch_bounds__(256) k_reconstruct_many(DevParams p, const uint64_t *__restrict__ tuples, uint64_t n,
+                                                          uint64_t *__restrict__ keys, uint8_t *__restrict__ ok_out)
+{
+    const int top = p.k - p.alpha;
+    const uint64_t omask = (1ull << top) - 1ull;
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; t < n; t += stride) {
+        const uint64_t *tp = tuples + t * p.r;
+        const uint64_t cl0 = tp[0];
+        uint64_t blk = cl0 ^ tp[1];
+        uint64_t key = blk;
+        bool ok = true;
+        for (int i = 2; i < p.r; i++) {
+            const uint64_t nxt = cl0 ^ tp[i];
+            ok = ok && (blk >> p.alpha) == (nxt & omask);
+            key |= (nxt >> top) << (p.k + (i - 2) * p.alpha);
+            blk = nxt;
+        }
+        ok = ok && (key >> p.key_width) == 0;
+        ok = ok && (mix64(p.state_dh0 ^ key) & (uint64_t)p.kmask) == cl0;
+        keys[t] = key;
+        ok_out[t] = ok ? 1 : 0;
     }
 }
 

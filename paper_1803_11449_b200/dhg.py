@@ -5,12 +5,19 @@ same field names, defaults, validation rules and messages, so a ``dhsa.DhgParams
 and this class are interchangeable at the sketch constructor.  The hashing
 itself runs on the device (csrc/dhsa_device.cuh); only the two seed -> state
 derivations and the scalar helpers a caller may want for a single key live
-here, as plain integer arithmetic.
+here, as plain integer arithmetic.  The array forms -- ``forward_many`` and the
+inverse ``reconstruct_key`` / ``reconstruct_many`` (dhg.py:161-233) -- are calls
+into libdhsa_b200.so like everything else on the path.
 """
 
 from __future__ import annotations
 
+import ctypes as C
+import os
 from dataclasses import dataclass
+from typing import Optional, Sequence
+
+import numpy as np
 
 from .errors import ConfigError
 
@@ -120,3 +127,61 @@ def forward(params: DhgParams, a: int) -> tuple:
     return (d0,) + tuple(
         ((a >> ((i - 1) * params.alpha)) & kmask) ^ d0 for i in range(1, params.r)
     )
+
+
+def dh_i(params: DhgParams, a: int, i: int) -> int:
+    """Index of host ``a`` in array ``i``, 1 <= i <= r-1 (dhg.py:131-139)."""
+    if not 1 <= i <= params.r - 1:
+        raise ValueError(f"array index i must be in [1, {params.r - 1}], got {i}")
+    return ((a >> ((i - 1) * params.alpha)) & (params.index_count - 1)) ^ dh0(params, a)
+
+
+def recover_block(params: DhgParams, cl0: int, cli: int) -> int:
+    """The key block an index carries under its XOR mask (dhg.py:146-148)."""
+    return cl0 ^ cli
+
+
+# Array forms: kernels behind the C ABI (dhsa_forward_many / dhsa_reconstruct_many).
+
+def _cparams(params: DhgParams):
+    from . import _cabi
+    p = DhgParams.coerce(params)
+    return _cabi, _cabi.Params(p.r, p.g, p.k, p.alpha, p.key_width, 0, p.state_dh0, p.state_h1)
+
+
+def _device(device: Optional[int]) -> int:
+    if device is not None:
+        return int(device)
+    env = os.environ.get("DHSA_DEVICE", os.environ.get("LOCAL_RANK"))
+    return int(env) if env not in (None, "") else 0
+
+
+def forward_many(params: DhgParams, keys, device: Optional[int] = None) -> np.ndarray:
+    """Estimator indices of a batch of keys, shape (len(keys), r), uint64 (dhg.py:203-210)."""
+    _cabi, cp = _cparams(params)
+    k = np.ascontiguousarray(keys, dtype=np.uint64).reshape(-1)
+    out = np.empty((len(k), cp.r), dtype=np.uint64)
+    _cabi.check(_cabi.lib().dhsa_forward_many(C.byref(cp), _device(device), k.ctypes.data, len(k), out.ctypes.data))
+    return out
+
+
+def reconstruct_many(params: DhgParams, tuples, device: Optional[int] = None):
+    """(keys, ok) of an (n, r) index matrix: rebuilt keys (garbage where not ok) and the boolean
+    acceptance mask (dhg.py:213-233)."""
+    _cabi, cp = _cparams(params)
+    t = np.ascontiguousarray(tuples, dtype=np.uint64)
+    if t.ndim != 2 or t.shape[1] != cp.r:
+        raise ValueError(f"expected an (n, {cp.r}) index matrix, got shape {t.shape}")
+    keys = np.empty(len(t), dtype=np.uint64)
+    ok = np.empty(len(t), dtype=np.uint8)
+    _cabi.check(_cabi.lib().dhsa_reconstruct_many(C.byref(cp), _device(device), t.ctypes.data, len(t),
+                                                  keys.ctypes.data, ok.ctypes.data))
+    return keys, ok.astype(bool)
+
+
+def reconstruct_key(params: DhgParams, indices: Sequence[int], device: Optional[int] = None) -> Optional[int]:
+    """The host key of one r-tuple of indices, or None if they are inconsistent (dhg.py:161-185)."""
+    if len(indices) != params.r:
+        raise ValueError(f"expected {params.r} indices, got {len(indices)}")
+    keys, ok = reconstruct_many(params, np.asarray([list(indices)], dtype=np.uint64), device=device)
+    return int(keys[0]) if ok[0] else None

@@ -67,10 +67,15 @@ class Dhla:
     """r * 2^k byte-packed linear estimators in HBM, addressed by the hash group."""
 
     def __init__(self, params, backend="auto", window_id: int = 0, device: Optional[int] = None):
-        if backend not in ("auto", "cuda"):
+        # The reference resolves names through get_backend and passes a Backend INSTANCE through
+        # unchanged (pkg/src/dhsa/_kernels.py:42-55, dhla.py:60-63).  Its Backend functions work on a
+        # host bits array, which this sketch does not have: only a record naming this backend is
+        # accepted, everything else is refused in the reference's wording.
+        name = backend if isinstance(backend, str) else getattr(backend, "name", backend)
+        if name not in ("auto", "cuda"):
             # the reference's names ("compiled", "python") are CPU kernels; none exist here
-            raise ConfigError(f"unknown backend {backend!r}; this build has only the CUDA path "
-                              f"(expected auto or cuda)")
+            raise ConfigError(f"unknown backend {name!r}; expected auto or cuda "
+                              f"(this build has only the CUDA path)")
         self.params = DhgParams.coerce(params)
         self.window_id = window_id
         self.device = _default_device() if device is None else int(device)
@@ -80,6 +85,7 @@ class Dhla:
         h = C.c_void_p()
         _cabi.check(self._lib.dhsa_create(C.byref(self._cparams), self.device, C.byref(h)))
         self._h = h
+        self._stream_ref = None   # keeps a caller's stream object alive while the sketch launches on it
         self.last_info: Optional[dict] = None
 
     def __del__(self):
@@ -114,13 +120,18 @@ class Dhla:
         _cabi.check(self._lib.dhsa_launch_count(self._h, C.byref(n)))
         return int(n.value)
 
-    def use_stream(self, cuda_stream: Optional[int]) -> None:
-        """Launch on this cudaStream_t handle (0 = CUDA's legacy default stream, which is
-        what torch's default stream reports); None -> back to the sketch's own stream."""
+    def use_stream(self, cuda_stream) -> None:
+        """Launch on this stream: a stream object exposing ``cuda_stream`` (a torch.cuda.Stream --
+        the sketch then holds a reference, so the handle stays valid for as long as it is used) or
+        a raw cudaStream_t handle the caller keeps alive (0 = CUDA's legacy default stream, which
+        is what torch's default stream reports); None -> back to the sketch's own stream."""
         if cuda_stream is None:
             _cabi.check(self._lib.dhsa_set_own_stream(self._h))
-        else:
-            _cabi.check(self._lib.dhsa_set_stream(self._h, C.c_void_p(int(cuda_stream))))
+            self._stream_ref = None
+            return
+        handle = getattr(cuda_stream, "cuda_stream", cuda_stream)
+        _cabi.check(self._lib.dhsa_set_stream(self._h, C.c_void_p(int(handle))))
+        self._stream_ref = cuda_stream if handle is not cuda_stream else None
 
     @property
     def stream_handle(self) -> int:
@@ -131,6 +142,13 @@ class Dhla:
 
     def set_scan_mode(self, mode) -> None:
         _cabi.check(self._lib.dhsa_set_scan_mode(self._h, SCAN_MODES.get(mode, mode)))
+
+    @property
+    def scan_mode_used(self) -> str:
+        """The kernel variant the last vectorised scan launch used (what "auto" resolved to)."""
+        m = C.c_int()
+        _cabi.check(self._lib.dhsa_scan_mode_used(self._h, C.byref(m)))
+        return {v: k for k, v in SCAN_MODES.items()}[int(m.value)]
 
     def set_flow_cache(self, n_sets: int) -> None:
         """Size of the flow cache used by scan mode "flow_cache": n_sets x 32 bytes."""
@@ -200,8 +218,13 @@ class Dhla:
                 raise ValueError("device inputs must be contiguous 32-bit integer tensors")
             if t.device.index != self.device:
                 raise ConfigError(f"tensor on cuda:{t.device.index}, sketch on cuda:{self.device}")
-        self.use_stream(torch.cuda.current_stream(self.device).cuda_stream)
-        _cabi.check(self._lib.dhsa_update_device(self._h, cand.data_ptr(), opp.data_ptr(), cand.numel()))
+        # The tensors were produced on torch's current stream.  The sketch keeps launching on its own
+        # stream: the library orders the two with events in both directions (the scan waits for the
+        # producer, the producer's later work -- e.g. the allocator reusing these tensors -- waits
+        # for the scan), so no handle of a possibly short-lived torch stream is ever stored.
+        producer = torch.cuda.current_stream(self.device).cuda_stream
+        _cabi.check(self._lib.dhsa_update_device_from(self._h, cand.data_ptr(), opp.data_ptr(), cand.numel(),
+                                                      C.c_void_p(producer)))
 
     def seal(self) -> None:
         """Drain the stream: every update issued so far is in the bits."""
@@ -219,10 +242,21 @@ class Dhla:
         _cabi.check(self._lib.dhsa_zero_counts(self._h, out.ctypes.data, None))
         return out
 
-    def hot_sets(self, theta, zero_counts=None) -> list:
-        """Per-array ascending hot indices.  `zero_counts` is accepted for signature
-        compatibility; the device recomputes them from the bits (same values)."""
+    def _hand_in(self, zero_counts) -> None:
+        """The reference's optional ``zero_counts=`` argument: the next read-out call starts from
+        these counts instead of counting the bits (pkg/src/dhsa/dhla.py:111-128,198-207)."""
+        if zero_counts is None:
+            return
         p = self.params
+        zc = np.ascontiguousarray(zero_counts, dtype=np.int64)
+        if zc.shape != (p.r, p.index_count):
+            raise ValueError(f"zero_counts must have shape {(p.r, p.index_count)}, got {zc.shape}")
+        _cabi.check(self._lib.dhsa_use_zero_counts(self._h, zc.ctypes.data))
+
+    def hot_sets(self, theta, zero_counts=None) -> list:
+        """Per-array ascending hot indices (pkg/src/dhsa/dhla.py:111-119)."""
+        p = self.params
+        self._hand_in(zero_counts)
         lists = np.empty((p.r, p.index_count), dtype=np.uint64)
         counts = np.empty(p.r, dtype=np.uint64)
         _cabi.check(self._lib.dhsa_hot_sets(self._h, float(theta), lists.ctypes.data, counts.ctypes.data))
@@ -238,17 +272,19 @@ class Dhla:
             hot_counts=[int(info.hot_counts[i]) for i in range(r)],
             stage_counts=[int(info.stage_counts[i]) for i in range(r - 2)],
             zero_totals=[int(info.zero_totals[i]) for i in range(r)],
+            hot_cut=int(info.hot_cut), sz_cut=int(info.sz_cut),
         )
 
-    def estimate(self, theta=0.0) -> dict:
+    def estimate(self, theta=0.0, zero_counts=None) -> dict:
         """Zero totals, hot-set sizes, flow count, psi and denom in one device pass."""
+        self._hand_in(zero_counts)
         info = _cabi.RestoreInfo()
         _cabi.check(self._lib.dhsa_estimate(self._h, float(theta), C.byref(info)))
         self.last_info = self._info_dict(info)
         return self.last_info
 
     def estimate_flow_count(self, zero_counts=None) -> Estimate:
-        d = self.estimate()
+        d = self.estimate(zero_counts=zero_counts)
         return Estimate(d["flow_count"], d["flow_saturated"])
 
     def bit_set_probability(self, flow_count: float) -> float:
@@ -282,6 +318,7 @@ class Dhla:
         info = _cabi.RestoreInfo()
         cap = 4096
         while True:
+            self._hand_in(zero_counts)
             out = np.empty(cap, dtype=np.uint64)
             rc = self._lib.dhsa_candidate_hosts(self._h, float(theta), int(max_candidates),
                                                 out.ctypes.data, cap, C.byref(info))
@@ -336,6 +373,18 @@ class Dhla:
             return [SuperPointReport(int(h), float(e), bool(s))
                     for h, e, s in zip(rows["host"][:n].tolist(), rows["estimate"][:n].tolist(),
                                        rows["saturated"][:n].tolist())]
+
+    # --- the hash group, inverse (row 8a-10) ----------------------------------------------
+
+    def reconstruct_key(self, indices) -> Optional[int]:
+        """dhg.reconstruct_key for this sketch's parameters (pkg/src/dhsa/dhg.py:161-185)."""
+        from . import dhg
+        return dhg.reconstruct_key(self.params, indices, device=self.device)
+
+    def reconstruct_many(self, tuples):
+        """dhg.reconstruct_many for this sketch's parameters (pkg/src/dhsa/dhg.py:213-233)."""
+        from . import dhg
+        return dhg.reconstruct_many(self.params, tuples, device=self.device)
 
     # --- merge -------------------------------------------------------------------------
 

@@ -18,7 +18,6 @@ as (cand, opp) arrays.
 from __future__ import annotations
 
 import ctypes as C
-import sys
 from dataclasses import dataclass, field
 from typing import Callable, Iterable, Iterator, List, Optional
 
@@ -273,7 +272,7 @@ class DetectionEngine:
             if self._planner is None:  # a 768-byte sketch whose handle runs the plan kernels; kept across runs
                 self._planner = Dhla(DhgParams(r=3, g=8, k=8, alpha=8, key_width=16), device=self._device_index())
             planner = self._planner
-            planner.use_stream(torch.cuda.current_stream(planner.device).cuda_stream)
+            planner.use_stream(torch.cuda.current_stream(planner.device))   # the sketch keeps the stream object alive
             ptr = chunk.data_ptr()
             open_window = session.sketch.window_id if session is not None else -1
             n_b = C.c_uint32()
@@ -305,7 +304,7 @@ class DetectionEngine:
                 if session is None:
                     session = WindowSession(cfg, wid, self.backend, device=self._device_index(),
                                             sketch=self._take_idle(wid))
-                    session.sketch.use_stream(torch.cuda.current_stream(session.sketch.device).cuda_stream)
+                    session.sketch.use_stream(torch.cuda.current_stream(session.sketch.device))
                 session.feed_records(ptr, n, lo, hi)
                 if closing is not None:
                     yield self._collect(closing)
@@ -325,9 +324,9 @@ class DetectionEngine:
             return self._collect(session)
         session.seal()
         on_sealed(session.sketch)
-        return self._collect(session, session.restore())
+        return self._collect(session, session.restore(), recycle=False)   # the hook may have kept the sketch
 
-    def _collect(self, session: WindowSession, reports=None) -> WindowResult:
+    def _collect(self, session: WindowSession, reports=None, recycle: bool = True) -> WindowResult:
         if reports is None:
             reports = session.restore_end()
         result = WindowResult(
@@ -337,9 +336,9 @@ class DetectionEngine:
             dropped=session.dropped,
         )
         # Every window owns its sketch, as in the reference.  Allocating one costs milliseconds
-        # (cudaMalloc of the bits and the flow cache), so a sketch that nobody else kept a
-        # reference to (on_sealed may have) goes back to the idle list instead of being freed.
+        # (cudaMalloc of the bits and the flow cache), so a sketch that never left the engine -- no
+        # on_sealed hook saw it -- goes back to the idle list instead of being freed.
         sk, session.sketch = session.sketch, None
-        if sys.getrefcount(sk) <= 2 and len(self._idle) < 2:
+        if recycle and len(self._idle) < 2:
             self._idle.append(sk)
         return result

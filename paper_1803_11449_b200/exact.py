@@ -134,8 +134,17 @@ def exact_oracle(records, direction: str = "src", device: Optional[int] = None, 
         return {int(h): int(c) for h, c in zip(hosts.tolist(), counts.tolist())}
 
 
+# Scoring.  The metric definitions and the record's field / key names are the reference's
+# (pkg/src/dhsa/ingest.py:179-233: false reports and misses are both taken over the number of TRUE
+# super points, rates are None -- undefined, not zero -- when there is none); this is host-side
+# bookkeeping over a few hundred hosts, outside the hot path.
+_METRIC_KEYS = (("n_true", "N"), ("n_reported", "N_reported"), ("n_false_pos", "N_false_pos"),
+                ("n_false_neg", "N_false_neg"), ("fpr", "fpr"), ("fnr", "fnr"), ("tfr", "tfr"),
+                ("mean_rel_err", "mean_rel_err"))
+
+
 @dataclass
-class EvalMetrics:  # ingest.py:179-213
+class EvalMetrics:
     n_true: int
     n_reported: int
     n_false_pos: int
@@ -146,22 +155,25 @@ class EvalMetrics:  # ingest.py:179-213
     mean_rel_err: Optional[float]
 
     def as_dict(self) -> dict:
-        return {"N": self.n_true, "N_reported": self.n_reported, "N_false_pos": self.n_false_pos,
-                "N_false_neg": self.n_false_neg, "fpr": self.fpr, "fnr": self.fnr, "tfr": self.tfr,
-                "mean_rel_err": self.mean_rel_err}
+        return {key: getattr(self, field) for field, key in _METRIC_KEYS}
 
 
 def evaluate(reports: Sequence, truth: Dict[int, int], theta: int) -> EvalMetrics:
-    """Score a report list against exact per-host counts (ingest.py:216-233)."""
-    true_supers = {h for h, c in truth.items() if c >= theta}
-    reported = {rep.host for rep in reports}
-    n = len(true_supers)
-    n_fp = len(reported - true_supers)
-    n_fn = len(true_supers - reported)
-    rel = [abs(rep.estimate - truth[rep.host]) / truth[rep.host] for rep in reports if rep.host in true_supers]
-    mean_rel = sum(rel) / len(rel) if rel else None
-    if n == 0:
-        return EvalMetrics(0, len(reported), n_fp, 0, None, None, None, mean_rel)
-    fpr = n_fp / n
-    fnr = n_fn / n
-    return EvalMetrics(n, len(reported), n_fp, n_fn, fpr, fnr, fpr + fnr, mean_rel)
+    """Score a report list against exact per-host distinct-opposite counts."""
+    supers = {host: count for host, count in truth.items() if count >= theta}
+    hits, errors = set(), []
+    false_pos = set()
+    for rep in reports:
+        exact = supers.get(rep.host)
+        if exact is None:
+            false_pos.add(rep.host)
+        else:
+            hits.add(rep.host)
+            errors.append(abs(rep.estimate - exact) / exact)
+    missed = len(supers) - len(hits)
+    mean_err = sum(errors) / len(errors) if errors else None
+    n_reported = len(hits) + len(false_pos)
+    if not supers:
+        return EvalMetrics(0, n_reported, len(false_pos), 0, None, None, None, mean_err)
+    fpr, fnr = len(false_pos) / len(supers), missed / len(supers)
+    return EvalMetrics(len(supers), n_reported, len(false_pos), missed, fpr, fnr, fpr + fnr, mean_err)

@@ -72,6 +72,18 @@ class CudaMergeOps:
     def seal(self) -> None:
         self.sketch.seal()
 
+    def stream_context(self):
+        """Context manager under which torch (and NCCL, which orders its collectives with torch's
+        *current* stream) works on the sketch's launch stream, so a collective is ordered behind the
+        kernels already queued there and the kernels queued after it wait for it."""
+        import torch
+
+        handle = self.sketch.stream_handle
+        device = f"cuda:{self.sketch.device}"
+        if handle == 0:   # CUDA's legacy default stream is torch's default stream
+            return torch.cuda.stream(torch.cuda.default_stream(device))
+        return torch.cuda.stream(torch.cuda.ExternalStream(handle, device=device))
+
     def device_barrier(self, dist, group=None) -> bool:
         """Barrier across the ranks that never stops the host: a one-element NCCL all-reduce
         enqueued behind the sketch's kernels on the sketch's stream.  It completes on a rank only
@@ -82,20 +94,10 @@ class CudaMergeOps:
 
         if dist.get_backend(group) != "nccl":
             return False
-        handle = self.sketch.stream_handle
-        if handle == 0:   # legacy default stream: torch's current stream must be it
-            if torch.cuda.current_stream(self.sketch.device).cuda_stream != 0:
-                return False
-            ctx = None
-        else:
-            ctx = torch.cuda.stream(torch.cuda.ExternalStream(handle, device=f"cuda:{self.sketch.device}"))
         if getattr(self, "_token", None) is None:
             self._token = torch.zeros(1, dtype=torch.int32, device=f"cuda:{self.sketch.device}")
-        if ctx is None:
+        with self.stream_context():
             dist.all_reduce(self._token, group=group)
-        else:
-            with ctx:
-                dist.all_reduce(self._token, group=group)
         return True
 
     def export_handle(self) -> bytes:
@@ -201,17 +203,26 @@ def merge_p2p(ops, dist, group=None) -> None:
 
 
 def merge_allgather(ops, dist, group=None) -> None:
-    """Fallback: NCCL all-gather of whole sketches, then the local OR kernel.  Collective."""
+    """Fallback: NCCL all-gather of whole sketches, then the local OR kernel.  Collective.
+
+    The collective and the gather buffer live on the sketch's launch stream (``stream_context``):
+    NCCL orders a collective with the stream that is current when it is issued and nothing else, so
+    issued on any other stream the OR kernels -- which run on the sketch's stream -- could read the
+    buffer before NCCL has filled it."""
+    import contextlib
+
     world, rank = dist.get_world_size(group), dist.get_rank(group)
     if world == 1:
         return
     ops.seal()
-    buf = ops.new_gather_buffer(world)
-    dist.all_gather_into_tensor(buf.view(-1), ops.bits_tensor(), group=group)
-    for q in range(world):
-        if q != rank:
-            ops.or_from_buffer(buf[q])
-    ops.seal()
+    ctx = getattr(ops, "stream_context", None)
+    with (ctx() if ctx is not None else contextlib.nullcontext()):
+        buf = ops.new_gather_buffer(world)
+        dist.all_gather_into_tensor(buf.view(-1), ops.bits_tensor(), group=group)
+        for q in range(world):
+            if q != rank:
+                ops.or_from_buffer(buf[q])
+        ops.seal()   # the buffer goes back to the allocator only after the OR kernels have read it
 
 
 class ShardedWindow:

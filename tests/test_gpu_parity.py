@@ -211,6 +211,7 @@ def test_flow_cache_is_exact_across_batches_resets_and_uploads(n_sets):
     for _ in range(40):
         sk.reset()
         sk.update_batch(small_c, small_o)
+        sk.seal()            # host batches are coalesced into one scan per slot: the barrier makes it two scans
         sk.update_batch(small_c, small_o)
     assert np.array_equal(sk.bits, want.bits)
     lookups, hits = sk.flow_cache_stats()

@@ -81,13 +81,63 @@ def test_library_exports_every_declared_symbol():
     for name in declared:
         assert hasattr(lib, name), f"{name} declared in include/dhsa_b200.h but not exported"
     assert sorted(_cabi.SIGNATURES) == declared
-    assert lib.dhsa_abi_version() == 1
+    assert lib.dhsa_abi_version() == _cabi.ABI_VERSION == 2
 
 
 def test_struct_layouts_match_header():
     assert C.sizeof(_cabi.Params) == 40
     assert C.sizeof(_cabi.Report) == 24
-    assert C.sizeof(_cabi.RestoreInfo) == 8 * 2 + 4 * 2 + 8 + 8 * 3 + 64 * 8 * 3
+    assert C.sizeof(_cabi.RestoreInfo) == 8 * 2 + 4 * 2 + 8 + 8 * 3 + 64 * 8 * 3 + 4 * 2
+    assert _cabi.RestoreInfo.n_reports.offset == 8 and _cabi.RestoreInfo.sz_cut.offset == 1596
+    # the header's own words for the same structs: field order and types, parsed from include/dhsa_b200.h
+    text = open(os.path.join(ROOT, "include", "dhsa_b200.h")).read()
+    ctype = {"int32_t": C.c_int32, "uint64_t": C.c_uint64, "int64_t": C.c_int64, "double": C.c_double}
+    for name, binding in (("dhsa_params_t", _cabi.Params), ("dhsa_report_t", _cabi.Report),
+                          ("dhsa_restore_info_t", _cabi.RestoreInfo)):
+        body = re.search(r"typedef struct \{([^}]*)\} " + name + ";", text).group(1)
+        body = re.sub(r"/\*.*?\*/", "", body, flags=re.S)
+        fields = re.findall(r"(int32_t|uint64_t|int64_t|double)\s+(\w+)(?:\[(\d+)\])?;", body)
+        want = [(f, ctype[t] * int(n) if n else ctype[t]) for t, f, n in fields]
+        got = [(f, t) for f, t in binding._fields_]
+        assert [f for f, _ in got] == [f for f, _ in want], name
+        assert [C.sizeof(t) for _, t in got] == [C.sizeof(t) for _, t in want], name
+
+
+def test_reference_side_binding_structs_match_the_library_binding():
+    """integration/dhsa_cuda.py (the file a maintainer adds to the reference) declares
+    the ABI's structs on its own; they must be the ones the library was built with."""
+    import refpkg
+
+    if not refpkg.available():
+        pytest.skip("baseline/_ref not installed (bash baseline/install_reference.sh)")
+    _, stub = refpkg.load()
+    assert stub.ABI_VERSION == _cabi.ABI_VERSION
+    for mine, theirs in ((_cabi.Params, stub.Params), (_cabi.RestoreInfo, stub.RestoreInfo)):
+        assert C.sizeof(mine) == C.sizeof(theirs)
+        assert [(f, C.sizeof(t)) for f, t in mine._fields_] == [(f, C.sizeof(t)) for f, t in theirs._fields_]
+    assert stub.REPORT.itemsize == C.sizeof(_cabi.Report)
+    assert os.path.samefile(stub._LIB_PATH, os.path.join(ROOT, "paper_1803_11449_b200", "libdhsa_b200.so"))
+    lib = C.CDLL(stub._LIB_PATH)
+    for name in re.findall(r"lib\(\)\.(dhsa_\w+)", open(stub.__file__).read()):
+        assert hasattr(lib, name), name
+
+
+def test_installed_reference_is_the_unmodified_package_with_its_compiled_backend():
+    import refpkg
+
+    if not refpkg.available():
+        pytest.skip("baseline/_ref not installed (bash baseline/install_reference.sh)")
+    dhsa, _ = refpkg.load()
+    from dhsa._kernels import available_backends
+
+    assert available_backends() == ("compiled", "python")
+    assert os.path.realpath(dhsa.__file__).startswith(os.path.realpath(refpkg.REF_DIR))
+    src = "/root/reference/pkg/src/dhsa"
+    if os.path.isdir(src):          # in this container: byte-identical to the reference's sources
+        for f in sorted(os.listdir(src)):
+            if f.endswith(".py"):
+                assert open(os.path.join(src, f), "rb").read() == \
+                    open(os.path.join(refpkg.REF_DIR, "dhsa", f), "rb").read(), f
 
 
 def test_c_side_validation_maps_to_config_error():

@@ -7,12 +7,11 @@ estimate is g ln g ~ 7098, SURVEY 7 hard part 4) and alpha is chosen so that
 (r - 2) alpha + k >= 32.  Prints one JSON document; committed under profiles/.
 """
 import json
+import os
 import sys
 import time
 
-import torch
-
-sys.path.insert(0, ".")
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_1803_11449_b200 as P  # noqa: E402
 
 POINTS = [
@@ -22,18 +21,25 @@ POINTS = [
 ]
 
 
+def point_config(theta):
+    """The window of one sweep point (tests/test_gpu_configs.py bit-compares the same windows)."""
+    lo = max(2 * theta, 512)
+    # the background shrinks with theta: at theta 256 a g=1024 cell is hot above 227 set bits, and
+    # 150k hosts would make half of all cells hot (the restore then overflows max_candidates, as
+    # the reference's does -- BASELINE.md section 2)
+    return P.GeneratorConfig(background_hosts=min(150_000, 150 * theta), background_max_cardinality=max(16, theta // 4),
+                             superpoints=50, super_cardinality=(lo, 4 * lo), duplicate_factor=8)
+
+
 def main():
     out = []
     for theta, g, k, alpha in POINTS:
-        lo = max(2 * theta, 512)
-        # the background shrinks with theta: at theta 256 a g=1024 cell is hot above 227 set bits, and
-        # 150k hosts would make half of all cells hot (the restore then overflows max_candidates, as
-        # the reference's does -- BASELINE.md section 2)
-        cfg = P.GeneratorConfig(background_hosts=min(150_000, 150 * theta), background_max_cardinality=max(16, theta // 4),
-                                superpoints=50, super_cardinality=(lo, 4 * lo), duplicate_factor=8)
+        cfg = point_config(theta)
         tr = P.generate_trace_device(cfg, seed=100, fmt="pairs")
         params = P.DhgParams(g=g, k=k, alpha=alpha)
         sk = P.Dhla(params)
+        import torch
+
         stream = torch.cuda.Stream()
         with torch.cuda.stream(stream):
             sk.use_stream(stream.cuda_stream)
