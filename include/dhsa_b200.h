@@ -321,7 +321,9 @@ int dhsa_ipc_close(int device, void *bits_dev);
 /* ---- measurement -------------------------------------------------------------
  * Random-address L2 probe used for the scan roofline: `ops` 32-bit operations at
  * hashed word addresses inside a `buffer_bytes` buffer.  kind 0 = atomic OR
- * (RED), 1 = load.  Returns the rate in operations per second. */
+ * (RED), 1 = load, 2 = four loads + one RED per `ops` count of four (do loads and REDs
+ * share a limit?), 3 = 256-bit load of a whole 32-byte sector (the flow-cache lookup's
+ * shape).  Returns the rate in operations per second. */
 int dhsa_probe_l2(int device, int kind, uint64_t buffer_bytes, uint64_t ops, double *ops_per_sec);
 
 #ifdef __cplusplus

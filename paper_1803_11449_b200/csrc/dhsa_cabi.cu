@@ -61,7 +61,7 @@ static int cuda_fail(cudaError_t e, const char *what)
 #define DHSA_READOUT_CTAS_PER_SM 4   // grid of the stage / verify / re-estimate kernels (grid-stride loops)
 #endif
 static const uint64_t kCounterBytes = 256;   // device counters kept behind the bit array
-static const uint64_t kPinnedReports = 256;
+static const uint64_t kPinnedReports = DHSA_HEAD_ROWS;  // report rows that come back with the control block
 static const uint32_t kPinnedBoundaries = 64;  // report rows copied back inside the read-out graph
 static const int kStageBufs = 3;            // staging buffers of the host-input pipeline
 static const uint64_t kStagePackets = 1ull << 22;  // packets per staged chunk (16 MiB per array)
@@ -114,8 +114,9 @@ struct dhsa_sketch {
     bool regime_few_keys;          // auto mode: the traffic's keys sit in a handful of hot words (see the auto policy)
 
     // read-out workspaces
-    Control *ctl;           // device
-    Control *ctl_host;      // pinned mirror
+    Readback *rb, *rb_host;  // control block + window counters + first report rows: device, and its pinned mirror
+    Control *ctl;           // = &rb->c
+    Control *ctl_host;      // = &rb_host->c
     int32_t *zc;            // ncell
     bool zc_given;          // s->zc holds counts handed in by the caller for the next read-out call
     uint32_t *lists;        // r * 2^k
@@ -149,7 +150,6 @@ struct dhsa_sketch {
     uint64_t restore_max_candidates;
     double restore_theta;
     uint64_t restore_seq;           // mutation_seq when the pending read-out was queued
-    int restore_last_buf;           // ping-pong buffer holding the last stage's partial keys
 
     // record streams
     unsigned long long *tally;      // device: records fed, records dropped
@@ -301,18 +301,20 @@ static int create_locked(dhsa_sketch *s, const dhsa_params_t *params, int device
     CU(cudaStreamCreateWithFlags(&s->own_stream, cudaStreamNonBlocking));
     CU(cudaStreamCreateWithFlags(&s->copy_stream, cudaStreamNonBlocking));
     s->stream = s->own_stream;
-    CU(cudaMalloc(&s->ctl, sizeof(Control)));
+    CU(cudaMalloc(&s->rb, sizeof(Readback)));
+    s->ctl = &s->rb->c;
     s->tally = reinterpret_cast<unsigned long long *>(s->bits + s->alloc_bytes);
     s->fc_stats = s->tally + 2;
-    CU(cudaMallocHost(&s->ctl_host, sizeof(Control)));
-    CU(cudaMallocHost(&s->reports_pinned, kPinnedReports * sizeof(ReportOut)));
+    CU(cudaMallocHost(&s->rb_host, sizeof(Readback)));
+    memset(s->rb_host, 0, sizeof(Readback));
+    s->ctl_host = &s->rb_host->c;
+    s->reports_pinned = s->rb_host->head;
+    s->tally_pinned = s->rb_host->c.counters;
     CU(cudaEventCreateWithFlags(&s->restore_ev, cudaEventDisableTiming));
     CU(cudaEventCreateWithFlags(&s->bridge_ev, cudaEventDisableTiming));
-    CU(cudaMallocHost(&s->tally_pinned, 6 * sizeof(unsigned long long)));
-    memset(s->tally_pinned, 0, 6 * sizeof(unsigned long long));
     s->graph_disabled = getenv("DHSA_NO_GRAPH") != nullptr;
     CU(cudaMemsetAsync(s->bits, 0, s->alloc_bytes + kCounterBytes, s->stream));
-    CU(cudaMemsetAsync(s->ctl, 0, sizeof(Control), s->stream));
+    CU(cudaMemsetAsync(s->rb, 0, sizeof(Readback), s->stream));
     CU(cudaStreamSynchronize(s->stream));
     CU(cudaFuncSetAttribute(k_sort_small, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             DHSA_SORT_SMEM_MAX * (int)sizeof(uint64_t)));
@@ -514,13 +516,11 @@ static int destroy_for_real(dhsa_sketch *s)
         cudaFreeHost(s->fc_stats_host);
         cudaEventDestroy(s->fc_stats_ev);
     }
-    cudaFree(s->ctl);
-    if (s->ctl_host) cudaFreeHost(s->ctl_host);
-    if (s->reports_pinned) cudaFreeHost(s->reports_pinned);
+    cudaFree(s->rb);
+    if (s->rb_host) cudaFreeHost(s->rb_host);
     if (s->host_tmp) cudaFreeHost(s->host_tmp);
     if (s->restore_ev) cudaEventDestroy(s->restore_ev);
     if (s->bridge_ev) cudaEventDestroy(s->bridge_ev);
-    if (s->tally_pinned) cudaFreeHost(s->tally_pinned);
     if (s->restore_graph) cudaGraphExecDestroy(s->restore_graph);
     if (s->own_stream) cudaStreamDestroy(s->own_stream);
     if (s->copy_stream) cudaStreamDestroy(s->copy_stream);
@@ -984,55 +984,51 @@ extern "C" int dhsa_record_tally_at_restore(dhsa_sketch_t *s, uint64_t *records_
 // a caller that finds the pool busy with another caller's job simply copies alone.
 class CopyPool {
 public:
-    struct Piece {
-        void *dst;
-        const void *src;
-        size_t bytes;
-    };
     static CopyPool &get()
     {
         static CopyPool *pool = new CopyPool();  // leaked on purpose: no destructor races at exit
         return *pool;
     }
-    // dst <- src for both arrays, split into pieces over the pool and the calling thread;
-    // returns when every byte is copied
+    // dst <- src for both arrays, split into one share per thread (helpers + the caller); returns
+    // when every byte is copied.  The two arrays are treated as one run of 2 * bytes_each bytes.
     void copy2(void *d0, const void *s0, void *d1, const void *s1, size_t bytes_each)
     {
-        const size_t kPiece = 32u << 10;  // 16 pieces for a 65,536-pair batch: late helpers still find work
-        const size_t per_array = (bytes_each + kPiece - 1) / kPiece;
-        if (n_helpers_ == 0 || per_array * 2 < 4 || !job_mu_.try_lock()) {
+        const size_t total = 2 * bytes_each;
+        if (n_helpers_ == 0 || total < (128u << 10) || !job_mu_.try_lock()) {
             memcpy(d0, s0, bytes_each);
             memcpy(d1, s1, bytes_each);
             return;
         }
-        // at most kMaxPieces pieces: larger pieces for larger jobs
-        size_t piece = kPiece;
-        while ((bytes_each + piece - 1) / piece * 2 > kMaxPieces) piece <<= 1;
-        uint32_t n = 0;
-        for (int a = 0; a < 2; a++) {
-            char *d = (char *)(a ? d1 : d0);
-            const char *src = (const char *)(a ? s1 : s0);
-            for (size_t lo = 0; lo < bytes_each; lo += piece)
-                pieces_[n++] = Piece{d + lo, src + lo, bytes_each - lo < piece ? bytes_each - lo : piece};
-        }
-        n_pieces_.store(n, std::memory_order_relaxed);
+        uint32_t shares = n_helpers_ + 1;
+        size_t per = ((total + shares - 1) / shares + 4095) & ~(size_t)4095;  // page-sized steps
+        if (per < (32u << 10)) per = 32u << 10;
+        shares = (uint32_t)((total + per - 1) / per);
+        job_ = Job{(char *)d0, (const char *)s0, (char *)d1, (const char *)s1, bytes_each, per, shares};
         done_.store(0, std::memory_order_relaxed);
-        const uint64_t gen = (ticket_.load(std::memory_order_relaxed) >> 32) + 1;
-        ticket_.store(gen << 32, std::memory_order_release);  // publishes pieces_ / n_pieces_
+        const uint64_t gen = gen_.load(std::memory_order_relaxed) + 1;
+        gen_.store(gen, std::memory_order_release);  // publishes job_
         if (sleepers_.load(std::memory_order_acquire) > 0) {
             { std::lock_guard<std::mutex> lk(cv_mu_); }
             cv_.notify_all();
         }
-        work(gen);
-        while (done_.load(std::memory_order_acquire) != n) cpu_relax();
-        // close the job: a helper that still holds an old ticket value can no longer claim a piece
-        // index once pieces_ is rewritten for the next job (its compare-exchange fails)
-        ticket_.store((gen << 32) | 0xFFFFFFFFull, std::memory_order_release);
+        work(gen, shares - 1);  // the caller starts from the last share, helper i from share i
+        while (done_.load(std::memory_order_acquire) != shares) cpu_relax();
         job_mu_.unlock();
     }
 
 private:
-    static const uint32_t kMaxPieces = 256;
+    static const uint32_t kMaxShares = 65;
+    struct Job {
+        char *d0;
+        const char *s0;
+        char *d1;
+        const char *s1;
+        size_t bytes_each, per;
+        uint32_t shares;
+    };
+    struct alignas(64) Claim {
+        std::atomic<uint64_t> gen{0};  // generation of the job this share was last claimed in
+    };
     static void cpu_relax()
     {
 #if defined(__x86_64__) || defined(__i386__)
@@ -1041,17 +1037,37 @@ private:
         std::this_thread::yield();
 #endif
     }
-    // take pieces of job `gen` until none is left (or the job is over)
-    void work(uint64_t gen)
+    // Claim shares of job `gen`, starting at `first`: one compare-exchange per share, on its own cache
+    // line.  Generations only grow, and a share is claimable only while its mark is OLDER than `gen`:
+    // a helper that wakes up late, after its job is over, finds every mark >= its generation and
+    // leaves -- so job_ is only ever read by threads the waiting caller still counts.
+    void work(uint64_t gen, uint32_t first)
     {
-        for (;;) {
-            uint64_t t = ticket_.load(std::memory_order_acquire);
-            if ((t >> 32) != gen) return;
-            const uint32_t idx = (uint32_t)t;
-            if (idx >= n_pieces_.load(std::memory_order_relaxed)) return;
-            if (!ticket_.compare_exchange_weak(t, t + 1, std::memory_order_acq_rel)) continue;
-            const Piece pc = pieces_[idx];
-            memcpy(pc.dst, pc.src, pc.bytes);
+        const uint32_t shares = job_.shares;
+        for (uint32_t k = 0; k < shares; k++) {
+            const uint32_t i = (first + k) % shares;
+            uint64_t seen = claims_[i].gen.load(std::memory_order_acquire);
+            if (seen >= gen) {
+                if (seen > gen) return;  // a newer job owns the table
+                continue;
+            }
+            if (!claims_[i].gen.compare_exchange_strong(seen, gen, std::memory_order_acq_rel)) {
+                if (seen > gen) return;
+                continue;
+            }
+            // Shares beyond the previous job's count can carry marks older than a late helper's own
+            // generation: a claim only counts while `gen` is still the current job.  If it is, the job
+            // cannot end before this share is done (nobody else can claim it), so job_ is stable below.
+            if (gen_.load(std::memory_order_acquire) != gen) return;
+            const Job j = job_;
+            if (i >= j.shares) continue;
+            size_t lo = (size_t)i * j.per, hi = lo + j.per < 2 * j.bytes_each ? lo + j.per : 2 * j.bytes_each;
+            if (lo < j.bytes_each) {
+                const size_t end = hi < j.bytes_each ? hi : j.bytes_each;
+                memcpy(j.d0 + lo, j.s0 + lo, end - lo);
+                lo = end;
+            }
+            if (hi > lo) memcpy(j.d1 + (lo - j.bytes_each), j.s1 + (lo - j.bytes_each), hi - lo);
             done_.fetch_add(1, std::memory_order_acq_rel);
         }
     }
@@ -1062,23 +1078,23 @@ private:
         unsigned n = hw > 4 ? (hw - 2 < 6 ? hw - 2 : 6) : (hw > 1 ? hw - 1 : 0);
         if (const char *env = getenv("DHSA_COPY_THREADS")) {
             const long v = strtol(env, nullptr, 10);
-            if (v >= 0 && v <= 64) n = (unsigned)v;
+            if (v >= 0 && v < (long)kMaxShares) n = (unsigned)v;
         }
         n_helpers_ = n;
         for (unsigned i = 0; i < n; i++) {
-            std::thread th([this] { run(); });
+            std::thread th([this, i] { run(i); });
             th.detach();
         }
     }
-    void run()
+    void run(uint32_t id)
     {
         uint64_t seen = 0;
         auto last = std::chrono::steady_clock::now();
         for (;;) {
-            const uint64_t gen = ticket_.load(std::memory_order_acquire) >> 32;
+            const uint64_t gen = gen_.load(std::memory_order_acquire);
             if (gen != seen) {
                 seen = gen;
-                work(gen);
+                work(gen, id);
                 last = std::chrono::steady_clock::now();
                 continue;
             }
@@ -1088,14 +1104,14 @@ private:
             }
             std::unique_lock<std::mutex> lk(cv_mu_);
             sleepers_.fetch_add(1, std::memory_order_acq_rel);
-            cv_.wait(lk, [&] { return (ticket_.load(std::memory_order_acquire) >> 32) != seen; });
+            cv_.wait(lk, [&] { return gen_.load(std::memory_order_acquire) != seen; });
             sleepers_.fetch_sub(1, std::memory_order_acq_rel);
         }
     }
-    std::mutex job_mu_;  // one job at a time
-    Piece pieces_[kMaxPieces];
-    std::atomic<uint32_t> n_pieces_{0};
-    std::atomic<uint64_t> ticket_{0};  // job generation << 32 | next piece
+    std::mutex job_mu_;  // one job at a time; a caller that finds it taken copies alone
+    Job job_{};
+    Claim claims_[kMaxShares];
+    std::atomic<uint64_t> gen_{0};
     std::atomic<uint32_t> done_{0};
     std::atomic<int> sleepers_{0};
     std::mutex cv_mu_;
@@ -1983,7 +1999,7 @@ extern "C" int dhsa_candidate_hosts(dhsa_sketch_t *s, double theta, uint64_t max
         if (int rc = launch_estimate(s, theta)) return rc;
         if (int rc = launch_restore_stages(s, max_candidates, true, nullptr)) return rc;
         k_sort_small<<<1, 1024, DHSA_SORT_SMEM_MAX * sizeof(uint64_t), s->stream>>>(s->keys, &s->ctl->n_candidates, s->ctl,
-                                                                                     nullptr, 0);
+                                                                                     nullptr, 0, nullptr, nullptr);
         s->launches++;
         CU(cudaGetLastError());
         if (int rc = read_control(s)) return rc;
@@ -2050,21 +2066,18 @@ static int enqueue_restore(dhsa_sketch *s, double theta, uint64_t max_candidates
     if (int rc = launch_estimate(s, theta)) return rc;
     int cur = 0;
     if (int rc = launch_restore_stages(s, max_candidates, false, &cur)) return rc;
-    s->restore_last_buf = cur;
     const int grid = s->sm_count * DHSA_READOUT_CTAS_PER_SM;
     // verify + re-estimate, then sort + emit: two launches for what were four
     k_verify_reestimate<<<grid, 256, 0, s->stream>>>(s->params.r - 2, s->dp, buffer_cap(s, max_candidates), max_candidates,
                                                      s->sub[cur], s->cl0[cur], s->bits, s->keys, s->cand_sz, s->packed,
                                                      s->ctl);
-    k_sort_small<<<1, 1024, DHSA_SORT_SMEM_MAX * sizeof(uint64_t), s->stream>>>(s->packed, &s->ctl->n_reports, s->ctl,
-                                                                                 s->reports, s->params.g);
+    // sort + emit; as the last kernel it also gathers the window counters (6 words behind the bit array) and
+    // the first report rows behind the control block: ONE copy brings everything the host reads back
+    k_sort_small<<<1, 1024, DHSA_SORT_SMEM_MAX * sizeof(uint64_t), s->stream>>>(
+        s->packed, &s->ctl->n_reports, s->ctl, s->reports, s->params.g, s->tally, s->rb->head);
     s->launches += 2;
     CU(cudaGetLastError());
-    CU(cudaMemcpyAsync(s->ctl_host, s->ctl, sizeof(Control), cudaMemcpyDeviceToHost, s->stream));
-    const uint64_t rows = s->cand_cap < kPinnedReports ? s->cand_cap : kPinnedReports;
-    CU(cudaMemcpyAsync(s->reports_pinned, s->reports, rows * sizeof(ReportOut), cudaMemcpyDeviceToHost, s->stream));
-    // record tally + the scan kernels' counters (6 words behind the bit array) as they stand at this read-out
-    CU(cudaMemcpyAsync(s->tally_pinned, s->tally, 6 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s->stream));
+    CU(cudaMemcpyAsync(s->rb_host, s->rb, sizeof(Readback), cudaMemcpyDeviceToHost, s->stream));
     return DHSA_OK;
 }
 
@@ -2154,13 +2167,13 @@ static int refilter_with_host_cut(dhsa_sketch *s, const HostScalars &h)
     CU(cudaMemcpyAsync(s->ctl, c, sizeof(Control), cudaMemcpyHostToDevice, s->stream));
     const int grid = s->sm_count * DHSA_READOUT_CTAS_PER_SM;
     k_refilter<<<grid, 256, 0, s->stream>>>(s->keys, s->cand_sz, h.sz_cut, s->packed, s->ctl);
-    k_sort_small<<<1, 1024, DHSA_SORT_SMEM_MAX * sizeof(uint64_t), s->stream>>>(s->packed, &s->ctl->n_reports, s->ctl,
-                                                                                 s->reports, s->params.g);
+    k_sort_small<<<1, 1024, DHSA_SORT_SMEM_MAX * sizeof(uint64_t), s->stream>>>(
+        s->packed, &s->ctl->n_reports, s->ctl, s->reports, s->params.g, nullptr, s->rb->head);
     s->launches += 2;
     CU(cudaGetLastError());
-    const uint64_t rows = s->cand_cap < kPinnedReports ? s->cand_cap : kPinnedReports;
-    CU(cudaMemcpyAsync(s->reports_pinned, s->reports, rows * sizeof(ReportOut), cudaMemcpyDeviceToHost, s->stream));
-    return read_control(s);
+    CU(cudaMemcpyAsync(s->rb_host, s->rb, sizeof(Readback), cudaMemcpyDeviceToHost, s->stream));
+    CU(cudaStreamSynchronize(s->stream));
+    return DHSA_OK;
 }
 
 static int restore_end_locked(dhsa_sketch *s, dhsa_report_t *reports_host, uint64_t reports_cap,
@@ -2618,7 +2631,7 @@ extern "C" int dhsa_exact_result(dhsa_exact_t *e, uint64_t min_count, uint64_t *
         CU(cudaFuncSetAttribute(k_sort_small, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 DHSA_SORT_SMEM_MAX * (int)sizeof(uint64_t)));
         k_sort_small<<<1, 1024, DHSA_SORT_SMEM_MAX * sizeof(uint64_t), st>>>(
-            reinterpret_cast<uint64_t *>(e->out), e->n_out, nullptr, nullptr, 0);
+            reinterpret_cast<uint64_t *>(e->out), e->n_out, nullptr, nullptr, 0, nullptr, nullptr);
     } else {
         const uint64_t len = pow2_ge(n);
         const int grid = exact_grid(e, len);
@@ -2686,7 +2699,8 @@ extern "C" int dhsa_generate_trace(int device, const uint32_t *hosts_dev, const 
 extern "C" int dhsa_probe_l2(int device, int kind, uint64_t buffer_bytes, uint64_t ops, double *ops_per_sec)
 {
     NEED(ops_per_sec);
-    if (kind != 0 && kind != 1) return fail(DHSA_ECONFIG, "probe kind must be 0 (atomic OR) or 1 (load)");
+    if (kind < 0 || kind > 3)
+        return fail(DHSA_ECONFIG, "probe kind must be 0 (atomic OR), 1 (load), 2 (4 loads + 1 atomic OR) or 3 (32-byte load)");
     uint64_t nwords = buffer_bytes / 4;
     if (nwords < 1024 || (nwords & (nwords - 1)) || nwords > (1ull << 32))
         return fail(DHSA_ECONFIG, "probe buffer must be a power-of-two number of words in [1024, 2^32]");
@@ -2706,10 +2720,12 @@ extern "C" int dhsa_probe_l2(int device, int kind, uint64_t buffer_bytes, uint64
     float best = 1e30f;
     for (int it = 0; it < 4; it++) {  // first pass warms L2 and the instruction cache
         CU(cudaEventRecord(a, st));
-        if (kind == 0)
-            k_probe_l2<0><<<grid, 256, 0, st>>>(buf, (uint32_t)(nwords - 1), ops, sink);
-        else
-            k_probe_l2<1><<<grid, 256, 0, st>>>(buf, (uint32_t)(nwords - 1), ops, sink);
+        switch (kind) {
+        case 0: k_probe_l2<0><<<grid, 256, 0, st>>>(buf, (uint32_t)(nwords - 1), ops, sink); break;
+        case 1: k_probe_l2<1><<<grid, 256, 0, st>>>(buf, (uint32_t)(nwords - 1), ops, sink); break;
+        case 2: k_probe_l2<2><<<grid, 256, 0, st>>>(buf, (uint32_t)(nwords - 1), ops, sink); break;
+        default: k_probe_l2<3><<<grid, 256, 0, st>>>(buf, (uint32_t)(nwords - 1), ops, sink); break;
+        }
         CU(cudaEventRecord(b, st));
         CU(cudaStreamSynchronize(st));
         CU(cudaGetLastError());

@@ -52,6 +52,8 @@ struct Control {
     int sz_cut;  // report filter as an integer: a candidate passes iff max(SZ, 1) <= sz_cut (see plan_readout)
     double flow_count, psi, denom;
     unsigned long long busy_cells;  // non-empty cells of array 0 = distinct dh0 values seen (the auto policy's signal)
+    unsigned long long counters[6];  // the window's counters as of this read-out: records fed / dropped, flow-cache
+                                     // lookups / hits, test-kernel packets / REDs (copied by the chain's last kernel)
 };
 
 // ------------------------------------------------------------------ hashing --
@@ -557,9 +559,24 @@ __global__ void __launch_bounds__(256) k_scan_vec4(SRC src, uint32_t *__restrict
 #ifndef DHSA_FC_CTAS_PER_SM
 #define DHSA_FC_CTAS_PER_SM 3
 #endif
+#ifndef DHSA_FC_DENSE_MISS
+#define DHSA_FC_DENSE_MISS 1
+#endif
+#if DHSA_FC_DENSE_MISS
+// A queued miss is just the key.  Everything only a miss needs -- the empty-way search, dh0, the R
+// word indices -- happens in the drain, where all 32 lanes hold a miss: in the lookup loop the same
+// code ran under `if (miss)` with one or two active lanes per warp (4% of the packets miss, so three
+// packet slots in four have at least one) and cost a quarter of the kernel's instructions.  The
+// drain re-reads the key's set (one more L2 sector per miss, +3% requests): it needs the ways to
+// pick the slot, and a key another warp recorded in the meantime turns into a hit there.
+struct FcMiss {
+    uint32_t cand, h;
+};
+#else
 struct FcMiss {
     uint32_t cand, h, slot;  // slot = set * 8 + way to fill, or DHSA_FC_NO_SLOT when the set was full
 };
+#endif
 
 // (set, entry) of a key in a table of 2^(32 - shift) sets
 __device__ __forceinline__ void fc_locate(const DevParams &p, uint32_t cand, uint32_t h, uint32_t &set, uint32_t &entry)
@@ -569,15 +586,49 @@ __device__ __forceinline__ void fc_locate(const DevParams &p, uint32_t cand, uin
     entry = (p.fc_epoch << p.fc_tag_bits) | ((a & ((1u << p.fc_shift) - 1u)) << p.log2g) | h;  // epoch >= 1
 }
 
+// The way of set `set_idx` a new key goes to: the first empty way (an entry of another epoch) as
+// loaded, searched from a key-dependent start so that lanes which loaded the same still-empty set do
+// not all pick way 0 and overwrite each other; DHSA_FC_NO_SLOT when the set is full (no eviction:
+// evicting a live key only moves the miss to another key and costs a store; the table empties with
+// every window).  A race only loses an entry.
+__device__ __forceinline__ uint32_t fc_pick_slot(const DevParams &p, const uint32_t (&way)[8], uint32_t set_idx,
+                                                 uint32_t entry)
+{
+    uint32_t empty = 0;
+#pragma unroll
+    for (int t = 0; t < 8; t++) empty |= (uint32_t)((way[t] >> p.fc_tag_bits) != p.fc_epoch) << t;
+    const uint32_t rot = entry & 7u;
+    const uint32_t turned = ((empty >> rot) | (empty << (8u - rot))) & 0xFFu;
+    return turned ? ((set_idx << 3) | (((uint32_t)(__ffs(turned) - 1) + rot) & 7u)) : DHSA_FC_NO_SLOT;
+}
+
 // Drain up to 32 queued misses, one per lane: the R test loads of a lane are in flight
 // together, REDs are warp-aggregated, then the key is recorded in the table.
 template <int R>
 __device__ __forceinline__ void fc_drain32(uint32_t *__restrict__ words, const DevParams &p, int wshift,
                                            const FcMiss *q, uint32_t n_active, uint32_t lane)
 {
-    const bool act = lane < n_active;
+    bool act = lane < n_active;
+#if DHSA_FC_DENSE_MISS
+    FcMiss m = {0u, 0u};
+    if (act) m = q[lane];
+    uint32_t set, entry;
+    fc_locate(p, m.cand, m.h, set, entry);
+    unsigned long long e[4] = {0ull, 0ull, 0ull, 0ull};
+    if (act) ld_fc_set(p.fcache + ((size_t)set << 2), e);
+    uint32_t way[8];
+#pragma unroll
+    for (int t = 0; t < 4; t++) way[2 * t] = (uint32_t)e[t], way[2 * t + 1] = (uint32_t)(e[t] >> 32);
+    bool hit = false;
+#pragma unroll
+    for (int t = 0; t < 8; t++) hit |= way[t] == entry;
+    act = act && !hit;  // recorded by another warp since the lookup: that warp issued its REDs
+    const uint32_t slot = fc_pick_slot(p, way, set, entry);
+#else
     FcMiss m = {0u, 0u, 0u};
     if (act) m = q[lane];
+    const uint32_t slot = m.slot;
+#endif
     const uint32_t d0 = (uint32_t)mix64(p.state_dh0 ^ (uint64_t)m.cand) & p.kmask;
     const uint32_t mask = 1u << (m.h & 31u);
     uint32_t widx[R], w[R];
@@ -586,16 +637,18 @@ __device__ __forceinline__ void fc_drain32(uint32_t *__restrict__ words, const D
     // evicted), so it is almost surely new and its bits still clear: skip the test loads and RED
     // unconditionally (a RED costs ~1.5 loads in L2, a test that finds the bit clear costs both).
     // Keys from full sets are usually repeats whose bits are set: those test first.
-    const bool fresh = DHSA_FC_SKIP_TEST && m.slot != DHSA_FC_NO_SLOT;
+    const bool fresh = DHSA_FC_SKIP_TEST && slot != DHSA_FC_NO_SLOT;
 #pragma unroll
     for (int i = 0; i < R; i++) w[i] = act ? (fresh ? 0u : ld_sketch(words + widx[i])) : 0xFFFFFFFFu;
 #pragma unroll
     for (int i = 0; i < R; i++) red_or_aggregated(words, widx[i], mask, (w[i] & mask) == 0, lane);
     // the key now counts as scanned: its tests/REDs above are issued before this store
-    if (act && m.slot != DHSA_FC_NO_SLOT) {
+    if (act && slot != DHSA_FC_NO_SLOT) {
+#if !DHSA_FC_DENSE_MISS
         uint32_t set, entry;
         fc_locate(p, m.cand, m.h, set, entry);
-        st_fc_way(reinterpret_cast<uint32_t *>(p.fcache) + m.slot, entry);
+#endif
+        st_fc_way(reinterpret_cast<uint32_t *>(p.fcache) + slot, entry);
     }
 }
 
@@ -699,19 +752,11 @@ __global__ void __launch_bounds__(256, DHSA_FC_CTAS_PER_SM) k_scan_flowcache(SRC
             const unsigned bal = __ballot_sync(0xFFFFFFFFu, miss);
             if (bal == 0) continue;
             if (miss) {
-                // record the key in the first empty way of its set as loaded; a full set keeps its
-                // entries (no eviction: evicting a live key only moves the miss to another key and
-                // costs a store; the table empties with every window).  A race only loses an entry.
-                // Lanes that loaded the same (still empty) set at the same time would all pick its
-                // first empty way and overwrite each other: start the search at a key-dependent way.
-                uint32_t empty = 0;
-#pragma unroll
-                for (int t = 0; t < 8; t++) empty |= (uint32_t)((way[t] >> p.fc_tag_bits) != p.fc_epoch) << t;
-                const uint32_t rot = entry[j] & 7u;
-                const uint32_t turned = ((empty >> rot) | (empty << (8u - rot))) & 0xFFu;
-                const uint32_t fill =
-                    turned ? ((set_idx[j] << 3) | ((uint32_t)(__ffs(turned) - 1) + rot) & 7u) : DHSA_FC_NO_SLOT;
-                FcMiss m = {cs[j], hs[j], fill};
+#if DHSA_FC_DENSE_MISS
+                const FcMiss m = {cs[j], hs[j]};
+#else
+                const FcMiss m = {cs[j], hs[j], fc_pick_slot(p, way, set_idx[j], entry[j])};
+#endif
                 q[qn + __popc(bal & lt_mask)] = m;
             }
             qn += __popc(bal);
@@ -971,50 +1016,74 @@ __device__ __forceinline__ double corrected_estimate(int g, int sz_clamped, doub
 
 // The threshold filter `estimate >= theta` (dhla.py:190-194) as an integer cut on the clamped
 // SZ: the estimate is non-increasing in SZ, so the passing values are a prefix [1, sz_cut] of
-// [1, g] (0 = nothing passes).  Found by bisection here so the chain stays on the device; the
+// [1, g] (0 = nothing passes).  Found by a search here so the chain stays on the device; the
 // host re-derives the cut with its own libm from the same zero totals when it collects the
 // read-out (dhsa_cabi.cu: host_scalars) and re-filters in the -- never yet observed -- case that
 // the two disagree, so the decision is the host formula's, not this libm's.
-__device__ __forceinline__ int report_cut(int g, double denom, double theta)
+// Called by one full warp: a 32-ary search (two rounds at g = 1024) instead of a bisection --
+// every probe is a dependent fp64 log, and the read-out chain is latency-bound.
+__device__ __forceinline__ int report_cut(int g, double denom, double theta, uint32_t lane)
 {
-    if (!(corrected_estimate(g, 1, denom) >= theta)) return 0;
-    int lo = 1, hi = g;  // invariant: lo passes
-    if (corrected_estimate(g, hi, denom) >= theta) return hi;
-    while (hi - lo > 1) {
-        const int mid = lo + ((hi - lo) >> 1);
-        if (corrected_estimate(g, mid, denom) >= theta) lo = mid; else hi = mid;
+    int lo = 0, hi = g;  // the answer lies in [lo, hi]; lo = 0 means "nothing passes"
+    while (hi > lo) {
+        const int step = (hi - lo + 31) / 32;
+        int x = lo + ((int)lane + 1) * step;
+        if (x > hi) x = hi;
+        const unsigned pass = __ballot_sync(0xFFFFFFFFu, corrected_estimate(g, x, denom) >= theta);
+        const int cnt = pass == 0xFFFFFFFFu ? 32 : __ffs(~pass) - 1;  // probes are ascending: the passing ones are a prefix
+        if (cnt == 32) {
+            lo = hi;  // lane 31 probed hi itself
+        } else {
+            const int fail_at = lo + (cnt + 1) * step < hi ? lo + (cnt + 1) * step : hi;
+            lo = lo + cnt * step;
+            hi = fail_at - 1;
+        }
     }
     return lo;
 }
 
-__device__ __forceinline__ void plan_readout(Control *ctl, int r, int k, int g, double theta)
+// Called by warp 0 of the CTA that finishes k_hot_sets last.
+__device__ __forceinline__ void plan_readout(Control *ctl, int r, int k, int g, double theta, uint32_t lane)
 {
     const double cap = (double)g * (double)(1ull << k);
-    double acc = 0.0;
+    // per-array terms in parallel (r <= 64: two per lane), summed in array order by lane 0
+    double term[2] = {0.0, 0.0};
     int sat = 0, empty = 0;
-    for (int i = 0; i < r; i++) {
-        long long z = ctl->zero_totals[i];
-        if (z == 0) {
-            sat = 1;
-            z = 1;
+    for (int h = 0; h < 2; h++) {
+        const int i = (int)lane + 32 * h;
+        if (i < r) {
+            long long z = ctl->zero_totals[i];
+            if (z == 0) {
+                sat = 1;
+                z = 1;
+            }
+            term[h] = -cap * log((double)z / cap);
+            if (ctl->hot_counts[i] == 0) empty = 1;
         }
-        acc += -cap * log((double)z / cap);
-        if (ctl->hot_counts[i] == 0) empty = 1;
     }
+    sat = __any_sync(0xFFFFFFFFu, sat);
+    empty = __any_sync(0xFFFFFFFFu, empty);
+    double acc = 0.0;
+    for (int i = 0; i < r; i++) acc += __shfl_sync(0xFFFFFFFFu, term[i >> 5], i & 31);
     const double flow = acc / r;
     const double psi = 1.0 - exp(-flow / cap);
-    ctl->flow_count = flow;
-    ctl->flow_saturated = sat;
-    ctl->psi = psi;
-    ctl->denom = g * (1.0 - pow(psi, (double)r));
-    ctl->sz_cut = report_cut(g, ctl->denom, theta);
-    ctl->any_empty = empty;
-    for (int i = 0; i < 64; i++) ctl->stage_counts[i] = 0;
-    ctl->n_candidates = 0;
-    ctl->n_reports = 0;
-    ctl->fail_stage = 0;
-    ctl->fail_count = 0;
-    ctl->sorted = 0;
+    const double denom = g * (1.0 - pow(psi, (double)r));
+    const int cut = report_cut(g, denom, theta, lane);
+    ctl->stage_counts[lane] = 0;
+    ctl->stage_counts[lane + 32] = 0;
+    if (lane == 0) {
+        ctl->flow_count = flow;
+        ctl->flow_saturated = sat;
+        ctl->psi = psi;
+        ctl->denom = denom;
+        ctl->sz_cut = cut;
+        ctl->any_empty = empty;
+        ctl->n_candidates = 0;
+        ctl->n_reports = 0;
+        ctl->fail_stage = 0;
+        ctl->fail_count = 0;
+        ctl->sorted = 0;
+    }
 }
 
 // Dhla.hot_sets (pkg/src/dhsa/dhla.py:111-119): HE(i) = { j : zc[i][j] < zmin },
@@ -1121,10 +1190,10 @@ __global__ void __launch_bounds__(1024) k_hot_sets(const int32_t *__restrict__ z
         is_last_s = atomicAdd(&ctl->blocks_done, 1u) == gridDim.x - 1;
     }
     __syncthreads();
-    if (is_last_s && threadIdx.x == 0) {
+    if (is_last_s && threadIdx.x < 32) {
         __threadfence();
-        plan_readout(ctl, r, k, g, theta);
-        ctl->blocks_done = 0;
+        plan_readout(ctl, r, k, g, theta, threadIdx.x);
+        if (threadIdx.x == 0) ctl->blocks_done = 0;
     }
 }
 
@@ -1166,12 +1235,12 @@ __device__ __forceinline__ bool stage_blocked(const Control *ctl, int stage_inde
 // Stage 1 (_stage_first, pkg/src/dhsa/dhla.py:252-274): (cl0, cl1) in HE0 x HE1,
 // b1 = cl0 ^ cl1 is the key's low block; cl2 = cl0 ^ b2 with
 // b2 & omask == b1 >> alpha; sub = b1 | (b2 >> (k - alpha)) << k.
-__global__ void __launch_bounds__(256) k_stage_first(const uint32_t *__restrict__ lists,
-                                                     const uint32_t *__restrict__ bitmaps,
-                                                     uint64_t bitmap_words_per_array, DevParams p,
-                                                     unsigned long long buf_cap,
-                                                     uint64_t *__restrict__ out_sub,
-                                                     uint32_t *__restrict__ out_cl0, Control *ctl)
+__device__ __forceinline__ void stage_first_body(const uint32_t *__restrict__ lists,
+                                                 const uint32_t *__restrict__ bitmaps,
+                                                 uint64_t bitmap_words_per_array, const DevParams &p,
+                                                 unsigned long long buf_cap, uint64_t *__restrict__ out_sub,
+                                                 uint32_t *__restrict__ out_cl0, Control *ctl, uint64_t tid,
+                                                 uint64_t stride)
 {
     if (stage_blocked(ctl, 0, buf_cap)) return;
     const uint64_t m = 1ull << p.k;
@@ -1184,8 +1253,7 @@ __global__ void __launch_bounds__(256) k_stage_first(const uint32_t *__restrict_
     const uint32_t omask = (uint32_t)((1ull << top) - 1);
     const uint32_t *he0 = lists, *he1 = lists + m, *he2 = lists + 2 * m;
     const uint32_t *bmp2 = bitmaps + 2 * bitmap_words_per_array;
-    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-    for (uint64_t f = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; f < total; f += stride) {
+    for (uint64_t f = tid; f < total; f += stride) {
         const uint64_t t = f % E, pair = f / E;
         const uint32_t cl0 = he0[pair / n1];
         const uint32_t b1 = cl0 ^ he1[pair % n1];
@@ -1208,17 +1276,27 @@ __global__ void __launch_bounds__(256) k_stage_first(const uint32_t *__restrict_
     }
 }
 
+__global__ void __launch_bounds__(256) k_stage_first(const uint32_t *__restrict__ lists,
+                                                     const uint32_t *__restrict__ bitmaps,
+                                                     uint64_t bitmap_words_per_array, DevParams p,
+                                                     unsigned long long buf_cap,
+                                                     uint64_t *__restrict__ out_sub,
+                                                     uint32_t *__restrict__ out_cl0, Control *ctl)
+{
+    stage_first_body(lists, bitmaps, bitmap_words_per_array, p, buf_cap, out_sub, out_cl0, ctl,
+                     (uint64_t)blockIdx.x * blockDim.x + threadIdx.x, (uint64_t)gridDim.x * blockDim.x);
+}
+
 // Stage for array i >= 3 (_stage_next, pkg/src/dhsa/dhla.py:277-299):
 // blk = cl0 ^ cl_i must satisfy blk & omask == sub >> (i-1) alpha;
 // sub |= (blk >> (k - alpha)) << (k + (i-2) alpha).
-__global__ void __launch_bounds__(256) k_stage_next(int i, const uint32_t *__restrict__ lists,
-                                                    const uint32_t *__restrict__ bitmaps,
-                                                    uint64_t bitmap_words_per_array, DevParams p,
-                                                    unsigned long long buf_cap,
-                                                    const uint64_t *__restrict__ in_sub,
-                                                    const uint32_t *__restrict__ in_cl0,
-                                                    uint64_t *__restrict__ out_sub,
-                                                    uint32_t *__restrict__ out_cl0, Control *ctl)
+__device__ __forceinline__ void stage_next_body(int i, const uint32_t *__restrict__ lists,
+                                                const uint32_t *__restrict__ bitmaps,
+                                                uint64_t bitmap_words_per_array, const DevParams &p,
+                                                unsigned long long buf_cap, const uint64_t *__restrict__ in_sub,
+                                                const uint32_t *__restrict__ in_cl0, uint64_t *__restrict__ out_sub,
+                                                uint32_t *__restrict__ out_cl0, Control *ctl, uint64_t tid,
+                                                uint64_t stride)
 {
     const int s = i - 2;  // stages already run
     if (stage_blocked(ctl, s, buf_cap)) return;
@@ -1233,8 +1311,7 @@ __global__ void __launch_bounds__(256) k_stage_next(int i, const uint32_t *__res
     const int sh_chk = (i - 1) * p.alpha, sh_put = p.k + (i - 2) * p.alpha;
     const uint32_t *he = lists + (uint64_t)i * m;
     const uint32_t *bmp = bitmaps + (uint64_t)i * bitmap_words_per_array;
-    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-    for (uint64_t f = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; f < total; f += stride) {
+    for (uint64_t f = tid; f < total; f += stride) {
         const uint64_t t = f % E, q = f / E;
         const uint64_t sp = in_sub[q];
         const uint32_t cl0 = in_cl0[q];
@@ -1256,6 +1333,19 @@ __global__ void __launch_bounds__(256) k_stage_next(int i, const uint32_t *__res
             }
         }
     }
+}
+
+__global__ void __launch_bounds__(256) k_stage_next(int i, const uint32_t *__restrict__ lists,
+                                                    const uint32_t *__restrict__ bitmaps,
+                                                    uint64_t bitmap_words_per_array, DevParams p,
+                                                    unsigned long long buf_cap,
+                                                    const uint64_t *__restrict__ in_sub,
+                                                    const uint32_t *__restrict__ in_cl0,
+                                                    uint64_t *__restrict__ out_sub,
+                                                    uint32_t *__restrict__ out_cl0, Control *ctl)
+{
+    stage_next_body(i, lists, bitmaps, bitmap_words_per_array, p, buf_cap, in_sub, in_cl0, out_sub, out_cl0, ctl,
+                    (uint64_t)blockIdx.x * blockDim.x + threadIdx.x, (uint64_t)gridDim.x * blockDim.x);
 }
 
 // Tail of _candidate_hosts (pkg/src/dhsa/dhla.py:213-216): drop partials with bits
@@ -1362,22 +1452,19 @@ __device__ __forceinline__ uint64_t pack_report(int sz, double denom, uint64_t h
 // _candidate_hosts), then SZ and the threshold filter (dhla.py:183-194) as the integer compare
 // max(SZ, 1) <= ctl->sz_cut.  Every verified key is kept with its SZ (keys[], cand_sz[]) so the
 // filter can be re-applied with another cut without touching the bits again (k_refilter).
-__global__ void __launch_bounds__(256) k_verify_reestimate(int n_stages, DevParams p, unsigned long long buf_cap,
-                                                           unsigned long long max_candidates,
-                                                           const uint64_t *__restrict__ in_sub,
-                                                           const uint32_t *__restrict__ in_cl0,
-                                                           const uint8_t *__restrict__ bits,
-                                                           uint64_t *__restrict__ keys, int32_t *__restrict__ cand_sz,
-                                                           uint64_t *__restrict__ packed, Control *ctl)
+__device__ __forceinline__ void verify_reestimate_body(int n_stages, const DevParams &p, unsigned long long buf_cap,
+                                                       const uint64_t *__restrict__ in_sub,
+                                                       const uint32_t *__restrict__ in_cl0,
+                                                       const uint8_t *__restrict__ bits, uint64_t *__restrict__ keys,
+                                                       int32_t *__restrict__ cand_sz, uint64_t *__restrict__ packed,
+                                                       Control *ctl, uint64_t warp, uint64_t nwarps)
 {
-    if (blockIdx.x == 0 && threadIdx.x == 0) record_capacity_failure(ctl, n_stages, buf_cap, max_candidates);
     if (stage_blocked(ctl, n_stages, buf_cap)) return;
     const uint32_t lane = threadIdx.x & 31u;
     const uint64_t np = ctl->stage_counts[n_stages - 1];
     const double denom = ctl->denom;
     const int cut = ctl->sz_cut;
-    const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
-    for (uint64_t q = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; q < np; q += nwarps) {
+    for (uint64_t q = warp; q < np; q += nwarps) {
         const uint64_t sub = in_sub[q];
         if (sub >> p.key_width) continue;           // warp-uniform
         if (dh0_of(p, sub) != in_cl0[q]) continue;  // warp-uniform
@@ -1389,6 +1476,19 @@ __global__ void __launch_bounds__(256) k_verify_reestimate(int n_stages, DevPara
             if ((sz == 0 ? 1 : sz) <= cut) packed[atomicAdd(&ctl->n_reports, 1ull)] = pack_report(sz, denom, sub);
         }
     }
+}
+
+__global__ void __launch_bounds__(256) k_verify_reestimate(int n_stages, DevParams p, unsigned long long buf_cap,
+                                                           unsigned long long max_candidates,
+                                                           const uint64_t *__restrict__ in_sub,
+                                                           const uint32_t *__restrict__ in_cl0,
+                                                           const uint8_t *__restrict__ bits,
+                                                           uint64_t *__restrict__ keys, int32_t *__restrict__ cand_sz,
+                                                           uint64_t *__restrict__ packed, Control *ctl)
+{
+    if (blockIdx.x == 0 && threadIdx.x == 0) record_capacity_failure(ctl, n_stages, buf_cap, max_candidates);
+    verify_reestimate_body(n_stages, p, buf_cap, in_sub, in_cl0, bits, keys, cand_sz, packed, ctl,
+                           ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5, ((uint64_t)gridDim.x * blockDim.x) >> 5);
 }
 
 // The filter again, over the verified keys and their SZ, with a cut handed in by the host
@@ -1450,12 +1550,26 @@ __global__ void __launch_bounds__(256) k_emit_reports(const uint64_t *__restrict
 
 // emit != nullptr: the sorted words are packed reports and their rows are written too
 // (sort + emit in one launch; the read-out chain is latency-bound, every launch is ~5 us).
+// emit != nullptr: the sorted words are packed reports and their rows are written too
+// (sort + emit in one launch; the read-out chain is latency-bound, every launch is ~5 us).
+// As the chain's last kernel it also gathers what the host reads back into ONE block behind the
+// control block -- the window counters and the first DHSA_HEAD_ROWS report rows -- so a read-out
+// costs one device-to-host copy, not three.
+#define DHSA_HEAD_ROWS 256
+struct Readback {
+    Control c;
+    ReportOut head[DHSA_HEAD_ROWS];
+};
+
 __global__ void __launch_bounds__(1024) k_sort_small(uint64_t *__restrict__ data,
                                                      const unsigned long long *__restrict__ n_ptr,
-                                                     Control *ctl, ReportOut *__restrict__ emit, int g)
+                                                     Control *ctl, ReportOut *__restrict__ emit, int g,
+                                                     const unsigned long long *__restrict__ counters,
+                                                     ReportOut *__restrict__ head)
 {
     extern __shared__ uint64_t sm[];
     const uint64_t n = *n_ptr;
+    if (counters && threadIdx.x < 6) ctl->counters[threadIdx.x] = counters[threadIdx.x];
     if (n > DHSA_SORT_SMEM_MAX) return;
     uint32_t len = 1;
     while (len < n) len <<= 1;
@@ -1480,7 +1594,11 @@ __global__ void __launch_bounds__(1024) k_sort_small(uint64_t *__restrict__ data
     for (uint32_t t = threadIdx.x; t < n; t += blockDim.x) data[t] = sm[t];
     if (emit) {
         const double denom = ctl->denom;
-        for (uint32_t t = threadIdx.x; t < n; t += blockDim.x) emit[t] = unpack_report(sm[t], g, denom);
+        for (uint32_t t = threadIdx.x; t < n; t += blockDim.x) {
+            const ReportOut row = unpack_report(sm[t], g, denom);
+            emit[t] = row;
+            if (head && t < DHSA_HEAD_ROWS) head[t] = row;
+        }
     }
     if (threadIdx.x == 0 && ctl) ctl->sorted = 1;
 }
@@ -1806,6 +1924,8 @@ __device__ __forceinline__ uint32_t probe_hash(uint64_t x)
     return (uint32_t)(x >> 32);
 }
 
+// KIND 0: RED.OR   1: 32-bit load   2: four loads + one RED per five operations (do the two share a
+// limit?)   3: 256-bit load of a whole sector (the flow-cache lookup's shape)
 template <int KIND>
 __global__ void __launch_bounds__(256) k_probe_l2(uint32_t *__restrict__ words, uint32_t word_mask,
                                                   uint64_t ops, uint32_t *__restrict__ sink)
@@ -1819,14 +1939,22 @@ __global__ void __launch_bounds__(256) k_probe_l2(uint32_t *__restrict__ words, 
             if (q < ops) {
                 const uint32_t hsh = probe_hash(q);
                 uint32_t *wp = words + (hsh & word_mask);
-                if (KIND == 0)
+                if (KIND == 0) {
                     red_or(wp, 1u << (hsh >> 27));
-                else
+                } else if (KIND == 1) {
                     acc += ld_sketch(wp);
+                } else if (KIND == 2) {
+                    acc += ld_sketch(wp);
+                    if (u == 3) red_or(words + (probe_hash(q ^ 0x5555555555ull) & word_mask), 1u << (hsh >> 27));
+                } else {
+                    unsigned long long e[4];
+                    ld_fc_set(reinterpret_cast<const unsigned long long *>(words + (hsh & word_mask & ~7u)), e);
+                    acc += (uint32_t)(e[0] ^ e[1] ^ e[2] ^ e[3]);
+                }
             }
         }
     }
-    if (KIND == 1 && acc == 0x12345678u) *sink = acc;
+    if (KIND != 0 && acc == 0x12345678u) *sink = acc;
 }
 
 }  // namespace dhsa
