@@ -48,7 +48,7 @@ if ROOT not in sys.path:
     sys.path.insert(0, ROOT)
 
 THETA = 1024
-CONTROL_BLOCK_BYTES = 1616   # sizeof(dhsa::Control), copied back with every read-out
+READBACK_BYTES = 1640 + 256 * 24   # sizeof(dhsa::Readback): control block with the window counters + the first 256 report rows
 WORKLOAD = ("config2: 100M-packet window per GPU, default DDH (r5 g1024 k14 a6), 150k uniform background hosts "
             "(Zipf1.5 cardinality<=256) + 50 scanners (2048-8192), ~3.8M distinct flows, theta 1024")
 
@@ -588,13 +588,16 @@ def run_ours(args, rank: int, local_rank: int, world: int) -> None:
         }
         if roofline["traffic"] is None:
             # dram__bytes_read.sum + dram__bytes_write.sum of one 100M-packet launch, from the committed ncu capture
-            tpath = os.path.join(ROOT, "profiles", "r01_traffic.json")
-            if os.path.exists(tpath) and n == 100_000_000:
-                entry = json.load(open(tpath)).get(kernel.split(",")[0] + (",2>" if "vec4" in kernel else ""), None) \
-                    or json.load(open(tpath)).get(kernel)
+            for tag in ("r02", "r01"):            # the newest committed capture of this kernel
+                tpath = os.path.join(ROOT, "profiles", f"{tag}_traffic.json")
+                if not (os.path.exists(tpath) and n == 100_000_000):
+                    continue
+                table = json.load(open(tpath))
+                entry = table.get(kernel.split(",")[0] + (",2>" if "vec4" in kernel else ""), None) or table.get(kernel)
                 if entry:
                     roofline["traffic"] = entry["dram_bytes_per_launch"]
-                    roofline["traffic_source"] = "profiles/r01_traffic.json (ncu --set full)"
+                    roofline["traffic_source"] = f"profiles/{tag}_traffic.json (ncu --set full)"
+                    break
         if l2:
             roofline["l2_probe"] = l2
         # The ceiling that actually binds (north star: the slower of HBM streaming and the sketch's L2
@@ -653,8 +656,8 @@ def run_ours(args, rank: int, local_rank: int, world: int) -> None:
         if rec_stats:
             line["records_path"] = rec_stats
         if e2e:
-            # dhsa_report_t rows + the control block + the window counters read back per window
-            reports_bytes = 24 * e2e[1] + CONTROL_BLOCK_BYTES + 48
+            # one copy per read-out: control block + window counters + the first 256 report rows
+            reports_bytes = READBACK_BYTES
             line["e2e"] = {"value": n_total * args.steps / (e2e_ms * 1e-3) / 1e6, "unit": "Mpps",
                            "h2d_bytes_per_step": 8 * n, "d2h_bytes_per_step": reports_bytes,
                            "ms_per_step": e2e_ms / args.steps}

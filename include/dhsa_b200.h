@@ -48,9 +48,8 @@ extern "C" {
 #define DHSA_SCAN_TEST_RED 1      /* load the word, atomic only if the bit is still clear      */
 #define DHSA_SCAN_TEST_AGG_RED 2  /* as 1, and lanes of a warp hitting one word merge first    */
 #define DHSA_SCAN_FLOW_CACHE 3    /* as 2 behind an exact L2-resident cache of scanned pairs   */
-#define DHSA_SCAN_AUTO 4          /* default: 3; 2 for the rest of a window whose flows do not repeat
-                                     (cache hit rate below ~1/3); 1 while read-outs show at most
-                                     128 busy cells per array (a few candidates: words sit in L1) */
+#define DHSA_SCAN_AUTO 4          /* default: 3, falling back to 1 for the rest of a window whose
+                                     flows do not repeat (cache hit rate below ~1/3)            */
 
 typedef struct dhsa_sketch dhsa_sketch_t; /* opaque; replaces dhsa.dhla.Dhla, pkg/src/dhsa/dhla.py:57-68 */
 

@@ -104,14 +104,13 @@ struct dhsa_sketch {
 
     // flow cache of scan mode 3
     unsigned long long *fcache;
-    unsigned long long *fc_stats;  // device: flow-cache lookups, hits; test-first kernel packets, REDs (auto policy)
+    unsigned long long *fc_stats;  // device: flow-cache lookups, hits
     uint32_t fc_sets;              // requested size in sets; the table is allocated on first use
     bool fc_dirty;                 // holds entries since the last clear
     unsigned long long *fc_stats_host;  // pinned snapshot of fc_stats for the auto policy
     cudaEvent_t fc_stats_ev;
     bool fc_stats_pending;
     bool auto_fell_back;           // auto mode: this window's flows do not repeat, use the 5-access kernel
-    bool regime_few_keys;          // auto mode: the traffic's keys sit in a handful of hot words (see the auto policy)
 
     // read-out workspaces
     Readback *rb, *rb_host;  // control block + window counters + first report rows: device, and its pinned mirror
@@ -145,7 +144,7 @@ struct dhsa_sketch {
     bool graph_disabled;
     ReportOut *reports_pinned;      // the first kPinnedReports rows land here with the control block
     cudaEvent_t restore_ev;         // read-out enqueued by dhsa_restore_begin has landed in the pinned mirrors
-    unsigned long long *tally_pinned;  // the 6 window counters (record tally, flow cache, test kernel) as of the last read-out
+    unsigned long long *tally_pinned;  // the 4 window counters (record tally, flow-cache lookups / hits) as of the last read-out
     bool restore_pending;
     uint64_t restore_max_candidates;
     double restore_theta;
@@ -362,7 +361,6 @@ static int scrub_for_parking(dhsa_sketch *s)
     s->launches = 0;
     s->restore_pending = false;
     s->zc_given = false;
-    s->regime_few_keys = false;
     CU(cudaMemsetAsync(s->bits, 0, s->alloc_bytes + kCounterBytes, s->stream));
     if (int rc = clear_flow_cache_locked(s, false)) return rc;
     CU(cudaStreamSynchronize(s->stream));
@@ -547,7 +545,7 @@ static int clear_flow_cache_locked(dhsa_sketch *s, bool clear_stats)
     } else {
         s->dp.fc_epoch++;
     }
-    if (clear_stats) CU(cudaMemsetAsync(s->fc_stats, 0, 4 * sizeof(unsigned long long), s->stream));
+    if (clear_stats) CU(cudaMemsetAsync(s->fc_stats, 0, 2 * sizeof(unsigned long long), s->stream));
     s->fc_dirty = false;
     return DHSA_OK;
 }
@@ -775,26 +773,20 @@ static void launch_scan_any_r(dhsa_sketch *s, int mode, const SRC &src)
 // Decided per launch from counters the scan kernels leave behind the bit array, read through
 // asynchronous pinned snapshots (never a synchronisation):
 //   * flows that do not repeat (cache hit rate under 0.3 after >= 4M lookups): the rest of the
-//     WINDOW goes to the 5-access kernel.  Break-even is a hit rate of about 1/3: 1 + 11 (1 - h)
+//     WINDOW goes to the 5-access test-first kernel.  Break-even is a hit rate of about 1/3: 1 + 11 (1 - h)
 //     requests per packet with the cache against 5 + 5 (1 - h) without.
-//   * a handful of candidate hosts (a DDoS window with the victims as candidates -- BASELINE
-//     config 4 -- where every packet lands in the same few cells): those cells' words sit in L1, so
-//     the plain test-first kernel needs no L2 access at all while a cache lookup is still one L2
-//     request per packet.  The signal is exact and free: every read-out counts the non-empty cells
-//     of array 0 (k_hot_sets), i.e. the distinct dh0 values seen.  At most kFewCells of them after a
-//     window of >= 4M packets switches the REGIME, which persists across resets (it is a property
-//     of the traffic, known one read-out late); more than that, or -- inside a window -- a test
-//     kernel that still issues a RED for more than 1 packet in 64, switches it back.
-static const unsigned long long kFewCells = 128;   // 5 x 128 cells x 128 B = 80 KB of sketch words
+// (A second rule of an earlier round -- the plain test-first kernel for windows whose candidates are a
+// handful of hosts, BASELINE config 4 with the victims as candidates -- was measured again after the
+// lookup loop lost its per-slot miss handling: the cache path now scans that window at 205 Gpps
+// against 183 for the test-first kernel, so the rule is gone; profiles/r02_config4_ddos_contention.json.)
 
 static void consume_policy_snapshots(dhsa_sketch *s, bool window_ends)
 {
     if (s->fc_stats_pending && cudaEventQuery(s->fc_stats_ev) == cudaSuccess) {
         s->fc_stats_pending = false;
         const unsigned long long lookups = s->fc_stats_host[0], hits = s->fc_stats_host[1];
-        const unsigned long long packets = s->fc_stats_host[2], reds = s->fc_stats_host[3];
+        // a snapshot that arrives when its window is over says nothing about the next one
         if (lookups >= kPolicyMinSample && !window_ends && hits * 10 < lookups * 3) s->auto_fell_back = true;
-        if (packets >= kPolicyMinSample && reds * 64 > packets) s->regime_few_keys = false;
     }
     (void)cudaGetLastError();
 }
@@ -805,8 +797,9 @@ static int pick_scan_mode_locked(dhsa_sketch *s)
     int mode = s->scan_mode;
     if (mode == DHSA_SCAN_AUTO) {
         consume_policy_snapshots(s, false);
-        mode = s->regime_few_keys ? DHSA_SCAN_TEST_RED
-                                  : (s->auto_fell_back ? DHSA_SCAN_TEST_AGG_RED : DHSA_SCAN_FLOW_CACHE);
+        // the fallback is the plain test-first kernel: without repeats there is nothing for warp aggregation to
+        // merge either (all-distinct window: 31.6 Gpps against 29.7 with aggregation)
+        mode = s->auto_fell_back ? DHSA_SCAN_TEST_RED : DHSA_SCAN_FLOW_CACHE;
     }
     if (mode == DHSA_SCAN_FLOW_CACHE && !flow_cache_supported(s)) mode = DHSA_SCAN_TEST_AGG_RED;
     return mode;
@@ -819,21 +812,18 @@ static int before_fast_scan_locked(dhsa_sketch *s, int mode)
         if (int rc = ensure_flow_cache_locked(s)) return rc;
         s->fc_dirty = true;
     }
-    // the test-first kernel counts packets and REDs only while the policy listens
-    s->dp.test_stats = (s->scan_mode == DHSA_SCAN_AUTO && mode == DHSA_SCAN_TEST_RED) ? s->fc_stats + 2 : nullptr;
     return DHSA_OK;
 }
 
 static int after_fast_scan_locked(dhsa_sketch *s, int mode)
 {
-    if (s->scan_mode == DHSA_SCAN_AUTO && (mode == DHSA_SCAN_FLOW_CACHE || mode == DHSA_SCAN_TEST_RED) &&
-        !s->fc_stats_pending) {
+    if (s->scan_mode == DHSA_SCAN_AUTO && mode == DHSA_SCAN_FLOW_CACHE && !s->fc_stats_pending) {
         if (!s->fc_stats_host) {
-            CU(cudaMallocHost(&s->fc_stats_host, 4 * sizeof(unsigned long long)));
+            CU(cudaMallocHost(&s->fc_stats_host, 2 * sizeof(unsigned long long)));
             CU(cudaEventCreateWithFlags(&s->fc_stats_ev, cudaEventDisableTiming));
-            memset(s->fc_stats_host, 0, 4 * sizeof(unsigned long long));
+            memset(s->fc_stats_host, 0, 2 * sizeof(unsigned long long));
         }
-        CU(cudaMemcpyAsync(s->fc_stats_host, s->fc_stats, 4 * sizeof(unsigned long long), cudaMemcpyDeviceToHost,
+        CU(cudaMemcpyAsync(s->fc_stats_host, s->fc_stats, 2 * sizeof(unsigned long long), cudaMemcpyDeviceToHost,
                            s->stream));
         CU(cudaEventRecord(s->fc_stats_ev, s->stream));
         s->fc_stats_pending = true;
@@ -1869,14 +1859,6 @@ static void fill_info(const dhsa_sketch *s, double theta, dhsa_restore_info_t *i
     }
 }
 
-// a window's read-out came back: what it says about the traffic (the auto policy's regime)
-static void note_traffic_regime(dhsa_sketch *s)
-{
-    const unsigned long long *w = s->tally_pinned;  // [0..1] record tally, [2..3] flow cache, [4..5] test kernel
-    const unsigned long long seen = w[2] + w[4];
-    if (seen >= kPolicyMinSample) s->regime_few_keys = s->ctl_host->busy_cells <= kFewCells;
-}
-
 extern "C" int dhsa_zero_counts(dhsa_sketch_t *s, int64_t *zc_host, int64_t *zr_host)
 {
     NEED(s);
@@ -2195,7 +2177,6 @@ static int restore_end_locked(dhsa_sketch *s, dhsa_report_t *reports_host, uint6
         if (int rc = run_restore(s, theta, max_candidates)) return rc;
         CU(cudaStreamSynchronize(s->stream));
     }
-    note_traffic_regime(s);
     if (s->ctl_host->fail_stage) {
         s->restore_pending = false;
         fill_info(s, theta, info);

@@ -32,7 +32,6 @@ struct DevParams {
     int fc_tag_bits;               // fc_shift + log2(g): key bits an entry stores
     uint32_t fc_epoch;             // entries of other epochs count as empty: a window reset is epoch + 1
     unsigned long long *fc_stats;  // [0] lookups, [1] hits
-    unsigned long long *test_stats;  // k_scan_vec4<.,1>: [0] packets, [1] REDs issued; null = do not count
 };
 
 // Device-resident control block of one read-out: every stage kernel reads its
@@ -51,9 +50,8 @@ struct Control {
     unsigned int blocks_done;  // k_hot_sets: CTAs finished (the last one computes the scalars)
     int sz_cut;  // report filter as an integer: a candidate passes iff max(SZ, 1) <= sz_cut (see plan_readout)
     double flow_count, psi, denom;
-    unsigned long long busy_cells;  // non-empty cells of array 0 = distinct dh0 values seen (the auto policy's signal)
-    unsigned long long counters[6];  // the window's counters as of this read-out: records fed / dropped, flow-cache
-                                     // lookups / hits, test-kernel packets / REDs (copied by the chain's last kernel)
+    unsigned long long counters[4];  // the window's counters as of this read-out: records fed / dropped, flow-cache
+                                     // lookups / hits (copied by the chain's last kernel)
 };
 
 // ------------------------------------------------------------------ hashing --
@@ -458,7 +456,6 @@ __global__ void __launch_bounds__(256) k_scan_vec4(SRC src, uint32_t *__restrict
     const int wshift = p.log2g - 5;
     const uint64_t pol = policy_evict_first();
     uint32_t on_time = 0, late = 0;
-    uint32_t n_red = 0, n_pkt = 0;  // MODE 1 under the auto policy: new bits per packet (p.test_stats)
 
     for (uint64_t base = warp0 * 32; base < nvec; base += nwarps * 32) {
         const uint64_t v = base + lane;
@@ -467,7 +464,6 @@ __global__ void __launch_bounds__(256) k_scan_vec4(SRC src, uint32_t *__restrict
         uint32_t cs[4], os[4];
         bool ok[4];
         src.unpack(raw, v, cs, os, ok, on_time, late);
-        if (MODE == 1) n_pkt += (uint32_t)ok[0] + (uint32_t)ok[1] + (uint32_t)ok[2] + (uint32_t)ok[3];
 
         uint32_t widx[4][R];
         uint32_t mask[4];
@@ -498,26 +494,12 @@ __global__ void __launch_bounds__(256) k_scan_vec4(SRC src, uint32_t *__restrict
                 for (int i = 0; i < R; i++) {
                     const bool need = (w[j][i] & mask[j]) == 0;
                     if (MODE == 1) {
-                        if (need) {
-                            red_or(words + widx[j][i], mask[j]);
-                            n_red++;
-                        }
+                        if (need) red_or(words + widx[j][i], mask[j]);
                     } else {
                         red_or_aggregated(words, widx[j][i], mask[j], need, lane);
                     }
                 }
             }
-        }
-    }
-    if (MODE == 1 && p.test_stats != nullptr) {
-        unsigned long long pk = n_pkt, rd = n_red;
-        for (int d = 16; d > 0; d >>= 1) {
-            pk += __shfl_xor_sync(0xFFFFFFFFu, pk, d);
-            rd += __shfl_xor_sync(0xFFFFFFFFu, rd, d);
-        }
-        if (lane == 0 && pk) {
-            atomicAdd(p.test_stats + 0, pk);
-            atomicAdd(p.test_stats + 1, rd);
         }
     }
     flush_tally(src, on_time, late, lane);
@@ -1111,7 +1093,6 @@ __global__ void __launch_bounds__(1024) k_hot_sets(const int32_t *__restrict__ z
     uint32_t *list = lists + (uint64_t)arr * m;
     uint32_t *bmp = bitmaps + (uint64_t)arr * bitmap_words_per_array;
     unsigned long long base = 0, total = 0;
-    uint32_t busy = 0;  // cells of this thread with at least one bit set
     for (uint64_t c0 = 0; c0 < m; c0 += 1024ull * DHSA_HOT_CPT) {
         const uint64_t j0 = c0 + (uint64_t)threadIdx.x * DHSA_HOT_CPT;
         uint32_t hot = 0;
@@ -1127,7 +1108,6 @@ __global__ void __launch_bounds__(1024) k_hot_sets(const int32_t *__restrict__ z
                 hot |= (uint32_t)(z.w <= zc_cut) << (4 * q + 3);
                 zs += (unsigned long long)z.x + (unsigned long long)z.y + (unsigned long long)z.z +
                       (unsigned long long)z.w;
-                busy += (uint32_t)(z.x < g) + (uint32_t)(z.y < g) + (uint32_t)(z.z < g) + (uint32_t)(z.w < g);
             }
         } else {
             for (int q = 0; q < DHSA_HOT_CPT; q++)
@@ -1135,7 +1115,6 @@ __global__ void __launch_bounds__(1024) k_hot_sets(const int32_t *__restrict__ z
                     const int32_t z = row[j0 + q];
                     hot |= (uint32_t)(z <= zc_cut) << q;
                     zs += (unsigned long long)z;
-                    busy += (uint32_t)(z < g);
                 }
         }
         // bitmap: two threads share a 32-bit word
@@ -1172,16 +1151,6 @@ __global__ void __launch_bounds__(1024) k_hot_sets(const int32_t *__restrict__ z
         base += chunk_total_s;
         total += chunk_sum_s;
         __syncthreads();
-    }
-    if (arr == 0) {  // block sum of the busy-cell counts (warp_count is free again after the loop's last barrier)
-        for (int d = 16; d > 0; d >>= 1) busy += __shfl_xor_sync(0xFFFFFFFFu, busy, d);
-        if (lane == 0) warp_count[wid] = busy;
-        __syncthreads();
-        if (threadIdx.x == 0) {
-            unsigned long long tot = 0;
-            for (int w = 0; w < 32; w++) tot += warp_count[w];
-            ctl->busy_cells = tot;
-        }
     }
     if (threadIdx.x == 0) {
         ctl->hot_counts[arr] = base;
@@ -1569,7 +1538,7 @@ __global__ void __launch_bounds__(1024) k_sort_small(uint64_t *__restrict__ data
 {
     extern __shared__ uint64_t sm[];
     const uint64_t n = *n_ptr;
-    if (counters && threadIdx.x < 6) ctl->counters[threadIdx.x] = counters[threadIdx.x];
+    if (counters && threadIdx.x < 4) ctl->counters[threadIdx.x] = counters[threadIdx.x];
     if (n > DHSA_SORT_SMEM_MAX) return;
     uint32_t len = 1;
     while (len < n) len <<= 1;

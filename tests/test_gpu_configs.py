@@ -165,35 +165,3 @@ def test_config4_ddos_contention_100m_packets(ddos, direction, mode):
     _same_outcome(_outcome(sk.restore_superpoints, 1024), want)
     if direction == "dst":
         assert [s for _, s, _ in want] == [True] * 4        # the four victims, saturated
-
-
-def test_auto_policy_follows_the_traffic_regime(ddos):
-    """auto: flow cache by default; the test-first kernel once a read-out has shown at most 128 busy
-    cells per array (a window whose candidates are a handful of hosts: their words sit in L1);
-    back to the flow cache when the traffic changes.  Bits are exact in every regime."""
-    cand, opp, want_bits, _ = ddos["dst"]
-    sk = P.Dhla(P.DhgParams())
-    sk.update_batch(cand, opp)
-    assert sk.scan_mode_used == "flow_cache"
-    sk.restore_superpoints(1024)                              # the read-out carries the signal
-    sk.reset()
-    sk.update_batch(cand, opp)
-    assert sk.scan_mode_used == "test" and sha(sk.bits) == want_bits
-    sk.restore_superpoints(1024)
-    # ordinary traffic again: many candidates
-    c2, o2 = O.distinct_pairs(3_000_000, 77)
-    pick = np.random.default_rng(7).integers(0, len(c2), size=12_000_000)
-    pick[: len(c2)] = np.arange(len(c2))                      # every flow at least once
-    import torch
-
-    ct = torch.from_numpy(c2[pick].view(np.int32)).cuda()
-    ot = torch.from_numpy(o2[pick].view(np.int32)).cuda()
-    ora = O.OracleSketch()
-    ora.update_batch(c2, o2, threads=8)
-    sk.reset()
-    sk.update_batch(ct, ot)                                   # still the few-candidates regime: exact anyway
-    assert sha(sk.bits) == sha(ora.bits)
-    sk.restore_superpoints(1024)                              # this read-out sees ~16k busy cells
-    sk.reset()
-    sk.update_batch(ct, ot)
-    assert sk.scan_mode_used == "flow_cache" and sha(sk.bits) == sha(ora.bits)

@@ -263,11 +263,12 @@ def test_auto_mode_falls_back_when_flows_do_not_repeat():
         sk.update_batch(cand[s:s + 2_000_000], opp[s:s + 2_000_000])
         sk.seal()
     assert sha(sk.bits) == sha(ora.bits)
+    assert sk.scan_mode_used == "test"                       # what auto resolved to for the last batches
     lookups, hits = sk.flow_cache_stats()
     assert 0 < lookups < len(cand) and hits * 10 < lookups   # later batches bypassed the cache
     sk.reset()                                               # next window starts behind the cache again
     sk.update_batch(cand[:1_000_000], opp[:1_000_000])
-    assert sk.flow_cache_stats()[0] == 1_000_000
+    assert sk.flow_cache_stats()[0] == 1_000_000 and sk.scan_mode_used == "flow_cache"
 
 
 def test_estimator_returns_one_cell():

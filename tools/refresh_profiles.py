@@ -6,7 +6,7 @@ import shutil
 import subprocess
 import sys
 
-TAG = sys.argv[1] if len(sys.argv) > 1 else "r01"
+TAG = sys.argv[1] if len(sys.argv) > 1 else "r02"
 OUT = "profiles"
 
 
@@ -29,6 +29,9 @@ KEYS = ['gpu__time_duration.sum', 'dram__bytes_read.sum', 'dram__bytes_write.sum
         'l1tex__m_xbar2l1tex_read_sectors_mem_global_op_tma_ld.sum', 'lts__t_sectors.sum',
         'lts__t_sectors_srcunit_tex_op_read.sum', 'lts__t_sectors_srcunit_tex_op_red.sum',
         'lts__t_sectors_srcunit_tex_op_write.sum', 'lts__t_requests_srcunit_ltcfabric.sum',
+        'lts__t_requests_srcunit_tex.sum', 'lts__t_requests_srcunit_tex_op_read.sum',
+        'lts__t_requests_srcunit_tex_op_red.sum', 'lts__t_requests_srcunit_tex_op_write.sum',
+        'lts__t_sectors_srcunit_tex_op_read_lookup_miss.sum', 'lts__t_sectors_srcunit_tex_op_red_lookup_miss.sum',
         'sm__throughput.avg.pct_of_peak_sustained_elapsed', 'sm__warps_active.avg.pct_of_peak_sustained_active',
         'smsp__issue_active.avg.pct_of_peak_sustained_active', 'launch__registers_per_thread', 'launch__grid_size',
         'launch__block_size', 'sm__cycles_elapsed.avg', 'smsp__inst_executed.sum',
@@ -63,13 +66,47 @@ traffic = {
     "k_scan_vec4<5,2>": {"dram_bytes_per_launch": dram(vec4), "algorithmic_bytes_per_launch": 8e8},
 }
 json.dump(traffic, open(f"{OUT}/{TAG}_traffic.json", "w"), indent=1)
+# what bench.py's roofline block reads: requests and REDs per packet of the scan kernels, from these captures
+PACKETS = 100_000_000
+
+
+def counters(entry, what):
+    g = lambda k: entry[k][0]
+    return {
+        "packets_per_launch": PACKETS,
+        "l2_requests_per_packet": g('lts__t_requests_srcunit_tex.sum') / PACKETS,
+        "l2_read_requests_per_packet": g('lts__t_requests_srcunit_tex_op_read.sum') / PACKETS,
+        "l2_red_per_packet": g('lts__t_requests_srcunit_tex_op_red.sum') / PACKETS,
+        "l2_write_requests_per_packet": g('lts__t_requests_srcunit_tex_op_write.sum') / PACKETS,
+        "l2_sectors_per_packet": (g('lts__t_sectors_srcunit_tex_op_read.sum') + g('lts__t_sectors_srcunit_tex_op_red.sum') +
+                                  g('lts__t_sectors_srcunit_tex_op_write.sum')) / PACKETS,
+        "tma_stream_sectors_per_packet": g('l1tex__m_xbar2l1tex_read_sectors_mem_global_op_tma_ld.sum') / PACKETS,
+        "remote_die_requests_per_packet": g('lts__t_requests_srcunit_ltcfabric.sum') / PACKETS,
+        "request_port_busy_pct": g('l1tex__m_l1tex2xbar_req_cycles_active.avg.pct_of_peak_sustained_elapsed'),
+        "lts_throughput_pct": g('lts__throughput.avg.pct_of_peak_sustained_elapsed'),
+        "dram_throughput_pct": g('gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed'),
+        "issue_active_pct": g('smsp__issue_active.avg.pct_of_peak_sustained_active'),
+        "warp_instructions_per_packet": g('smsp__inst_executed.sum') / PACKETS,
+        "gpu_time_us": g('gpu__time_duration.sum'),
+        "registers_per_thread": g('launch__registers_per_thread'),
+        "source": f"ncu --set full --clock-control none, one {PACKETS}-packet launch of bench.py's config-2 window ({what}); "
+                  f"raw export profiles/{TAG}_{what}_raw.csv; counters lts__t_requests_srcunit_tex[_op_read|_op_red|_op_write].sum, "
+                  f"l1tex__m_l1tex2xbar_req_cycles_active, lts__throughput, gpu__dram_throughput",
+    }
+
+
+json.dump({"k_scan_flowcache<5>": counters(fc, "k_scan_flowcache"), "k_scan_vec4<5,2>": counters(vec4, "k_scan_vec4_mode2")},
+          open(f"{OUT}/{TAG}_scan_counters.json", "w"), indent=1)
 for k, v in fc.items():
     print(k, v)
 print("traffic", traffic)
 
 shutil.copy(f"gpurun_out/launches_{TAG}.csv", f"{OUT}/{TAG}_launch_list_bench_steps2.csv")
-for name in ("", "_reference", "_test_agg", "_test", "_red"):
+for name in ("", "_reference", "_test_agg", "_test", "_red", "_config3"):
     shutil.copy(f"gpurun_out/bench_{TAG}{name}.json", f"{OUT}/{TAG}_bench{name}.json")
+for src, dst in ((f"feed_probe_{TAG}.json", f"{TAG}_host_feed_probe.json"), (f"l2_probe_{TAG}.json", f"{TAG}_l2_probe.json"),
+                 (f"soak_{TAG}.txt", f"{TAG}_soak.txt")):
+    shutil.copy(f"gpurun_out/{src}", f"{OUT}/{dst}")
 for src, dst in ((f"config3_{TAG}.json", f"{TAG}_config3_1b_packet_window.json"),
                  (f"config4_{TAG}.json", f"{TAG}_config4_ddos_contention.json"),
                  (f"config5_{TAG}.json", f"{TAG}_config5_accuracy_sweep.json"),
