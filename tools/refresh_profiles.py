@@ -117,9 +117,10 @@ hdr = rows[0]
 ki, vi = hdr.index('Kernel Name'), hdr.index('Metric Value')
 agg = collections.OrderedDict()
 for r in rows[1:]:
-    if 'dhsa::' not in r[ki]:
+    name = r[ki].replace('dhsa::', '').replace('void ', '')
+    if not name.startswith('k_'):      # this library's kernels (torch's generators and fills are not ours)
         continue
-    a = agg.setdefault(r[ki].split('(')[0][:62], [0, 0.0])
+    a = agg.setdefault(name.split('(')[0][:62], [0, 0.0])
     a[0] += 1
     a[1] += float(r[vi].replace(',', ''))
 tot = sum(a[1] for a in agg.values())
