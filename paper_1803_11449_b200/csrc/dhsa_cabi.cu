@@ -1625,7 +1625,18 @@ static uint64_t pow2_at_least(uint64_t v)
 // Workspaces of the stage chain: 64 bytes per partial key.  max_candidates is only a bound in the
 // reference (pkg/src/dhsa/dhla.py:34,269-273), and callers pass huge values for "unlimited", so the
 // buffers start at the default bound and grow when a stage needs more (restore_collect).
-static const uint64_t kInitialCandidates = 1ull << 20;  // DEFAULT_MAX_CANDIDATES, dhla.py:34
+static uint64_t initial_candidates()
+{
+    static const uint64_t v = [] {
+        uint64_t n = 1ull << 20;  // DEFAULT_MAX_CANDIDATES, dhla.py:34
+        if (const char *env = getenv("DHSA_INITIAL_CANDIDATES")) {  // tests shrink it to exercise the growth path
+            const long long q = strtoll(env, nullptr, 10);
+            if (q >= 1) n = (uint64_t)q;
+        }
+        return n;
+    }();
+    return v;
+}
 
 static int ensure_candidates(dhsa_sketch *s, uint64_t want)
 {
@@ -1664,8 +1675,9 @@ static uint64_t buffer_cap(const dhsa_sketch *s, uint64_t max_candidates)
 
 static int ensure_candidates_for(dhsa_sketch *s, uint64_t max_candidates)
 {
-    if (s->cand_cap >= max_candidates || s->cand_cap >= kInitialCandidates) return DHSA_OK;
-    return ensure_candidates(s, max_candidates < kInitialCandidates ? max_candidates : kInitialCandidates);
+    const uint64_t first = initial_candidates();
+    if (s->cand_cap >= max_candidates || s->cand_cap >= first) return DHSA_OK;
+    return ensure_candidates(s, max_candidates < first ? max_candidates : first);
 }
 
 // K2: zero counts of every cell.

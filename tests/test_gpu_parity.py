@@ -679,7 +679,7 @@ def _ipc_rank(rank, world, port, mode, q):
                                           for r in range(world)]),
                           np.concatenate([opp[packet_slice(len(cand), r, world)[0]:packet_slice(len(cand), r, world)[1]][::2]
                                           for r in range(world)]), threads=2)
-        ok = ok and used2 == used and len(win.ops._opened) == opened == world - 1 \
+        ok = ok and used2 == used and len(win.ops._opened) == opened == (world - 1 if mode == "p2p" else 0) \
             and np.array_equal(win.sketch.bits, ora2.bits)
         q.put((rank, used, bool(ok)))
         dist.barrier()
@@ -688,8 +688,8 @@ def _ipc_rank(rank, world, port, mode, q):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world", [2, 3])
-def test_sharded_window_merges_over_cuda_ipc_between_processes(world):
+@pytest.mark.parametrize("world, mode", [(2, "p2p"), (3, "p2p"), (2, "allgather")])
+def test_sharded_window_merges_over_cuda_ipc_between_processes(world, mode):
     """The real multi-process path -- one process per rank, sketches exported with
     cudaIpcGetMemHandle, peers mapped with cudaIpcOpenMemHandle, k_or_merge and
     k_copy_slice reading the mapped pointers -- with every rank on this one GPU
@@ -700,8 +700,8 @@ def test_sharded_window_merges_over_cuda_ipc_between_processes(world):
 
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
-    port = 29700 + os.getpid() % 1000 + world
-    procs = [ctx.Process(target=_ipc_rank, args=(r, world, port, "p2p", q)) for r in range(world)]
+    port = 29700 + os.getpid() % 1000 + world + (7 if mode == "allgather" else 0)
+    procs = [ctx.Process(target=_ipc_rank, args=(r, world, port, mode, q)) for r in range(world)]
     for p_ in procs:
         p_.start()
     results = [q.get(timeout=300) for _ in range(world)]
@@ -709,7 +709,7 @@ def test_sharded_window_merges_over_cuda_ipc_between_processes(world):
         p_.join(timeout=60)
         assert p_.exitcode == 0
     assert sorted(r[0] for r in results) == list(range(world))
-    assert all(used == "p2p" and ok for _, used, ok in results), results
+    assert all(used == mode and ok for _, used, ok in results), results
 
 
 def _nccl_single_rank(port, q):
@@ -757,3 +757,88 @@ def test_device_barrier_is_a_stream_ordered_nccl_all_reduce():
     p_.join(timeout=60)
     assert p_.exitcode == 0
     assert results == [True] * 4 and token == 0
+
+
+# ------------------------------------------ max_candidates is a bound, not an allocation --
+
+
+def test_huge_max_candidates_is_a_bound_not_an_allocation():
+    """The reference treats max_candidates purely as a bound (pkg/src/dhsa/dhla.py:34,269-273); callers pass
+    huge values for "unlimited".  The stage workspaces start at the default bound and grow on demand."""
+    sk = P.Dhla(P.DhgParams())
+    for n, host in enumerate((0x0A0B0C0D, 0xC63A1B02, 0x01020304)):
+        sk.update_batch(*O.plant_pairs(host, 2048 + 300 * n, 20 + n))
+    ora = O.OracleSketch()
+    for n, host in enumerate((0x0A0B0C0D, 0xC63A1B02, 0x01020304)):
+        ora.update_batch(*O.plant_pairs(host, 2048 + 300 * n, 20 + n))
+    want = ora.restore_superpoints(1024)
+    for bound in (1 << 40, 1 << 62):
+        got = sk.restore_superpoints(1024, max_candidates=bound)
+        assert [(r.host, r.saturated) for r in got] == [(r.host, r.saturated) for r in want]
+        assert sk._candidate_hosts(1024, max_candidates=bound).tolist() == sorted(r.host for r in want)
+    sk.restore_superpoints_begin(1024, max_candidates=1 << 40)
+    assert [r.host for r in sk.restore_superpoints_end()] == [r.host for r in want]
+
+
+_GROWTH_SCRIPT = r"""
+import json, sys
+sys.path.insert(0, sys.argv[1]); sys.path.insert(0, sys.argv[1] + "/tests")
+import numpy as np
+import paper_1803_11449_b200 as P
+from helpers import restore_cases, case_batches
+case = next(c for c in restore_cases() if c["name"] == "six_dense")
+sk = P.Dhla(P.DhgParams(**case["params"]))
+for c, o in case_batches(case):
+    sk.update_batch(c, o)
+out = {}
+got = sk.restore_superpoints(case["theta"], max_candidates=1 << 30)        # synchronous: grows and reruns
+out["stage_counts"] = sk.last_info["stage_counts"]
+out["reports"] = [[r.host, r.estimate, r.saturated] for r in got]
+out["candidates"] = sk._candidate_hosts(case["theta"], max_candidates=1 << 30).tolist()
+tiny = P.Dhla(P.DhgParams(r=6, g=512, k=12, alpha=5, seed_dh0=99))           # other seeds: a new sketch, small buffers
+for c, o in case_batches(case):
+    tiny.update_batch(c, o)
+tiny.restore_superpoints_begin(case["theta"], max_candidates=1 << 30)
+tiny.reset()                                                                 # the next window is already in the bits
+try:
+    tiny.restore_superpoints_end()
+    out["async_after_reset"] = "no error"
+except P.ConfigError as exc:
+    out["async_after_reset"] = str(exc)
+tiny2 = P.Dhla(P.DhgParams(r=6, g=512, k=12, alpha=5, seed_dh0=98))
+for c, o in case_batches(case):
+    tiny2.update_batch(c, o)
+tiny2.restore_superpoints_begin(case["theta"], max_candidates=1 << 30)       # untouched sketch: collected after growing
+out["async_untouched"] = len(tiny2.restore_superpoints_end())
+try:
+    sk.restore_superpoints(case["theta"], max_candidates=1000)               # the bound itself still raises
+    out["capacity"] = "no error"
+except P.CapacityError as exc:
+    out["capacity"] = str(exc)
+print(json.dumps(out))
+"""
+
+
+def test_stage_workspaces_grow_on_demand_and_the_counts_stay_exact():
+    """With the workspaces started at 4096 entries (DHSA_INITIAL_CANDIDATES), the dense six-array fixture --
+    stage survivors [91677, 167552, 296923, 462877] -- has to grow them several times; counts, candidates and
+    reports are the fixture's, a bound below the first stage still raises the reference's CapacityError, and a
+    pipelined read-out that cannot be rerun (the window was reset meanwhile) says so instead of truncating."""
+    import json
+    import os
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, DHSA_INITIAL_CANDIDATES="4096")
+    proc = subprocess.run([sys.executable, "-c", _GROWTH_SCRIPT, root], capture_output=True, text=True, env=env, timeout=600)
+    assert proc.returncode == 0, proc.stderr[-2000:]
+    out = json.loads(proc.stdout.strip().splitlines()[-1])
+    case = next(c for c in CASES if c["name"] == "six_dense")
+    assert out["stage_counts"] == case["stage_counts"] == [91677, 167552, 296923, 462877]
+    assert out["candidates"] == case["candidates"]
+    assert [(h, s) for h, _, s in out["reports"]] == [(h, s) for h, _, s in case["reports"]]
+    for (_, a, _), (_, b, _) in zip(out["reports"], case["reports"]):
+        assert a == pytest.approx(b, rel=REL_TOL)
+    assert out["capacity"] == "restore stage 1 produced 91677 partial keys (max_candidates=1000)"
+    assert "sketch was modified" in out["async_after_reset"] and out["async_untouched"] >= 0
