@@ -33,6 +33,30 @@ res = eng.run(got["records"])
 c = P.ExactCounter(expected_pairs=got["flows"])
 c.add_pairs(got["cand"], got["opp"])
 hosts, counts, n_pairs, n_hosts = c.result(min_count=1024)
+# round 2 kernels and paths: hash group forward/inverse, the re-filter, host batches through the slots from threads,
+# workspace growth, range download/upload (snapshot), zero_counts hand-in, a parked sketch handed out again
+from paper_1803_11449_b200 import dhg
+from concurrent.futures import ThreadPoolExecutor
+import io
+keys = np.arange(5000, dtype=np.uint64) * 977
+t = dhg.forward_many(P.DhgParams(), keys)
+k2, ok = dhg.reconstruct_many(P.DhgParams(), t)
+assert ok.all() and np.array_equal(k2, keys)
+sk = P.Dhla(P.DhgParams())
+with ThreadPoolExecutor(4) as pool:
+    for f in [pool.submit(sk.update_batch, cand[lo:lo + 3001], opp[lo:lo + 3001]) for lo in range(0, len(cand), 3001)]:
+        f.result()
+assert np.array_equal(sk.bits, ora.bits)
+assert len(sk.restore_superpoints(1024, max_candidates=1 << 40)) == len(want)
+zc = sk.zero_counts()
+assert [len(h) for h in sk.hot_sets(1024, zero_counts=zc)] == [len(h) for h in sk.hot_sets(1024)]
+buf = io.BytesIO()
+P.write_snapshot(sk, buf)
+buf.seek(0)
+assert np.array_equal(P.read_snapshot(buf).bits, ora.bits)
+del sk
+sk = P.Dhla(P.DhgParams())          # the parked one
+assert not sk.bits.any()
 print("sanitizer run ok:", [len(r.reports) for r in res], n_pairs, n_hosts)
 PY
 for tool in memcheck racecheck synccheck; do
