@@ -13,9 +13,10 @@ There is no CPU implementation in this package: without the CUDA library or a
 GPU every data-path call raises.
 """
 
+from . import dhg
 from .dhg import DhgParams
 from .dhla import (DEFAULT_MAX_CANDIDATES, Dhla, Estimate, SuperPointReport, hot_threshold,
-                   merge)
+                   merge, release_cached)
 from .engine import (DetectionEngine, TRACE_DTYPE, WindowConfig, WindowResult, WindowSession,
                      split_pairs)
 from .exact import EvalMetrics, ExactCounter, evaluate, exact_oracle
@@ -24,10 +25,10 @@ from .snapshot import read_snapshot, write_snapshot
 from .errors import (CapacityError, ConfigError, CudaError, DataError, DhsaError,
                      SealedWindowError)
 
-__version__ = "0.1.0"
+__version__ = "0.2.0"
 
 __all__ = [
-    "DhgParams", "Dhla", "SuperPointReport", "Estimate", "merge", "hot_threshold",
+    "DhgParams", "dhg", "Dhla", "SuperPointReport", "Estimate", "merge", "hot_threshold", "release_cached",
     "DEFAULT_MAX_CANDIDATES", "DetectionEngine", "WindowConfig", "WindowResult", "WindowSession",
     "split_pairs", "TRACE_DTYPE", "read_snapshot", "write_snapshot", "GeneratorConfig", "generate_trace", "generate_trace_device", "exact_oracle", "ExactCounter", "evaluate", "EvalMetrics", "DhsaError", "ConfigError", "DataError", "CapacityError",
     "SealedWindowError", "CudaError",

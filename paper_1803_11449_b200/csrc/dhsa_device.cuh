@@ -332,11 +332,21 @@ struct SoaSource {
             r.o = ld_stream_v4(opp4 + v, pol);
         }
     }
-    // staged form: one warp trip = 32 vectors = 512 B of cand then 512 B of opp in shared memory
-    static constexpr int kStageBytes = 1024;
-#ifndef DHSA_FC_SOA_STAGES
-#define DHSA_FC_SOA_STAGES 4
+    // staged form: one stage = kTrips warp trips = kTrips * 32 vectors of cand, then as many of opp, in shared
+    // memory; one mbarrier wait, one refill (two bulk copies) per stage
+#ifndef DHSA_FC_SOA_TRIPS
+#define DHSA_FC_SOA_TRIPS 4
 #endif
+#ifndef DHSA_FC_SOA_STAGES
+#define DHSA_FC_SOA_STAGES 2
+#endif
+#ifndef DHSA_FC_TRIP_UNROLL
+#define DHSA_FC_TRIP_UNROLL 1
+#endif
+#define DHSA_STR_(x) #x
+#define DHSA_UNROLL(n) _Pragma(DHSA_STR_(unroll n))
+    static constexpr int kTrips = DHSA_FC_SOA_TRIPS;
+    static constexpr int kStageBytes = 1024 * kTrips;
     static constexpr int kStages = DHSA_FC_SOA_STAGES;
     __device__ __forceinline__ void stage_issue(uint32_t smem_dst, uint32_t mbar, uint64_t base, uint32_t count,
                                                 uint64_t pol) const
@@ -344,12 +354,12 @@ struct SoaSource {
         const uint32_t bytes = count * 16u;
         mbar_expect_tx(mbar, 2u * bytes);
         bulk_g2s(smem_dst, cand4 + base, bytes, mbar, pol);
-        bulk_g2s(smem_dst + 512u, opp4 + base, bytes, mbar, pol);
+        bulk_g2s(smem_dst + 512u * kTrips, opp4 + base, bytes, mbar, pol);
     }
-    __device__ __forceinline__ void stage_read(Raw &r, const uint8_t *stage, uint32_t lane) const
+    __device__ __forceinline__ void stage_read(Raw &r, const uint8_t *stage, uint32_t idx) const
     {
-        r.c = *reinterpret_cast<const uint4 *>(stage + lane * 16u);
-        r.o = *reinterpret_cast<const uint4 *>(stage + 512u + lane * 16u);
+        r.c = *reinterpret_cast<const uint4 *>(stage + idx * 16u);
+        r.o = *reinterpret_cast<const uint4 *>(stage + 512u * kTrips + idx * 16u);
     }
     __device__ __forceinline__ void unpack(const Raw &r, uint64_t v, uint32_t (&cs)[4], uint32_t (&os)[4],
                                            bool (&ok)[4], uint32_t &, uint32_t &) const
@@ -394,9 +404,16 @@ struct RecordSource {
             r.c = ld_stream_v4(rec4 + 3 * v + 2, pol);
         }
     }
-    // staged form: one warp trip = 32 quads = 1536 contiguous bytes of records
-    static constexpr int kStageBytes = 1536;
-    static constexpr int kStages = 4;
+    // staged form: one warp trip = 32 quads = 1536 contiguous bytes of records; kTrips trips per stage
+#ifndef DHSA_FC_REC_TRIPS
+#define DHSA_FC_REC_TRIPS 2
+#endif
+#ifndef DHSA_FC_REC_STAGES
+#define DHSA_FC_REC_STAGES 2
+#endif
+    static constexpr int kTrips = DHSA_FC_REC_TRIPS;
+    static constexpr int kStageBytes = 1536 * kTrips;
+    static constexpr int kStages = DHSA_FC_REC_STAGES;
     __device__ __forceinline__ void stage_issue(uint32_t smem_dst, uint32_t mbar, uint64_t base, uint32_t count,
                                                 uint64_t pol) const
     {
@@ -404,9 +421,9 @@ struct RecordSource {
         mbar_expect_tx(mbar, bytes);
         bulk_g2s(smem_dst, rec4 + 3 * base, bytes, mbar, pol);
     }
-    __device__ __forceinline__ void stage_read(Raw &r, const uint8_t *stage, uint32_t lane) const
+    __device__ __forceinline__ void stage_read(Raw &r, const uint8_t *stage, uint32_t idx) const
     {
-        const uint4 *q = reinterpret_cast<const uint4 *>(stage + lane * 48u);
+        const uint4 *q = reinterpret_cast<const uint4 *>(stage + idx * 48u);
         r.a = q[0], r.b = q[1], r.c = q[2];
     }
     __device__ __forceinline__ void unpack(const Raw &r, uint64_t v, uint32_t (&cs)[4], uint32_t (&os)[4],
@@ -541,24 +558,15 @@ __global__ void __launch_bounds__(256) k_scan_vec4(SRC src, uint32_t *__restrict
 #ifndef DHSA_FC_CTAS_PER_SM
 #define DHSA_FC_CTAS_PER_SM 3
 #endif
-#ifndef DHSA_FC_DENSE_MISS
-#define DHSA_FC_DENSE_MISS 1
-#endif
-#if DHSA_FC_DENSE_MISS
 // A queued miss is just the key.  Everything only a miss needs -- the empty-way search, dh0, the R
 // word indices -- happens in the drain, where all 32 lanes hold a miss: in the lookup loop the same
 // code ran under `if (miss)` with one or two active lanes per warp (4% of the packets miss, so three
-// packet slots in four have at least one) and cost a quarter of the kernel's instructions.  The
-// drain re-reads the key's set (one more L2 sector per miss, +3% requests): it needs the ways to
-// pick the slot, and a key another warp recorded in the meantime turns into a hit there.
+// packet slots in four have at least one) and cost 7% of the kernel's instructions.  The drain
+// re-reads the key's set (one more L2 sector per miss, +3% requests): it needs the ways to pick the
+// slot, and a key another warp recorded in the meantime turns into a hit there (-20% REDs).
 struct FcMiss {
     uint32_t cand, h;
 };
-#else
-struct FcMiss {
-    uint32_t cand, h, slot;  // slot = set * 8 + way to fill, or DHSA_FC_NO_SLOT when the set was full
-};
-#endif
 
 // (set, entry) of a key in a table of 2^(32 - shift) sets
 __device__ __forceinline__ void fc_locate(const DevParams &p, uint32_t cand, uint32_t h, uint32_t &set, uint32_t &entry)
@@ -585,13 +593,12 @@ __device__ __forceinline__ uint32_t fc_pick_slot(const DevParams &p, const uint3
 }
 
 // Drain up to 32 queued misses, one per lane: the R test loads of a lane are in flight
-// together, REDs are warp-aggregated, then the key is recorded in the table.
+// together, then its REDs, then the key is recorded in the table.
 template <int R>
 __device__ __forceinline__ void fc_drain32(uint32_t *__restrict__ words, const DevParams &p, int wshift,
                                            const FcMiss *q, uint32_t n_active, uint32_t lane)
 {
     bool act = lane < n_active;
-#if DHSA_FC_DENSE_MISS
     FcMiss m = {0u, 0u};
     if (act) m = q[lane];
     uint32_t set, entry;
@@ -606,11 +613,6 @@ __device__ __forceinline__ void fc_drain32(uint32_t *__restrict__ words, const D
     for (int t = 0; t < 8; t++) hit |= way[t] == entry;
     act = act && !hit;  // recorded by another warp since the lookup: that warp issued its REDs
     const uint32_t slot = fc_pick_slot(p, way, set, entry);
-#else
-    FcMiss m = {0u, 0u, 0u};
-    if (act) m = q[lane];
-    const uint32_t slot = m.slot;
-#endif
     const uint32_t d0 = (uint32_t)mix64(p.state_dh0 ^ (uint64_t)m.cand) & p.kmask;
     const uint32_t mask = 1u << (m.h & 31u);
     uint32_t widx[R], w[R];
@@ -622,16 +624,14 @@ __device__ __forceinline__ void fc_drain32(uint32_t *__restrict__ words, const D
     const bool fresh = DHSA_FC_SKIP_TEST && slot != DHSA_FC_NO_SLOT;
 #pragma unroll
     for (int i = 0; i < R; i++) w[i] = act ? (fresh ? 0u : ld_sketch(words + widx[i])) : 0xFFFFFFFFu;
+    // Plain REDs, no warp aggregation: every drained key is new to the table and sets its own bit, so a word sees at
+    // most 32 REDs (plus lost-race duplicates) per window -- there is no same-address burst to merge, and five
+    // MATCH.ANY + shuffle rounds per drain were 10% of the kernel's stall samples.
 #pragma unroll
-    for (int i = 0; i < R; i++) red_or_aggregated(words, widx[i], mask, (w[i] & mask) == 0, lane);
+    for (int i = 0; i < R; i++)
+        if ((w[i] & mask) == 0) red_or(words + widx[i], mask);
     // the key now counts as scanned: its tests/REDs above are issued before this store
-    if (act && slot != DHSA_FC_NO_SLOT) {
-#if !DHSA_FC_DENSE_MISS
-        uint32_t set, entry;
-        fc_locate(p, m.cand, m.h, set, entry);
-#endif
-        st_fc_way(reinterpret_cast<uint32_t *>(p.fcache) + slot, entry);
-    }
+    if (act && slot != DHSA_FC_NO_SLOT) st_fc_way(reinterpret_cast<uint32_t *>(p.fcache) + slot, entry);
 }
 
 template <typename SRC>
@@ -663,7 +663,8 @@ __global__ void __launch_bounds__(256, DHSA_FC_CTAS_PER_SM) k_scan_flowcache(SRC
     const uint64_t nvec = src.vectors();
     const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
     const uint64_t warp0 = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    const uint64_t step = nwarps * 32;
+    constexpr uint32_t kPerStage = 32u * SRC::kTrips;  // vectors a warp takes per stage
+    const uint64_t step = nwarps * kPerStage;
     const int wshift = p.log2g - 5;
     const uint64_t pol = policy_evict_first();
     const uint32_t lt_mask = (1u << lane) - 1u;
@@ -677,35 +678,41 @@ __global__ void __launch_bounds__(256, DHSA_FC_CTAS_PER_SM) k_scan_flowcache(SRC
     }
     __syncwarp();
     // fill the ring
-    uint64_t issue_base = warp0 * 32;
+    uint64_t issue_base = warp0 * kPerStage;
     if (lane == 0) {
         for (int st = 0; st < SRC::kStages; st++) {
             if (issue_base < nvec) {
                 const uint64_t left = nvec - issue_base;
                 src.stage_issue(smem_u32(stage_s[wib][st]), smem_u32(&mbar_s[wib][st]), issue_base,
-                                (uint32_t)(left < 32 ? left : 32), pol);
+                                (uint32_t)(left < kPerStage ? left : kPerStage), pol);
             }
             issue_base += step;
         }
     }
     uint32_t slot = 0, parity = 0;
-    for (uint64_t base = warp0 * 32; base < nvec; base += step) {
+    for (uint64_t sbase = warp0 * kPerStage; sbase < nvec; sbase += step) {
         mbar_wait(smem_u32(&mbar_s[wib][slot]), parity);
+      DHSA_UNROLL(DHSA_FC_TRIP_UNROLL)
+      for (int tr = 0; tr < SRC::kTrips; tr++) {
+        const uint64_t base = sbase + 32u * tr;
+        if (base >= nvec) break;  // warp-uniform
         typename SRC::Raw raw;
-        src.stage_read(raw, stage_s[wib][slot], lane);
-        __syncwarp();
-        if (lane == 0) {  // the slot is free again: refill it with the trip kStages ahead
-            const uint64_t nb = base + (uint64_t)SRC::kStages * step;
-            if (nb < nvec) {
-                fence_proxy_async_smem();
-                const uint64_t left = nvec - nb;
-                src.stage_issue(smem_u32(stage_s[wib][slot]), smem_u32(&mbar_s[wib][slot]), nb,
-                                (uint32_t)(left < 32 ? left : 32), pol);
+        src.stage_read(raw, stage_s[wib][slot], lane + 32u * tr);
+        if (tr + 1 == SRC::kTrips || base + 32u >= nvec) {  // the stage's last trip has been read: refill the slot
+            __syncwarp();
+            if (lane == 0) {
+                const uint64_t nb = sbase + (uint64_t)SRC::kStages * step;
+                if (nb < nvec) {
+                    fence_proxy_async_smem();
+                    const uint64_t left = nvec - nb;
+                    src.stage_issue(smem_u32(stage_s[wib][slot]), smem_u32(&mbar_s[wib][slot]), nb,
+                                    (uint32_t)(left < kPerStage ? left : kPerStage), pol);
+                }
             }
-        }
-        if (++slot == SRC::kStages) {
-            slot = 0;
-            parity ^= 1u;
+            if (++slot == SRC::kStages) {
+                slot = 0;
+                parity ^= 1u;
+            }
         }
         uint32_t cs[4], os[4];
         bool ok[4];
@@ -734,11 +741,7 @@ __global__ void __launch_bounds__(256, DHSA_FC_CTAS_PER_SM) k_scan_flowcache(SRC
             const unsigned bal = __ballot_sync(0xFFFFFFFFu, miss);
             if (bal == 0) continue;
             if (miss) {
-#if DHSA_FC_DENSE_MISS
                 const FcMiss m = {cs[j], hs[j]};
-#else
-                const FcMiss m = {cs[j], hs[j], fc_pick_slot(p, way, set_idx[j], entry[j])};
-#endif
                 q[qn + __popc(bal & lt_mask)] = m;
             }
             qn += __popc(bal);
@@ -749,6 +752,7 @@ __global__ void __launch_bounds__(256, DHSA_FC_CTAS_PER_SM) k_scan_flowcache(SRC
             fc_drain32<R>(words, p, wshift, q + qn, 32, lane);
         }
         __syncwarp();
+      }
     }
     if (qn) fc_drain32<R>(words, p, wshift, q, qn, lane);
     unsigned long long hits64 = fc_hits, lookups64 = fc_lookups;

@@ -397,6 +397,13 @@ class Dhla:
         _cabi.check(self._lib.dhsa_or_merge(self._h, other._h))
 
 
+def release_cached() -> None:
+    """Free what destroyed sketches left parked for reuse (bit arrays, workspaces, page-locked slots).  The
+    reference builds a new Dhla per window (pkg/src/dhsa/engine.py:63); the library recycles them instead of paying
+    tens of milliseconds of allocation per window.  Call this to hand the memory back."""
+    _cabi.check(_cabi.lib().dhsa_release_cached())
+
+
 def merge(a: Dhla, b: Dhla) -> Dhla:
     """Union of two sketches with identical parameters (pkg/src/dhsa/dhla.py:305-318)."""
     if a.params != b.params:
