@@ -669,11 +669,14 @@ __global__ void __launch_bounds__(256, DHSA_FC_CTAS_PER_SM) k_scan_flowcache(SRC
     const uint64_t pol = policy_evict_first();
     const uint32_t lt_mask = (1u << lane) - 1u;
     const H1Consts hc = h1_consts(p.state_h1);
-    uint32_t fc_hits = 0, fc_lookups = 0;  // per thread and launch: far below 2^32
+    uint32_t fc_miss = 0, fc_trips = 0;  // per thread and launch: far below 2^32
     uint32_t on_time = 0, late = 0;
+    // this warp's stage ring and mbarriers as shared-window addresses
+    const uint32_t ring_a = smem_u32(stage_s[wib][0]);
+    const uint32_t mbar_a = smem_u32(&mbar_s[wib][0]);
 
     if (lane == 0) {
-        for (int st = 0; st < SRC::kStages; st++) mbar_init(smem_u32(&mbar_s[wib][st]), 1);
+        for (int st = 0; st < SRC::kStages; st++) mbar_init(mbar_a + 8u * st, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncwarp();
@@ -683,7 +686,7 @@ __global__ void __launch_bounds__(256, DHSA_FC_CTAS_PER_SM) k_scan_flowcache(SRC
         for (int st = 0; st < SRC::kStages; st++) {
             if (issue_base < nvec) {
                 const uint64_t left = nvec - issue_base;
-                src.stage_issue(smem_u32(stage_s[wib][st]), smem_u32(&mbar_s[wib][st]), issue_base,
+                src.stage_issue(ring_a + (uint32_t)SRC::kStageBytes * st, mbar_a + 8u * st, issue_base,
                                 (uint32_t)(left < kPerStage ? left : kPerStage), pol);
             }
             issue_base += step;
@@ -691,7 +694,7 @@ __global__ void __launch_bounds__(256, DHSA_FC_CTAS_PER_SM) k_scan_flowcache(SRC
     }
     uint32_t slot = 0, parity = 0;
     for (uint64_t sbase = warp0 * kPerStage; sbase < nvec; sbase += step) {
-        mbar_wait(smem_u32(&mbar_s[wib][slot]), parity);
+        mbar_wait(mbar_a + 8u * slot, parity);
       DHSA_UNROLL(DHSA_FC_TRIP_UNROLL)
       for (int tr = 0; tr < SRC::kTrips; tr++) {
         const uint64_t base = sbase + 32u * tr;
@@ -705,7 +708,7 @@ __global__ void __launch_bounds__(256, DHSA_FC_CTAS_PER_SM) k_scan_flowcache(SRC
                 if (nb < nvec) {
                     fence_proxy_async_smem();
                     const uint64_t left = nvec - nb;
-                    src.stage_issue(smem_u32(stage_s[wib][slot]), smem_u32(&mbar_s[wib][slot]), nb,
+                    src.stage_issue(ring_a + (uint32_t)SRC::kStageBytes * slot, mbar_a + 8u * slot, nb,
                                     (uint32_t)(left < kPerStage ? left : kPerStage), pol);
                 }
             }
@@ -717,6 +720,7 @@ __global__ void __launch_bounds__(256, DHSA_FC_CTAS_PER_SM) k_scan_flowcache(SRC
         uint32_t cs[4], os[4];
         bool ok[4];
         src.unpack(raw, base + lane, cs, os, ok, on_time, late);
+        fc_trips += base + lane < nvec;
 
         unsigned long long e[4][4];
         uint32_t set_idx[4], entry[4], hs[4];
@@ -734,10 +738,8 @@ __global__ void __launch_bounds__(256, DHSA_FC_CTAS_PER_SM) k_scan_flowcache(SRC
             bool hit = false;
 #pragma unroll
             for (int t = 0; t < 8; t++) hit |= way[t] == entry[j];
-            hit = hit && ok[j];
             const bool miss = ok[j] && !hit;
-            fc_hits += hit;
-            fc_lookups += ok[j];
+            fc_miss += miss;
             const unsigned bal = __ballot_sync(0xFFFFFFFFu, miss);
             if (bal == 0) continue;
             if (miss) {
@@ -755,7 +757,10 @@ __global__ void __launch_bounds__(256, DHSA_FC_CTAS_PER_SM) k_scan_flowcache(SRC
       }
     }
     if (qn) fc_drain32<R>(words, p, wshift, q, qn, lane);
-    unsigned long long hits64 = fc_hits, lookups64 = fc_lookups;
+    // lookups = the packets this lane examined (on-time records of a record source: unpack counted them; every packet
+    // of its vectors otherwise), hits = lookups - misses
+    unsigned long long lookups64 = SRC::kTally ? on_time : 4u * fc_trips;
+    unsigned long long hits64 = lookups64 - fc_miss;
     for (int d = 16; d > 0; d >>= 1) {
         hits64 += __shfl_xor_sync(0xFFFFFFFFu, hits64, d);
         lookups64 += __shfl_xor_sync(0xFFFFFFFFu, lookups64, d);
