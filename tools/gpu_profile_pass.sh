@@ -26,5 +26,5 @@ timeout 600 python tools/host_feed_probe.py > gpurun_out/feed_probe_${TAG}.json 
 timeout 300 python tools/l2_probe.py > gpurun_out/l2_probe_${TAG}.json 2> gpurun_out/l2_probe.err
 timeout 600 python tests/checks/soak.py 120 > gpurun_out/soak_${TAG}.txt 2>&1
 timeout 600 python tests/checks/soak_engine.py 90 >> gpurun_out/soak_${TAG}.txt 2>&1
-tail -3 gpurun_out/pytest_gpu.log; tail -2 gpurun_out/smoke.log; cat gpurun_out/bench_${TAG}.json gpurun_out/bench_${TAG}_reference.json; tail -2 gpurun_out/ncu_full.log
-tail -3 gpurun_out/config3.err gpurun_out/config4.err gpurun_out/config5.err gpurun_out/tools.err gpurun_out/soak_${TAG}.txt
+tail -n 3 gpurun_out/pytest_gpu.log; tail -n 2 gpurun_out/smoke.log; cat gpurun_out/bench_${TAG}.json gpurun_out/bench_${TAG}_reference.json | cut -c1-600; tail -n 2 gpurun_out/ncu_full.log
+for f in gpurun_out/config3.err gpurun_out/config4.err gpurun_out/config5.err gpurun_out/tools.err gpurun_out/soak_${TAG}.txt; do tail -n 3 $f | cut -c1-300; done
