@@ -317,6 +317,11 @@ int dhsa_ipc_export(dhsa_sketch_t *s, uint8_t handle_out[64]);
 int dhsa_ipc_open(int device, const uint8_t handle[64], void **bits_dev);
 int dhsa_ipc_close(int device, void *bits_dev);
 
+/* Host-only self test of the helper-thread copy pool behind dhsa_update_host (no CUDA call, runs
+ * without a GPU): `threads` concurrent callers x `iterations` two-array copies of random sizes up to
+ * bytes_each, each verified; *mismatches = copies that differed from their source. */
+int dhsa_selftest_copy_pool(uint64_t bytes_each, int iterations, int threads, uint64_t *mismatches);
+
 /* ---- measurement -------------------------------------------------------------
  * Random-address L2 probe used for the scan roofline: `ops` 32-bit operations at
  * hashed word addresses inside a `buffer_bytes` buffer.  kind 0 = atomic OR

@@ -102,6 +102,7 @@ SIGNATURES = {
     "dhsa_ipc_export": [_vp, _vp],
     "dhsa_ipc_open": [C.c_int, _vp, C.POINTER(_vp)],
     "dhsa_ipc_close": [C.c_int, _vp],
+    "dhsa_selftest_copy_pool": [_u64, C.c_int, C.c_int, C.POINTER(_u64)],
     "dhsa_probe_l2": [C.c_int, C.c_int, _u64, _u64, C.POINTER(C.c_double)],
 }
 

@@ -1109,6 +1109,36 @@ private:
     unsigned n_helpers_ = 0;
 };
 
+// Host-only self test of the copy pool (no CUDA call): `threads` callers issue `iterations` two-array copies of
+// random sizes up to bytes_each between private buffers at once -- one of them gets the helpers, the others
+// copy alone -- and every copy is compared with its source.  The CPU test suite runs it (tests/test_host_logic.py).
+extern "C" int dhsa_selftest_copy_pool(uint64_t bytes_each, int iterations, int threads, uint64_t *mismatches)
+{
+    NEED(mismatches);
+    *mismatches = 0;
+    if (bytes_each < 64 || iterations < 1 || threads < 1 || threads > 64)
+        return fail(DHSA_ECONFIG, "self test needs bytes_each >= 64, iterations >= 1, 1 <= threads <= 64");
+    std::atomic<uint64_t> bad{0};
+    std::vector<std::thread> pool;
+    for (int t = 0; t < threads; t++)
+        pool.emplace_back([&, t] {
+            std::vector<uint8_t> s0(bytes_each), s1(bytes_each), d0(bytes_each), d1(bytes_each);
+            uint64_t x = 0x9E3779B97F4A7C15ull * (uint64_t)(t + 1);
+            for (int it = 0; it < iterations; it++) {
+                x ^= x << 13, x ^= x >> 7, x ^= x << 17;
+                const size_t n = 64 + (size_t)(x % (bytes_each - 63));
+                for (size_t i = 0; i < n; i += 61) s0[i] = (uint8_t)(x >> (i & 31)), s1[i] = (uint8_t)(~x >> (i & 15));
+                memset(d0.data(), 0xA5, n);
+                memset(d1.data(), 0x5A, n);
+                CopyPool::get().copy2(d0.data(), s0.data(), d1.data(), s1.data(), n);
+                if (memcmp(d0.data(), s0.data(), n) != 0 || memcmp(d1.data(), s1.data(), n) != 0) bad.fetch_add(1);
+            }
+        });
+    for (auto &th : pool) th.join();
+    *mismatches = bad.load();
+    return DHSA_OK;
+}
+
 static bool is_pageable(const void *p)
 {
     cudaPointerAttributes a;
@@ -1989,7 +2019,9 @@ extern "C" int dhsa_candidate_hosts(dhsa_sketch_t *s, double theta, uint64_t max
     if (int rc = flush_host_locked(s)) return rc;
     if (int rc = ensure_readout(s)) return rc;
     if (int rc = ensure_candidates_for(s, max_candidates)) return rc;
+    const bool zc_given = s->zc_given;  // a rerun after growing the workspaces starts from the same zero counts
     for (;;) {
+        s->zc_given = zc_given;
         if (int rc = launch_estimate(s, theta)) return rc;
         if (int rc = launch_restore_stages(s, max_candidates, true, nullptr)) return rc;
         k_sort_small<<<1, 1024, DHSA_SORT_SMEM_MAX * sizeof(uint64_t), s->stream>>>(s->keys, &s->ctl->n_candidates, s->ctl,

@@ -190,3 +190,16 @@ def test_library_has_no_device_function_host_stubs_on_call_paths():
     _cabi.lib()
     asm = subprocess.run(["objdump", "-d", "--no-show-raw-insn", _build.LIB_PATH], capture_output=True, text=True).stdout
     assert "<exit@plt>" not in asm.replace("<__cxa_atexit@plt>", "")
+
+
+@pytest.mark.parametrize("threads", [1, 3, 8])
+def test_copy_pool_is_exact_under_concurrent_callers(threads):
+    """The helper-thread pool that copies host batches into the page-locked slots (lock-free share claims,
+    helpers that go to sleep and wake late): every byte of every copy arrives, whoever shares the pool.
+    Host-only: runs without a GPU."""
+    lib = _cabi.lib()
+    bad = C.c_uint64(12345)
+    _cabi.check(lib.dhsa_selftest_copy_pool(1 << 20, 400, threads, C.byref(bad)))
+    assert bad.value == 0
+    _cabi.check(lib.dhsa_selftest_copy_pool(200_000, 3000, threads, C.byref(bad)))     # small jobs: share count varies
+    assert bad.value == 0
