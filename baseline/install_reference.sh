@@ -17,6 +17,11 @@ cp -r "$SRC" "$TMP/pkg"
 rm -rf "$HERE/_ref"
 python -m pip install --no-index --no-build-isolation --no-deps --find-links /opt/wheelhouse \
     --target "$HERE/_ref" "$TMP/pkg"
+# the reference's own test files travel too (git-ignored like _ref): tests/test_gpu_reference_suite.py
+# runs them, unmodified, against the CUDA sketch on the GPU box
+rm -rf "$HERE/_ref_tests"
+mkdir -p "$HERE/_ref_tests"
+cp "$SRC"/tests/*.py "$HERE/_ref_tests/"
 rm -rf "$TMP"
 python - <<PY
 import sys

@@ -8,11 +8,12 @@ window_id=)``, ``update_batch``, ``window_id`` and ``restore_superpoints(theta,
 max_candidates=, workers=)``.
 
 Every data-path method is a call into libdhsa_b200.so (include/dhsa_b200.h);
-Python only moves arguments and shapes results.  The one contract that differs
-from the reference is ``bits``: the array lives in HBM, so the attribute is a
-host *copy* taken after the sketch's stream drains, and ``load_bits`` is the
-explicit write (the reference writes ``sketch.bits[...]`` in place,
-pkg/src/dhsa/dhla.py:372, pkg/tests/test_dhla.py:88-90).
+Python only moves arguments and shapes results.  The one contract that needs
+care is ``bits``: the array lives in HBM, so the attribute is a host mirror
+taken after the sketch's stream drains.  The reference writes ``sketch.bits[...]``
+in place (pkg/src/dhsa/dhla.py:372, pkg/tests/test_dhla.py:88-90,139); the mirror
+is therefore write-through -- an item assignment into it (or into a view of it)
+uploads the mirror to the device -- and ``load_bits`` is the explicit bulk write.
 """
 
 from __future__ import annotations
@@ -59,8 +60,43 @@ def _default_device() -> int:
     return int(env) if env not in (None, "") else 0
 
 
+def _same_params(a, b) -> bool:
+    """Field-wise equality: a sketch may carry the reference's own DhgParams record (dhg.py:59-76)."""
+    return DhgParams.coerce(a) == DhgParams.coerce(b)
+
+
 def _is_cuda_tensor(x) -> bool:
     return hasattr(x, "data_ptr") and getattr(x, "is_cuda", False)
+
+
+class DeviceBits(np.ndarray):
+    """Host mirror of a device sketch's bit array, as ``Dhla.bits`` returns it.
+
+    Reading is plain numpy.  ``mirror[...] = value`` -- on the mirror itself or on any view of it
+    (``sketch.bits[1, 9, 80] = 0x7F``, ``sketch.bits[i] = cells``) -- also uploads the mirror, so
+    code written against the reference's live host array (pkg/src/dhsa/dhla.py:64-67,372) keeps
+    working.  Every such write moves the whole array (10 MiB at the defaults) over PCIe: edit a
+    plain copy and call ``load_bits`` once for anything bulky.  Copies and arithmetic results are
+    ordinary detached arrays.
+    """
+
+    _sketch = None  # the Dhla a write goes back to
+    _root = None    # the whole (r, 2^k, g/8) mirror this array is (a view of)
+
+    def __array_finalize__(self, obj):
+        if isinstance(obj, DeviceBits) and obj._sketch is not None and self.base is not None \
+                and np.shares_memory(self, obj):
+            self._sketch, self._root = obj._sketch, obj._root
+        else:
+            self._sketch = self._root = None
+
+    def __setitem__(self, key, value):
+        super().__setitem__(key, value)
+        if self._sketch is not None:
+            self._sketch.load_bits(np.asarray(self._root))
+
+    def __reduce__(self):  # pickles as a plain array: a handle to a device sketch does not travel
+        return np.asarray(self).__reduce__()
 
 
 class Dhla:
@@ -164,11 +200,14 @@ class Dhla:
 
     @property
     def bits(self) -> np.ndarray:
-        """Host copy, shape (r, 2^k, g/8) uint8, the reference's layout."""
+        """Host mirror, shape (r, 2^k, g/8) uint8, the reference's layout; item assignment
+        writes through to the device (DeviceBits)."""
         p = self.params
         out = np.empty((p.r, p.index_count, p.g // 8), dtype=np.uint8)
         _cabi.check(self._lib.dhsa_download_bits(self._h, out.ctypes.data, out.nbytes))
-        return out
+        mirror = out.view(DeviceBits)
+        mirror._sketch, mirror._root = self, mirror
+        return mirror
 
     def estimator(self, i: int, j: int) -> np.ndarray:
         """The g/8 bytes of estimator j of array i (pkg/src/dhsa/dhla.py:107-109).  A copy: the
@@ -390,7 +429,7 @@ class Dhla:
 
     def merge_from(self, other: "Dhla") -> None:
         """self |= other, on the device (peer access when the devices differ)."""
-        if self.params != other.params:
+        if not _same_params(self.params, other.params):
             raise ConfigError(
                 f"cannot merge sketches with different parameters: {self.params} vs {other.params}"
             )
@@ -406,7 +445,7 @@ def release_cached() -> None:
 
 def merge(a: Dhla, b: Dhla) -> Dhla:
     """Union of two sketches with identical parameters (pkg/src/dhsa/dhla.py:305-318)."""
-    if a.params != b.params:
+    if not _same_params(a.params, b.params):
         raise ConfigError(
             f"cannot merge sketches with different parameters: {a.params} vs {b.params}"
         )

@@ -132,3 +132,28 @@ def test_restore_capacity_overflow_aborts_loudly_with_the_reference_text():
         sk.restore_superpoints(1024, max_candidates=100)
     assert str(got.value) == str(want.value)
     assert len(sk.restore_superpoints(1024)) == 40          # the default budget restores them all
+
+
+def test_in_place_writes_to_bits_reach_the_device():
+    # the reference paints cells through the live array (pkg/tests/test_dhla.py:85-95; test_kernels.py:53-59)
+    p = P.DhgParams()
+    sk = P.Dhla(p)
+    sk.bits[0, 5, :81] = 0xFF        # 648 ones -> 376 zeros
+    sk.bits[1, 9, :80] = 0xFF
+    sk.bits[1, 9, 80] = 0x7F         # 647 ones -> 377 zeros
+    zc = sk.zero_counts()
+    assert zc[0, 5] == 376 and zc[1, 9] == 377 and int(zc.sum()) == p.r * p.index_count * p.g - 648 - 647
+    hot = sk.hot_sets(1024)
+    assert 5 in hot[0] and 9 not in hot[1]
+    small = P.DhgParams(r=3, g=8, k=8, alpha=8, key_width=16)
+    sk = P.Dhla(small)
+    paint = np.random.default_rng(4).integers(0, 256, size=sk.bits.shape, dtype=np.uint8)
+    sk.bits[:] = paint
+    assert np.array_equal(sk.bits, paint)
+    assert np.array_equal(sk.zero_counts(), small.g - np.unpackbits(paint, axis=2).sum(axis=2))
+    copy = sk.bits.copy()
+    copy[:] = 0                      # a copy is detached
+    assert np.array_equal(sk.bits, paint)
+    # a scan after a painted upload still lands (the flow cache was emptied by the upload)
+    sk.update_batch(np.array([1, 2, 3], np.uint32), np.array([4, 5, 6], np.uint32))
+    assert np.array_equal(sk.bits & paint, paint)

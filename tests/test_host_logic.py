@@ -3,6 +3,7 @@ import ctypes as C
 import os
 import re
 
+import numpy as np
 import pytest
 
 import paper_1803_11449_b200 as P
@@ -203,3 +204,66 @@ def test_copy_pool_is_exact_under_concurrent_callers(threads):
     assert bad.value == 0
     _cabi.check(lib.dhsa_selftest_copy_pool(200_000, 3000, threads, C.byref(bad)))     # small jobs: share count varies
     assert bad.value == 0
+
+
+def test_bits_mirror_writes_through_and_copies_detach():
+    """Dhla.bits is a write-through host mirror (the reference writes sketch.bits[...] in place,
+    pkg/tests/test_dhla.py:88-90,139; test_kernels.py:57): item assignment on the mirror or a view
+    uploads it, copies and arithmetic results are detached.  Host-only: a stand-in sketch."""
+    from paper_1803_11449_b200.dhla import DeviceBits
+
+    class Sketch:
+        def __init__(self):
+            self.dev, self.uploads = np.zeros((2, 4, 8), np.uint8), 0
+
+        def load_bits(self, a):
+            self.dev[...] = a
+            self.uploads += 1
+
+        @property
+        def bits(self):
+            m = self.dev.copy().view(DeviceBits)
+            m._sketch, m._root = self, m
+            return m
+
+    s = Sketch()
+    s.bits[0, 1, :3] = 0xFF
+    assert s.dev[0, 1, :3].tolist() == [255] * 3 and s.uploads == 1
+    s.bits[:] = 1
+    assert s.dev.sum() == s.dev.size and s.uploads == 2
+    view = s.bits[1]
+    view[0, 0] = 7                                   # a view writes the whole mirror back
+    assert s.dev[1, 0, 0] == 7 and s.dev[0].sum() == 32 and s.uploads == 3
+    detached = s.bits.copy()
+    detached[0, 0, 0] = 9
+    (s.bits | 1)[0, 0, 0] = 9
+    np.asarray(s.bits)[0, 0, 0] = 9
+    assert s.uploads == 3 and s.dev[0, 0, 0] == 1
+    assert np.array_equal(s.bits, s.dev) and len(s.bits.tobytes()) == s.dev.size
+    import pickle
+
+    assert type(pickle.loads(pickle.dumps(s.bits))) is np.ndarray
+
+
+def test_exceptions_derive_from_the_reference_classes_when_it_is_importable():
+    """`except dhsa.errors.CapacityError` in a host application must catch what the CUDA sketch
+    raises (errors.py); without the reference on the path the hierarchy stands alone."""
+    import subprocess
+    import sys
+
+    import refpkg
+    import paper_1803_11449_b200.errors as E
+
+    for name, bases in (("ConfigError", (E.DhsaError, ValueError)), ("DataError", (E.DhsaError,)),
+                        ("CapacityError", (E.DhsaError,)), ("SealedWindowError", (E.DhsaError, RuntimeError)),
+                        ("CudaError", (E.DhsaError, RuntimeError))):
+        assert all(issubclass(getattr(E, name), b) for b in bases), name
+    if not refpkg.available():
+        pytest.skip("baseline/_ref not installed (bash baseline/install_reference.sh)")
+    code = ("import sys; sys.path[:0] = [%r, %r]\n"
+            "import dhsa.errors as R, paper_1803_11449_b200.errors as E\n"
+            "for n in ('DhsaError', 'ConfigError', 'DataError', 'CapacityError', 'SealedWindowError'):\n"
+            "    assert issubclass(getattr(E, n), getattr(R, n)) and issubclass(getattr(E, n), E.DhsaError), n\n"
+            "assert issubclass(E.ConfigError, ValueError) and issubclass(E.CudaError, R.DhsaError)\n"
+            % (ROOT, refpkg.REF_DIR))
+    subprocess.run([sys.executable, "-c", code], check=True)
