@@ -352,7 +352,13 @@ def run_ours(args, rank: int, local_rank: int, world: int) -> None:
         ora = O.OracleSketch()
         ora.update_batch(src, dst, threads=os.cpu_count() or 1)
         want = ora.restore_superpoints(THETA)
-        bits_ok = (n * world >= flows) and sha(sk.bits) == sha(ora.bits)
+        if win.merged_with == "partition":   # the merged bits stay with their owners: this rank checks its own range and
+            from paper_1803_11449_b200.multi import partition_ranges   # the gathered zero counts of every cell
+            blo, bhi = partition_ranges(win.ops, world)[rank]
+            bits_ok = (n * world >= flows) and sha(sk.bits.reshape(-1)[blo:bhi]) == sha(ora.bits.reshape(-1)[blo:bhi]) \
+                and bool(np.array_equal(sk.zero_counts(), ora.zero_counts()))
+        else:
+            bits_ok = (n * world >= flows) and sha(sk.bits) == sha(ora.bits)
         sp_ok = [(r.host, r.saturated) for r in reports] == [(r.host, r.saturated) for r in want] and \
             all(abs(a.estimate - b.estimate) <= 1e-6 * abs(b.estimate) for a, b in zip(reports, want))
         parity = {"bits_equal_oracle": bool(bits_ok), "superpoints_equal_oracle": bool(sp_ok),
@@ -695,7 +701,7 @@ def main() -> None:
     ap.add_argument("--seed", type=int, default=100)
     ap.add_argument("--scan-mode", default="auto", choices=["red", "test", "test_agg", "flow_cache", "auto"])
     ap.add_argument("--flow-cache-mib", type=int, default=32, help="flow cache size; flow_cache mode only")
-    ap.add_argument("--merge", default="auto", choices=["auto", "p2p", "allgather"])
+    ap.add_argument("--merge", default="auto", choices=["auto", "p2p", "partition", "allgather"])
     ap.add_argument("--cpu-sample", type=int, default=100_000_000,
                     help="packets of the window the in-run CPU baseline scans (default: the whole config-2 window)")
     ap.add_argument("--config", type=int, default=2, choices=[2, 3],

@@ -312,6 +312,29 @@ int dhsa_copy_slice_from_peer(dhsa_sketch_t *dst, const void *peer_bits_dev, uin
 /* dst |= bits_dev (a whole sketch image already on this device, e.g. one slot of an
  * NCCL all-gather buffer). */
 int dhsa_or_merge_buffer(dhsa_sketch_t *dst, const void *bits_dev, uint64_t nbytes);
+/* Partitioned read-out (BASELINE.json north star: "estimation and restore are partitioned by cell range";
+ * SURVEY.md section 8e "K2 over the GPU's own cell range").  After dhsa_or_merge_peers rank q holds the
+ * merged byte range q.  Instead of all-gathering the merged bits, each rank counts the zeros of ITS range
+ * (the per-range half of Backend.zero_counts, pkg/src/dhsa/_core.pyx:89-118), the counts are gathered
+ * (4 bytes per cell instead of g/8), and the cells a candidate's re-estimation ANDs together
+ * (shared_zero_counts, pkg/src/dhsa/dhla.py:136-143) are read from their owners through the peer-mapped
+ * sketch pointers.  Ranges are byte ranges of the sketch on cell boundaries (multiples of g/8).
+ *   dhsa_zero_counts_range             zero counts of the cells in [byte_lo, byte_hi) into the sketch's
+ *                                      device-side counts (stream-ordered; the other cells are left alone)
+ *   dhsa_zero_counts_offset            where those counts live, as a byte offset from the sketch's base
+ *                                      pointer: they share the allocation -- and the IPC handle -- of the bits
+ *   dhsa_gather_zero_counts_from_peer  counts of the cells in [byte_lo, byte_hi) copied from a peer's sketch
+ *   dhsa_set_cell_owners               n_owners > 0: until it is called again with 0, every read-out call on
+ *                                      this handle (restore, candidate hosts, hot sets, shared zero counts)
+ *                                      takes the zero counts as gathered and reads cells [byte_cuts[q],
+ *                                      byte_cuts[q+1]) from bits_dev[q] (this rank's own base pointer for its
+ *                                      own range).  dhsa_download_bits still returns the local array only. */
+int dhsa_zero_counts_range(dhsa_sketch_t *s, uint64_t byte_lo, uint64_t byte_hi);
+int dhsa_zero_counts_offset(const dhsa_sketch_t *s, uint64_t *byte_offset);
+int dhsa_gather_zero_counts_from_peer(dhsa_sketch_t *s, const void *peer_bits_dev, uint64_t byte_lo,
+                                      uint64_t byte_hi);
+int dhsa_set_cell_owners(dhsa_sketch_t *s, const void *const *bits_dev, const uint64_t *byte_cuts,
+                         int n_owners);
 /* CUDA IPC plumbing so one-process-per-GPU ranks can map each other's bit arrays. */
 int dhsa_ipc_export(dhsa_sketch_t *s, uint8_t handle_out[64]);
 int dhsa_ipc_open(int device, const uint8_t handle[64], void **bits_dev);

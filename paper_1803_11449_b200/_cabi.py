@@ -99,6 +99,10 @@ SIGNATURES = {
     "dhsa_or_merge_peers": [_vp, C.POINTER(_vp), C.c_int, _u64, _u64],
     "dhsa_copy_slice_from_peer": [_vp, _vp, _u64, _u64],
     "dhsa_or_merge_buffer": [_vp, _vp, _u64],
+    "dhsa_zero_counts_range": [_vp, _u64, _u64],
+    "dhsa_zero_counts_offset": [_vp, C.POINTER(_u64)],
+    "dhsa_gather_zero_counts_from_peer": [_vp, _vp, _u64, _u64],
+    "dhsa_set_cell_owners": [_vp, C.POINTER(_vp), C.POINTER(_u64), C.c_int],
     "dhsa_ipc_export": [_vp, _vp],
     "dhsa_ipc_open": [C.c_int, _vp, C.POINTER(_vp)],
     "dhsa_ipc_close": [C.c_int, _vp],

@@ -116,8 +116,10 @@ struct dhsa_sketch {
     Readback *rb, *rb_host;  // control block + window counters + first report rows: device, and its pinned mirror
     Control *ctl;           // = &rb->c
     Control *ctl_host;      // = &rb_host->c
-    int32_t *zc;            // ncell
+    int32_t *zc;            // ncell; lives behind the bit array and the window counters, inside the same allocation, so
+                            // a peer that has the sketch mapped can read this rank's zero counts too
     bool zc_given;          // s->zc holds counts handed in by the caller for the next read-out call
+    CellOwners owners;      // n > 0: partitioned read-out -- zero counts as gathered into s->zc, cells from their owners
     uint32_t *lists;        // r * 2^k
     uint32_t *bitmaps;      // r * bitmap_words
     uint64_t bitmap_words;  // per array
@@ -254,9 +256,10 @@ static int validate(const dhsa_params_t *p)
 extern "C" int dhsa_abi_version(void) { return DHSA_ABI_VERSION; }
 extern "C" const char *dhsa_last_error(void) { return g_err; }
 
+static uint64_t zero_counts_bytes(const dhsa_sketch *s) { return (s->dp.ncell * sizeof(int32_t) + 15) & ~15ull; }
+
 static void free_workspaces(dhsa_sketch *s)
 {
-    cudaFree(s->zc);
     cudaFree(s->lists);
     cudaFree(s->bitmaps);
     for (int b = 0; b < 2; b++) {
@@ -269,7 +272,7 @@ static void free_workspaces(dhsa_sketch *s)
     cudaFree(s->reports);
     cudaFree(s->hosts_in);
     cudaFree(s->sz_out);
-    s->zc = nullptr, s->lists = nullptr, s->bitmaps = nullptr, s->keys = nullptr, s->packed = nullptr, s->cand_sz = nullptr;
+    s->lists = nullptr, s->bitmaps = nullptr, s->keys = nullptr, s->packed = nullptr, s->cand_sz = nullptr;
     s->reports = nullptr, s->hosts_in = nullptr, s->sz_out = nullptr;
     s->sub[0] = s->sub[1] = nullptr, s->cl0[0] = s->cl0[1] = nullptr;
     s->cand_cap = s->packed_cap = s->hosts_in_cap = 0;
@@ -296,7 +299,9 @@ static int create_locked(dhsa_sketch *s, const dhsa_params_t *params, int device
     s->bitmap_words = m >= 32 ? m / 32 : 1;
     // the window's counters (record tally, flow-cache statistics) sit right behind the
     // bit array, so a window reset is ONE memset
-    CU(cudaMalloc(&s->bits, s->alloc_bytes + kCounterBytes));
+    // [bits | window counters | zero counts]: one allocation, one CUDA IPC handle for everything a peer reads
+    CU(cudaMalloc(&s->bits, s->alloc_bytes + kCounterBytes + zero_counts_bytes(s)));
+    s->zc = reinterpret_cast<int32_t *>(s->bits + s->alloc_bytes + kCounterBytes);
     CU(cudaStreamCreateWithFlags(&s->own_stream, cudaStreamNonBlocking));
     CU(cudaStreamCreateWithFlags(&s->copy_stream, cudaStreamNonBlocking));
     s->stream = s->own_stream;
@@ -361,6 +366,7 @@ static int scrub_for_parking(dhsa_sketch *s)
     s->launches = 0;
     s->restore_pending = false;
     s->zc_given = false;
+    s->owners.n = 0;
     CU(cudaMemsetAsync(s->bits, 0, s->alloc_bytes + kCounterBytes, s->stream));
     if (int rc = clear_flow_cache_locked(s, false)) return rc;
     CU(cudaStreamSynchronize(s->stream));
@@ -1628,8 +1634,7 @@ extern "C" int dhsa_upload_bits(dhsa_sketch_t *s, const uint8_t *bits_host, uint
 
 static int ensure_readout(dhsa_sketch *s)
 {
-    if (s->zc) return DHSA_OK;
-    CU(cudaMalloc(&s->zc, s->dp.ncell * sizeof(int32_t)));
+    if (s->lists) return DHSA_OK;
     CU(cudaMalloc(&s->lists, s->dp.ncell * sizeof(uint32_t)));
     CU(cudaMalloc(&s->bitmaps, (uint64_t)s->params.r * s->bitmap_words * sizeof(uint32_t)));
     return DHSA_OK;
@@ -1710,19 +1715,21 @@ static int ensure_candidates_for(dhsa_sketch *s, uint64_t max_candidates)
     return ensure_candidates(s, max_candidates < first ? max_candidates : first);
 }
 
-// K2: zero counts of every cell.
-static int launch_zero_counts(dhsa_sketch *s)
+// K2: zero counts of the cells [cell_lo, cell_hi) -- every cell, or this rank's range of a partitioned read-out.
+static int launch_zero_counts(dhsa_sketch *s, uint64_t cell_lo, uint64_t cell_hi)
 {
-    const uint64_t bpe = (uint64_t)s->params.g / 8;
+    if (cell_lo >= cell_hi) return DHSA_OK;
+    const uint64_t bpe = (uint64_t)s->params.g / 8, ncell = cell_hi - cell_lo;
+    const uint8_t *first = s->bits + cell_lo * bpe;
     if (bpe >= 16) {
         const int vecs = (int)(bpe / 16);
         const int lanes = vecs < 32 ? vecs : 32;
-        const int grid = grid_for(s, s->dp.ncell * (uint64_t)lanes, 256, 8);
-        k_zero_counts_vec<<<grid, 256, 0, s->stream>>>(reinterpret_cast<const uint4 *>(s->bits), s->zc, s->dp.ncell,
+        const int grid = grid_for(s, ncell * (uint64_t)lanes, 256, 8);
+        k_zero_counts_vec<<<grid, 256, 0, s->stream>>>(reinterpret_cast<const uint4 *>(first), s->zc + cell_lo, ncell,
                                                        vecs, lanes, s->params.g);
     } else {
-        const int grid = grid_for(s, s->dp.ncell, 256, 8);
-        k_zero_counts_small<<<grid, 256, 0, s->stream>>>(s->bits, s->zc, s->dp.ncell, (int)bpe, s->params.g);
+        const int grid = grid_for(s, ncell, 256, 8);
+        k_zero_counts_small<<<grid, 256, 0, s->stream>>>(first, s->zc + cell_lo, ncell, (int)bpe, s->params.g);
     }
     s->launches++;
     CU(cudaGetLastError());
@@ -1821,7 +1828,9 @@ static int launch_estimate(dhsa_sketch *s, double theta)
     if (int rc = ensure_readout(s)) return rc;
     if (s->zc_given) {
         s->zc_given = false;  // the caller's zero counts are already in s->zc (dhsa_use_zero_counts)
-    } else if (int rc = launch_zero_counts(s)) {
+    } else if (s->owners.n > 0) {
+        // partitioned read-out: s->zc was counted range by range on the owners and gathered (multi.py)
+    } else if (int rc = launch_zero_counts(s, 0, s->dp.ncell)) {
         return rc;
     }
     k_hot_sets<<<s->params.r, 1024, 0, s->stream>>>(s->zc, hot_cut(s, theta), theta, s->params.r, s->params.k,
@@ -2068,7 +2077,10 @@ extern "C" int dhsa_shared_zero_counts(dhsa_sketch_t *s, const uint64_t *hosts_h
     }
     CU(cudaMemcpyAsync(s->hosts_in, hosts_host, n * sizeof(uint64_t), cudaMemcpyHostToDevice, s->stream));
     const int grid = grid_for(s, n * 32, 256, 8);
-    k_shared_zero_counts<<<grid, 256, 0, s->stream>>>(s->bits, s->dp, s->hosts_in, n, s->sz_out);
+    if (s->owners.n > 0)
+        k_shared_zero_counts_owned<<<grid, 256, 0, s->stream>>>(s->owners, s->dp, s->hosts_in, n, s->sz_out);
+    else
+        k_shared_zero_counts<<<grid, 256, 0, s->stream>>>(s->bits, s->dp, s->hosts_in, n, s->sz_out);
     s->launches++;
     CU(cudaGetLastError());
     int32_t *tmp = (int32_t *)malloc(n * sizeof(int32_t));
@@ -2094,9 +2106,14 @@ static int enqueue_restore(dhsa_sketch *s, double theta, uint64_t max_candidates
     if (int rc = launch_restore_stages(s, max_candidates, false, &cur)) return rc;
     const int grid = s->sm_count * DHSA_READOUT_CTAS_PER_SM;
     // verify + re-estimate, then sort + emit: two launches for what were four
-    k_verify_reestimate<<<grid, 256, 0, s->stream>>>(s->params.r - 2, s->dp, buffer_cap(s, max_candidates), max_candidates,
-                                                     s->sub[cur], s->cl0[cur], s->bits, s->keys, s->cand_sz, s->packed,
-                                                     s->ctl);
+    if (s->owners.n > 0)
+        k_verify_reestimate_owned<<<grid, 256, 0, s->stream>>>(s->params.r - 2, s->dp, buffer_cap(s, max_candidates),
+                                                               max_candidates, s->sub[cur], s->cl0[cur], s->owners, s->keys,
+                                                               s->cand_sz, s->packed, s->ctl);
+    else
+        k_verify_reestimate<<<grid, 256, 0, s->stream>>>(s->params.r - 2, s->dp, buffer_cap(s, max_candidates),
+                                                         max_candidates, s->sub[cur], s->cl0[cur], s->bits, s->keys,
+                                                         s->cand_sz, s->packed, s->ctl);
     // sort + emit; as the last kernel it also gathers the window counters (6 words behind the bit array) and
     // the first report rows behind the control block: ONE copy brings everything the host reads back
     k_sort_small<<<1, 1024, DHSA_SORT_SMEM_MAX * sizeof(uint64_t), s->stream>>>(
@@ -2114,7 +2131,7 @@ static int run_restore(dhsa_sketch *s, double theta, uint64_t max_candidates)
 {
     if (int rc = ensure_readout(s)) return rc;
     if (int rc = ensure_candidates_for(s, max_candidates)) return rc;
-    if (!s->graph_disabled) {
+    if (!s->graph_disabled && s->owners.n == 0) {  // (a partitioned read-out launches its kernels directly)
         const bool fresh = s->restore_graph && s->graph_theta == theta &&
                            s->graph_max_candidates == max_candidates && s->graph_cand_cap == s->cand_cap;
         if (!fresh) {
@@ -2472,6 +2489,96 @@ extern "C" int dhsa_or_merge_buffer(dhsa_sketch_t *dst, const void *bits_dev, ui
     const uint64_t aligned = nbytes & ~15ull;
     if (aligned != nbytes) return fail(DHSA_ECONFIG, "sketch size %llu is not a multiple of 16 bytes", (unsigned long long)nbytes);
     return merge_range_locked(dst, peers, 1, 0, aligned);
+}
+
+// ---- partitioned read-out (multi-GPU) -----------------------------------------------------------
+// After the OR reduce-scatter rank q holds the merged byte range q.  Instead of all-gathering the
+// merged bits (10 MiB per sketch), each rank counts the zeros of its own range, the counts are
+// gathered (4 bytes per cell), and the few cells the candidates' re-estimation needs are read from
+// their owners through the peer-mapped pointers.
+
+extern "C" int dhsa_zero_counts_offset(const dhsa_sketch_t *s, uint64_t *byte_offset)
+{
+    NEED(s);
+    NEED(byte_offset);
+    *byte_offset = s->alloc_bytes + kCounterBytes;  // from the sketch's base pointer (dhsa_bits_device_ptr / dhsa_ipc_open)
+    return DHSA_OK;
+}
+
+static int cell_range_of(const dhsa_sketch *s, uint64_t byte_lo, uint64_t byte_hi, uint64_t *cell_lo, uint64_t *cell_hi)
+{
+    const uint64_t bpe = (uint64_t)s->params.g / 8;
+    if (byte_lo > byte_hi || byte_hi > s->alloc_bytes) return fail(DHSA_ECONFIG, "cell range out of bounds");
+    if (byte_hi > s->nbytes) byte_hi = s->nbytes;  // the padding of the last range holds no cell
+    if (byte_lo > byte_hi) byte_lo = byte_hi;
+    if (byte_lo % bpe || byte_hi % bpe)
+        return fail(DHSA_ECONFIG, "cell range [%llu, %llu) does not fall on %llu-byte cell boundaries",
+                    (unsigned long long)byte_lo, (unsigned long long)byte_hi, (unsigned long long)bpe);
+    *cell_lo = byte_lo / bpe, *cell_hi = byte_hi / bpe;
+    return DHSA_OK;
+}
+
+extern "C" int dhsa_zero_counts_range(dhsa_sketch_t *s, uint64_t byte_lo, uint64_t byte_hi)
+{
+    NEED(s);
+    uint64_t lo, hi;
+    if (int rc = cell_range_of(s, byte_lo, byte_hi, &lo, &hi)) return rc;
+    std::lock_guard<std::mutex> lk(s->mu);
+    if (int rc = use_device(s)) return rc;
+    if (int rc = refuse_if_restore_pending(s)) return rc;
+    if (int rc = flush_host_locked(s)) return rc;
+    return launch_zero_counts(s, lo, hi);
+}
+
+extern "C" int dhsa_gather_zero_counts_from_peer(dhsa_sketch_t *s, const void *peer_bits_dev, uint64_t byte_lo,
+                                                 uint64_t byte_hi)
+{
+    NEED(s);
+    NEED(peer_bits_dev);
+    uint64_t lo, hi;
+    if (int rc = cell_range_of(s, byte_lo, byte_hi, &lo, &hi)) return rc;
+    if (lo == hi) return DHSA_OK;
+    std::lock_guard<std::mutex> lk(s->mu);
+    if (int rc = use_device(s)) return rc;
+    if (int rc = refuse_if_restore_pending(s)) return rc;
+    const uint32_t *src = reinterpret_cast<const uint32_t *>(static_cast<const uint8_t *>(peer_bits_dev) + s->alloc_bytes +
+                                                             kCounterBytes);
+    k_copy_words<<<grid_for(s, hi - lo, 256, 8), 256, 0, s->stream>>>(reinterpret_cast<uint32_t *>(s->zc), src, lo, hi);
+    s->launches++;
+    CU(cudaGetLastError());
+    return DHSA_OK;
+}
+
+extern "C" int dhsa_set_cell_owners(dhsa_sketch_t *s, const void *const *bits_dev, const uint64_t *byte_cuts, int n_owners)
+{
+    NEED(s);
+    if (n_owners < 0 || n_owners > DHSA_MAX_OWNERS)
+        return fail(DHSA_ECONFIG, "owner count must be 0..%d (got %d)", DHSA_MAX_OWNERS, n_owners);
+    CellOwners own;
+    memset(&own, 0, sizeof own);
+    if (n_owners > 0) {
+        NEED(bits_dev);
+        NEED(byte_cuts);
+        const uint64_t bpe = (uint64_t)s->params.g / 8;
+        if (byte_cuts[0] != 0 || byte_cuts[n_owners] < s->nbytes)
+            return fail(DHSA_ECONFIG, "owner ranges must cover the sketch: [%llu, %llu) of %llu bytes",
+                        (unsigned long long)byte_cuts[0], (unsigned long long)byte_cuts[n_owners],
+                        (unsigned long long)s->nbytes);
+        for (int q = 0; q < n_owners; q++) {
+            if (!bits_dev[q]) return fail(DHSA_ECONFIG, "owner %d has no sketch pointer", q);
+            if (byte_cuts[q] > byte_cuts[q + 1] || (byte_cuts[q + 1] < s->nbytes && byte_cuts[q + 1] % bpe))
+                return fail(DHSA_ECONFIG, "owner cut %llu is not an ascending %llu-byte cell boundary",
+                            (unsigned long long)byte_cuts[q + 1], (unsigned long long)bpe);
+            own.base[q] = static_cast<const uint8_t *>(bits_dev[q]);
+            own.cut[q] = byte_cuts[q];
+        }
+        own.cut[n_owners] = byte_cuts[n_owners];
+        own.n = n_owners;
+    }
+    std::lock_guard<std::mutex> lk(s->mu);
+    if (int rc = refuse_if_restore_pending(s)) return rc;
+    s->owners = own;
+    return DHSA_OK;
 }
 
 extern "C" int dhsa_ipc_export(dhsa_sketch_t *s, uint8_t handle_out[64])

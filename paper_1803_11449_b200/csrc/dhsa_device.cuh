@@ -1367,9 +1367,48 @@ __global__ void __launch_bounds__(256) k_verify_keys(int n_stages, DevParams p, 
 
 // ------------------------------- K4: re-estimate + threshold filter + order --
 
+// Multi-GPU, partitioned read-out: after the OR reduce-scatter the merged copy of byte range q of the
+// sketch lives on rank q only (multi.py merge_partitioned).  A kernel that needs a candidate's cells
+// reads each from its owner, over NVLink through the peer-mapped sketch pointers, instead of every
+// rank first copying the whole merged sketch.  Cuts fall on cell boundaries.
+#define DHSA_MAX_OWNERS 16
+struct CellOwners {
+    const uint8_t *base[DHSA_MAX_OWNERS];  // start of owner q's sketch (this rank's own bits for q = rank)
+    uint64_t cut[DHSA_MAX_OWNERS + 1];     // owner q holds bytes [cut[q], cut[q + 1])
+    int n;
+};
+
+template <bool OWNED>
+__device__ __forceinline__ const uint8_t *cell_bytes(const uint8_t *__restrict__ bits, const CellOwners &own, uint64_t off)
+{
+    if (!OWNED) return bits + off;
+    int q = 0;
+    while (q + 1 < own.n && off >= own.cut[q + 1]) q++;
+    return own.base[q] + off;
+}
+
+template <bool OWNED>
+__device__ __forceinline__ uint4 ld_cell_v4(const uint8_t *ptr)
+{
+    if (!OWNED) return *reinterpret_cast<const uint4 *>(ptr);
+    uint4 x;  // possibly peer memory: past L1, like k_or_merge
+    asm volatile("ld.global.cv.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(x.x), "=r"(x.y), "=r"(x.z), "=r"(x.w) : "l"(ptr));
+    return x;
+}
+
+template <bool OWNED>
+__device__ __forceinline__ uint32_t ld_cell_u8(const uint8_t *ptr)
+{
+    if (!OWNED) return *ptr;
+    uint32_t x;
+    asm volatile("ld.global.cv.u8 %0, [%1];" : "=r"(x) : "l"(ptr));
+    return x;
+}
+
 // SZ of one key: g - popcount(AND of its r cells) (pkg/src/dhsa/dhla.py:136-143).
 // One warp per key, 16-byte vectors when cells are at least 16 bytes wide.
-__device__ __forceinline__ int shared_zero_count_warp(const uint8_t *__restrict__ bits,
+template <bool OWNED>
+__device__ __forceinline__ int shared_zero_count_warp(const uint8_t *__restrict__ bits, const CellOwners &own,
                                                       const DevParams &p, uint64_t key, uint32_t lane)
 {
     const uint32_t d0 = dh0_of(p, key);
@@ -1381,7 +1420,7 @@ __device__ __forceinline__ int shared_zero_count_warp(const uint8_t *__restrict_
             uint4 acc = make_uint4(~0u, ~0u, ~0u, ~0u);
             for (int i = 0; i < p.r; i++) {
                 const uint64_t cell = ((uint64_t)i << p.k) | index_of(p, key, d0, i);
-                const uint4 q = *reinterpret_cast<const uint4 *>(bits + cell * bpe + (uint64_t)v * 16);
+                const uint4 q = ld_cell_v4<OWNED>(cell_bytes<OWNED>(bits, own, cell * bpe) + (uint64_t)v * 16);
                 acc.x &= q.x, acc.y &= q.y, acc.z &= q.z, acc.w &= q.w;
             }
             ones += __popc(acc.x) + __popc(acc.y) + __popc(acc.z) + __popc(acc.w);
@@ -1391,7 +1430,7 @@ __device__ __forceinline__ int shared_zero_count_warp(const uint8_t *__restrict_
             uint32_t acc = 0xFFu;
             for (int i = 0; i < p.r; i++) {
                 const uint64_t cell = ((uint64_t)i << p.k) | index_of(p, key, d0, i);
-                acc &= bits[cell * bpe + b];
+                acc &= ld_cell_u8<OWNED>(cell_bytes<OWNED>(bits, own, cell * bpe) + b);
             }
             ones += __popc(acc);
         }
@@ -1400,16 +1439,31 @@ __device__ __forceinline__ int shared_zero_count_warp(const uint8_t *__restrict_
     return (int)g - ones;
 }
 
-__global__ void __launch_bounds__(256) k_shared_zero_counts(const uint8_t *__restrict__ bits, DevParams p,
-                                                            const uint64_t *__restrict__ keys, uint64_t n,
-                                                            int32_t *__restrict__ sz)
+template <bool OWNED>
+__device__ __forceinline__ void shared_zero_counts_body(const uint8_t *__restrict__ bits, const CellOwners &own,
+                                                        const DevParams &p, const uint64_t *__restrict__ keys, uint64_t n,
+                                                        int32_t *__restrict__ sz)
 {
     const uint32_t lane = threadIdx.x & 31u;
     const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
     for (uint64_t t = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; t < n; t += nwarps) {
-        const int z = shared_zero_count_warp(bits, p, keys[t], lane);
+        const int z = shared_zero_count_warp<OWNED>(bits, own, p, keys[t], lane);
         if (lane == 0) sz[t] = z;
     }
+}
+
+__global__ void __launch_bounds__(256) k_shared_zero_counts(const uint8_t *__restrict__ bits, DevParams p,
+                                                            const uint64_t *__restrict__ keys, uint64_t n,
+                                                            int32_t *__restrict__ sz)
+{
+    shared_zero_counts_body<false>(bits, CellOwners(), p, keys, n, sz);
+}
+
+__global__ void __launch_bounds__(256) k_shared_zero_counts_owned(CellOwners own, DevParams p,
+                                                                  const uint64_t *__restrict__ keys, uint64_t n,
+                                                                  int32_t *__restrict__ sz)
+{
+    shared_zero_counts_body<true>(nullptr, own, p, keys, n, sz);
 }
 
 // Sort key of one report.  The reference orders by (-estimate, host)
@@ -1430,10 +1484,12 @@ __device__ __forceinline__ uint64_t pack_report(int sz, double denom, uint64_t h
 // _candidate_hosts), then SZ and the threshold filter (dhla.py:183-194) as the integer compare
 // max(SZ, 1) <= ctl->sz_cut.  Every verified key is kept with its SZ (keys[], cand_sz[]) so the
 // filter can be re-applied with another cut without touching the bits again (k_refilter).
+template <bool OWNED>
 __device__ __forceinline__ void verify_reestimate_body(int n_stages, const DevParams &p, unsigned long long buf_cap,
                                                        const uint64_t *__restrict__ in_sub,
                                                        const uint32_t *__restrict__ in_cl0,
-                                                       const uint8_t *__restrict__ bits, uint64_t *__restrict__ keys,
+                                                       const uint8_t *__restrict__ bits, const CellOwners &own,
+                                                       uint64_t *__restrict__ keys,
                                                        int32_t *__restrict__ cand_sz, uint64_t *__restrict__ packed,
                                                        Control *ctl, uint64_t warp, uint64_t nwarps)
 {
@@ -1446,7 +1502,7 @@ __device__ __forceinline__ void verify_reestimate_body(int n_stages, const DevPa
         const uint64_t sub = in_sub[q];
         if (sub >> p.key_width) continue;           // warp-uniform
         if (dh0_of(p, sub) != in_cl0[q]) continue;  // warp-uniform
-        const int sz = shared_zero_count_warp(bits, p, sub, lane);
+        const int sz = shared_zero_count_warp<OWNED>(bits, own, p, sub, lane);
         if (lane == 0) {
             const unsigned long long pos = atomicAdd(&ctl->n_candidates, 1ull);  // < np <= buf_cap
             keys[pos] = sub;
@@ -1465,8 +1521,23 @@ __global__ void __launch_bounds__(256) k_verify_reestimate(int n_stages, DevPara
                                                            uint64_t *__restrict__ packed, Control *ctl)
 {
     if (blockIdx.x == 0 && threadIdx.x == 0) record_capacity_failure(ctl, n_stages, buf_cap, max_candidates);
-    verify_reestimate_body(n_stages, p, buf_cap, in_sub, in_cl0, bits, keys, cand_sz, packed, ctl,
-                           ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5, ((uint64_t)gridDim.x * blockDim.x) >> 5);
+    verify_reestimate_body<false>(n_stages, p, buf_cap, in_sub, in_cl0, bits, CellOwners(), keys, cand_sz, packed, ctl,
+                                  ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5,
+                                  ((uint64_t)gridDim.x * blockDim.x) >> 5);
+}
+
+// the same with every candidate cell read from the rank that owns its merged copy
+__global__ void __launch_bounds__(256) k_verify_reestimate_owned(int n_stages, DevParams p, unsigned long long buf_cap,
+                                                                 unsigned long long max_candidates,
+                                                                 const uint64_t *__restrict__ in_sub,
+                                                                 const uint32_t *__restrict__ in_cl0, CellOwners own,
+                                                                 uint64_t *__restrict__ keys, int32_t *__restrict__ cand_sz,
+                                                                 uint64_t *__restrict__ packed, Control *ctl)
+{
+    if (blockIdx.x == 0 && threadIdx.x == 0) record_capacity_failure(ctl, n_stages, buf_cap, max_candidates);
+    verify_reestimate_body<true>(n_stages, p, buf_cap, in_sub, in_cl0, nullptr, own, keys, cand_sz, packed, ctl,
+                                 ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5,
+                                 ((uint64_t)gridDim.x * blockDim.x) >> 5);
 }
 
 // The filter again, over the verified keys and their SZ, with a cut handed in by the host
@@ -1644,6 +1715,18 @@ __global__ void __launch_bounds__(256) k_copy_slice(uint4 *__restrict__ dst, con
                      : "=r"(x.x), "=r"(x.y), "=r"(x.z), "=r"(x.w)
                      : "l"(src + v));
         dst[v] = x;
+    }
+}
+
+// all-gather of the per-range zero counts (int32 per cell) from a peer's counts region
+__global__ void __launch_bounds__(256) k_copy_words(uint32_t *__restrict__ dst, const uint32_t *__restrict__ src,
+                                                    uint64_t lo, uint64_t hi)
+{
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t w = lo + (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; w < hi; w += stride) {
+        uint32_t x;
+        asm volatile("ld.global.cv.u32 %0, [%1];" : "=r"(x) : "l"(src + w));
+        dst[w] = x;
     }
 }
 

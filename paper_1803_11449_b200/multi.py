@@ -11,6 +11,15 @@ window shards by packets with no data-path collective during the scan:
             all-gather             -- rank p copies the merged range q from peer q
     restore runs on the merged sketch (microseconds; every rank holds the result)
 
+or, with ``merge="partition"`` (the north star's "estimation and restore are partitioned by cell
+range"): the all-gather of merged bits is replaced by
+
+    rank p counts the zeros of ITS merged range (K2 over its own cells)
+    all-gather of the zero counts   -- 4 bytes per cell instead of g/8: 327 KB instead of 10 MiB
+    restore                         -- the stage chain works from the counts alone; the r cells of
+                                       each surviving candidate are read from the ranks that own
+                                       them, over the same peer-mapped pointers
+
 ``torch.distributed`` is plumbing only: rendezvous, the 64-byte IPC handle
 exchange and barriers.  If peer mapping is unavailable the merge falls back to
 ``all_gather_into_tensor`` of whole sketches over NCCL followed by the local OR
@@ -113,6 +122,8 @@ class CudaMergeOps:
         return int(ptr.value)
 
     def close_handles(self) -> None:
+        if self.sketch._h:   # the owner table points into the mappings that go away below
+            self._lib.dhsa_set_cell_owners(self.sketch._h, None, None, 0)
         for ptr in self._opened:
             self._lib.dhsa_ipc_close(self.sketch.device, C.c_void_p(ptr))
         self._opened = []
@@ -123,6 +134,25 @@ class CudaMergeOps:
 
     def copy_from_peer(self, peer_ptr: int, lo: int, hi: int) -> None:
         _cabi.check(self._lib.dhsa_copy_slice_from_peer(self.sketch._h, C.c_void_p(peer_ptr), lo, hi))
+
+    # partitioned read-out
+    @property
+    def cell_bytes(self) -> int:
+        return self.sketch.params.g // 8
+
+    def own_pointer(self) -> int:
+        return self.sketch.bits_device_ptr
+
+    def zero_counts_range(self, lo: int, hi: int) -> None:
+        _cabi.check(self._lib.dhsa_zero_counts_range(self.sketch._h, lo, hi))
+
+    def gather_zero_counts(self, peer_ptr: int, lo: int, hi: int) -> None:
+        _cabi.check(self._lib.dhsa_gather_zero_counts_from_peer(self.sketch._h, C.c_void_p(peer_ptr), lo, hi))
+
+    def set_cell_owners(self, ptrs: Sequence[int], cuts: Sequence[int]) -> None:
+        arr = (C.c_void_p * len(ptrs))(*ptrs)
+        cut = (C.c_uint64 * len(cuts))(*cuts)
+        _cabi.check(self._lib.dhsa_set_cell_owners(self.sketch._h, arr, cut, len(ptrs)))
 
     # all-gather fallback: whole sketch images as torch tensors on this device
     def bits_tensor(self):
@@ -202,6 +232,33 @@ def merge_p2p(ops, dist, group=None) -> None:
     _barrier(ops, dist, group)    # nobody resets while a peer still reads
 
 
+def partition_ranges(ops, world: int) -> List[Tuple[int, int]]:
+    """Byte ranges of a partitioned read-out: as byte_ranges, cut on cell boundaries."""
+    return byte_ranges(ops.alloc_bytes, world, align=max(16, ops.cell_bytes))
+
+
+def merge_partitioned(ops, dist, group=None) -> None:
+    """Reduce-scatter(OR), then zero counts per owner and an all-gather of the COUNTS; the merged
+    bits stay where they were reduced and the read-out reads candidate cells from their owners.
+    Collective.  [barrier][k_or_merge][k_zero_counts over the own range][barrier][k_copy_words x (P-1)];
+    the caller puts a barrier behind the read-out (ShardedWindow.restore), because peers read this
+    rank's cells until their read-out is done."""
+    world, rank = dist.get_world_size(group), dist.get_rank(group)
+    if world == 1:
+        return
+    ranges = partition_ranges(ops, world)
+    ptrs = peer_pointers(ops, dist, group)
+    _barrier(ops, dist, group)    # my scan has landed, and so has everyone's
+    lo, hi = ranges[rank]
+    ops.or_from_peers([ptrs[q] for q in sorted(ptrs)], lo, hi)
+    ops.zero_counts_range(lo, hi)
+    _barrier(ops, dist, group)    # every owner's range and its counts are final
+    for q in sorted(ptrs):
+        ops.gather_zero_counts(ptrs[q], *ranges[q])
+    bases = [ops.own_pointer() if q == rank else ptrs[q] for q in range(world)]
+    ops.set_cell_owners(bases, [ranges[0][0]] + [r[1] for r in ranges])
+
+
 def merge_allgather(ops, dist, group=None) -> None:
     """Fallback: NCCL all-gather of whole sketches, then the local OR kernel.  Collective.
 
@@ -232,8 +289,8 @@ class ShardedWindow:
                  max_candidates: int = DEFAULT_MAX_CANDIDATES, merge: str = "auto"):
         import torch.distributed as dist
 
-        if merge not in ("auto", "p2p", "allgather"):
-            raise ConfigError(f"merge must be auto, p2p or allgather (got {merge!r})")
+        if merge not in ("auto", "p2p", "partition", "allgather"):
+            raise ConfigError(f"merge must be auto, p2p, partition or allgather (got {merge!r})")
         self._dist = dist
         self.group = group
         self.theta = theta
@@ -261,18 +318,18 @@ class ShardedWindow:
             self.merged_with = "none"
             return self.merged_with
         mode = self.merge_mode
-        if mode in ("auto", "p2p"):
-            ok = self._try_p2p()
+        if mode in ("auto", "p2p", "partition"):
+            ok = self._try_p2p(partition=mode == "partition")
             if ok:
-                self.merged_with = "p2p"
+                self.merged_with = "partition" if mode == "partition" else "p2p"
                 return self.merged_with
-            if mode == "p2p":
+            if mode != "auto":
                 raise ConfigError("peer-mapped merge requested but CUDA IPC mapping failed on some rank")
         merge_allgather(self.ops, self._dist, self.group)
         self.merged_with = "allgather"
         return self.merged_with
 
-    def _try_p2p(self) -> bool:
+    def _try_p2p(self, partition: bool = False) -> bool:
         import torch
 
         dist = self._dist
@@ -302,7 +359,7 @@ class ShardedWindow:
                 except Exception:
                     pass
         if self._p2p_ok:
-            merge_p2p(self.ops, dist, self.group)
+            (merge_partitioned if partition else merge_p2p)(self.ops, dist, self.group)
         return self._p2p_ok
 
     def close(self) -> None:
@@ -315,12 +372,22 @@ class ShardedWindow:
         except Exception:
             pass
 
+    def _after_readout(self) -> None:
+        """Partitioned read-out: peers read this rank's cells until their read-out is done, so nobody
+        goes on to the next window's reset before everybody's is queued behind a barrier."""
+        if self.merged_with == "partition":
+            _barrier(self.ops, self._dist, self.group)
+
     def restore(self):
-        return self.sketch.restore_superpoints(self.theta, max_candidates=self.max_candidates)
+        try:
+            return self.sketch.restore_superpoints(self.theta, max_candidates=self.max_candidates)
+        finally:
+            self._after_readout()
 
     def restore_begin(self) -> None:
         """Enqueue the read-out; the next window's reset() + scan() may follow before restore_end()."""
         self.sketch.restore_superpoints_begin(self.theta, max_candidates=self.max_candidates)
+        self._after_readout()
 
     def restore_end(self):
         return self.sketch.restore_superpoints_end()

@@ -665,9 +665,22 @@ def _ipc_rank(rank, world, port, mode, q):
         ora = O.OracleSketch()
         ora.update_batch(cand, opp, threads=2)
         want = ora.restore_superpoints(1024)
+        if mode == "partition":
+            # the merged bits stay with their owners: this rank holds its own range, reads the zero counts as
+            # gathered and every candidate cell from the rank that owns it
+            from paper_1803_11449_b200.multi import partition_ranges
+            blo, bhi = partition_ranges(win.ops, world)[rank]
+            mine = np.array_equal(win.sketch.bits.reshape(-1)[blo:bhi], ora.bits.reshape(-1)[blo:bhi])
+            hosts = np.array([r.host for r in want] + [12345], dtype=np.uint64)
+            mine = (mine and np.array_equal(win.sketch.zero_counts(), ora.zero_counts())
+                    and np.array_equal(win.sketch.shared_zero_counts(hosts), ora.shared_zero_counts(hosts))
+                    and np.array_equal(win.sketch._candidate_hosts(1024), ora.candidate_hosts(1024)))
+        else:
+            mine = np.array_equal(win.sketch.bits, ora.bits)
         got = win.restore()
-        ok = (np.array_equal(win.sketch.bits, ora.bits)
+        ok = (mine
               and [(r.host, r.saturated) for r in got] == [(r.host, r.saturated) for r in want]
+              and all(abs(a.estimate - b.estimate) <= 1e-6 * b.estimate for a, b in zip(got, want))
               and len(got) == 3)
         # a second window on the same sketches: peers stay mapped, the agreed merge kind is reused
         opened = len(win.ops._opened)
@@ -679,8 +692,13 @@ def _ipc_rank(rank, world, port, mode, q):
                                           for r in range(world)]),
                           np.concatenate([opp[packet_slice(len(cand), r, world)[0]:packet_slice(len(cand), r, world)[1]][::2]
                                           for r in range(world)]), threads=2)
-        ok = ok and used2 == used and len(win.ops._opened) == opened == (world - 1 if mode == "p2p" else 0) \
-            and np.array_equal(win.sketch.bits, ora2.bits)
+        ok = ok and used2 == used and len(win.ops._opened) == opened == (0 if mode == "allgather" else world - 1)
+        if mode == "partition":
+            got2, want2 = win.restore(), ora2.restore_superpoints(1024)
+            ok = ok and np.array_equal(win.sketch.zero_counts(), ora2.zero_counts()) \
+                and [(r.host, r.saturated) for r in got2] == [(r.host, r.saturated) for r in want2]
+        else:
+            ok = ok and np.array_equal(win.sketch.bits, ora2.bits)
         q.put((rank, used, bool(ok)))
         dist.barrier()
         win.close()
@@ -688,7 +706,7 @@ def _ipc_rank(rank, world, port, mode, q):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world, mode", [(2, "p2p"), (3, "p2p"), (2, "allgather")])
+@pytest.mark.parametrize("world, mode", [(2, "p2p"), (3, "p2p"), (2, "allgather"), (2, "partition"), (3, "partition")])
 def test_sharded_window_merges_over_cuda_ipc_between_processes(world, mode):
     """The real multi-process path -- one process per rank, sketches exported with
     cudaIpcGetMemHandle, peers mapped with cudaIpcOpenMemHandle, k_or_merge and
@@ -700,7 +718,7 @@ def test_sharded_window_merges_over_cuda_ipc_between_processes(world, mode):
 
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
-    port = 29700 + os.getpid() % 1000 + world + (7 if mode == "allgather" else 0)
+    port = 29700 + os.getpid() % 1000 + world + {"p2p": 0, "allgather": 7, "partition": 13}[mode]
     procs = [ctx.Process(target=_ipc_rank, args=(r, world, port, mode, q)) for r in range(world)]
     for p_ in procs:
         p_.start()

@@ -16,7 +16,8 @@ import torch.distributed as dist
 import torch.multiprocessing as mp
 
 from paper_1803_11449_b200 import ConfigError
-from paper_1803_11449_b200.multi import byte_ranges, merge_allgather, merge_p2p, packet_slice
+from paper_1803_11449_b200.multi import (byte_ranges, merge_allgather, merge_p2p, merge_partitioned, packet_slice,
+                                         partition_ranges)
 
 from oracle import oracle as O
 
@@ -51,15 +52,23 @@ def test_packet_slices_partition_the_window():
 class HostOps:
     """Host stand-in for CudaMergeOps: same methods, numpy memory."""
 
+    COUNTERS = 256   # the device layout: [bits | window counters | zero counts] in one mapped allocation
+
     def __init__(self, sketch: O.OracleSketch, path: str):
         self.sketch, self.path = sketch, path
         n = sketch.bits.nbytes
         self.alloc_bytes = (n + 15) & ~15
-        self.mem = np.memmap(path, dtype=np.uint8, mode="w+", shape=(self.alloc_bytes,))
+        self.cell_bytes = sketch.bits.shape[2]
+        self.ncell = sketch.bits.shape[0] * sketch.bits.shape[1]
+        self.zc = np.full(self.ncell, -1, dtype=np.int32)      # -1: never counted nor gathered
+        self.mem_bytes = self.alloc_bytes + self.COUNTERS + 4 * self.ncell
+        self.mem = np.memmap(path, dtype=np.uint8, mode="w+", shape=(self.mem_bytes,))
         self.opened = []
+        self.owners = None
 
     def seal(self):
         self.mem[: self.sketch.bits.nbytes] = self.sketch.bits.reshape(-1)
+        self.mem[self.alloc_bytes + self.COUNTERS:] = self.zc.view(np.uint8)
         self.mem.flush()
 
     def _load(self):
@@ -69,7 +78,7 @@ class HostOps:
         return self.path.encode().ljust(64, b"\0")
 
     def open_handle(self, handle: bytes):
-        m = np.memmap(handle.rstrip(b"\0").decode(), dtype=np.uint8, mode="r", shape=(self.alloc_bytes,))
+        m = np.memmap(handle.rstrip(b"\0").decode(), dtype=np.uint8, mode="r", shape=(self.mem_bytes,))
         self.opened.append(m)
         return m
 
@@ -86,6 +95,33 @@ class HostOps:
         flat = self.sketch.bits.reshape(-1)
         hi = min(hi, flat.size)
         flat[lo:hi] = np.asarray(peer[lo:hi])
+
+    # partitioned read-out
+    def own_pointer(self):
+        return None   # "this rank's own bits"
+
+    def zero_counts_range(self, lo, hi):
+        hi = min(hi, self.sketch.bits.nbytes)
+        assert lo % self.cell_bytes == 0 and hi % self.cell_bytes == 0
+        cells = self.sketch.bits.reshape(self.ncell, self.cell_bytes)[lo // self.cell_bytes: hi // self.cell_bytes]
+        self.zc[lo // self.cell_bytes: hi // self.cell_bytes] = 8 * self.cell_bytes - np.unpackbits(cells, axis=1).sum(axis=1)
+
+    def gather_zero_counts(self, peer, lo, hi):
+        hi = min(hi, self.sketch.bits.nbytes)
+        theirs = np.asarray(peer[self.alloc_bytes + self.COUNTERS:]).view(np.int32)
+        self.zc[lo // self.cell_bytes: hi // self.cell_bytes] = theirs[lo // self.cell_bytes: hi // self.cell_bytes]
+
+    def set_cell_owners(self, bases, cuts):
+        self.owners = (list(bases), list(cuts))
+
+    def merged_view(self) -> O.OracleSketch:
+        """What a partitioned read-out sees: every cell from the rank that owns it."""
+        bases, cuts = self.owners
+        flat = np.empty(self.sketch.bits.nbytes, dtype=np.uint8)
+        for q, base in enumerate(bases):
+            lo, hi = cuts[q], min(cuts[q + 1], flat.size)
+            flat[lo:hi] = self.sketch.bits.reshape(-1)[lo:hi] if base is None else np.asarray(base[lo:hi])
+        return flat.reshape(self.sketch.bits.shape)
 
     def bits_tensor(self):
         return torch.from_numpy(self.sketch.bits.reshape(-1))
@@ -130,6 +166,19 @@ def _worker(rank, world, port, tmpdir, mode, kw, n_packets):
                 if kw.get("key_width", 32) < 32:
                     ec = ec & np.uint32((1 << kw["key_width"]) - 1)
                 cand, opp = np.concatenate([cand, ec]), np.concatenate([opp, eo])
+        elif mode == "partition":
+            merge_partitioned(ops, dist)
+            blo, bhi = partition_ranges(ops, world)[rank]
+            assert blo % ops.cell_bytes == 0 and (bhi % ops.cell_bytes == 0 or bhi == ops.alloc_bytes)
+            whole = O.OracleSketch(**kw)
+            whole.update_batch(cand, opp)
+            # own range merged, counts of every cell gathered, cells of every range reachable through its owner
+            mine = np.array_equal(sk.bits.reshape(-1)[blo:bhi], whole.bits.reshape(-1)[blo:bhi])
+            counts = np.array_equal(ops.zc.reshape(whole.zero_counts().shape), whole.zero_counts())
+            seen = np.array_equal(ops.merged_view(), whole.bits)
+            dist.barrier()        # (ShardedWindow.restore puts this barrier behind the read-out)
+            sk.bits[:] = ops.merged_view()
+            assert mine and counts and seen, f"rank {rank}: partitioned merge differs ({mine}, {counts}, {seen})"
         else:
             merge_allgather(ops, dist)
         whole = O.OracleSketch(**kw)
@@ -145,7 +194,7 @@ def _worker(rank, world, port, tmpdir, mode, kw, n_packets):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("mode", ["p2p", "allgather"])
+@pytest.mark.parametrize("mode", ["p2p", "allgather", "partition"])
 @pytest.mark.parametrize("world, kw", [(2, TOY), (3, TOY), (2, dict())])
 def test_sharded_scan_and_merge_equals_single_scan(mode, world, kw):
     port = 29500 + (os.getpid() + hash((mode, world, bool(kw)))) % 2000
