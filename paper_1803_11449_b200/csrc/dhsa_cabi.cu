@@ -120,6 +120,7 @@ struct dhsa_sketch {
                             // a peer that has the sketch mapped can read this rank's zero counts too
     bool zc_given;          // s->zc holds counts handed in by the caller for the next read-out call
     CellOwners owners;      // n > 0: partitioned read-out -- zero counts as gathered into s->zc, cells from their owners
+    uint64_t owners_seq;    // bumped whenever the owner table changes (it is baked into the read-out graph)
     uint32_t *lists;        // r * 2^k
     uint32_t *bitmaps;      // r * bitmap_words
     uint64_t bitmap_words;  // per array
@@ -142,6 +143,7 @@ struct dhsa_sketch {
     double graph_theta;
     uint64_t graph_max_candidates;
     uint64_t graph_cand_cap;
+    uint64_t graph_owners_seq;
     uint64_t graph_kernels;
     bool graph_disabled;
     ReportOut *reports_pinned;      // the first kPinnedReports rows land here with the control block
@@ -367,6 +369,7 @@ static int scrub_for_parking(dhsa_sketch *s)
     s->restore_pending = false;
     s->zc_given = false;
     s->owners.n = 0;
+    s->owners_seq++;
     CU(cudaMemsetAsync(s->bits, 0, s->alloc_bytes + kCounterBytes, s->stream));
     if (int rc = clear_flow_cache_locked(s, false)) return rc;
     CU(cudaStreamSynchronize(s->stream));
@@ -2131,8 +2134,8 @@ static int run_restore(dhsa_sketch *s, double theta, uint64_t max_candidates)
 {
     if (int rc = ensure_readout(s)) return rc;
     if (int rc = ensure_candidates_for(s, max_candidates)) return rc;
-    if (!s->graph_disabled && s->owners.n == 0) {  // (a partitioned read-out launches its kernels directly)
-        const bool fresh = s->restore_graph && s->graph_theta == theta &&
+    if (!s->graph_disabled) {
+        const bool fresh = s->restore_graph && s->graph_theta == theta && s->graph_owners_seq == s->owners_seq &&
                            s->graph_max_candidates == max_candidates && s->graph_cand_cap == s->cand_cap;
         if (!fresh) {
             if (s->restore_graph) {
@@ -2164,6 +2167,7 @@ static int run_restore(dhsa_sketch *s, double theta, uint64_t max_candidates)
                 s->graph_theta = theta;
                 s->graph_max_candidates = max_candidates;
                 s->graph_cand_cap = s->cand_cap;
+                s->graph_owners_seq = s->owners_seq;
             }
         }
         if (s->restore_graph) {
@@ -2578,6 +2582,7 @@ extern "C" int dhsa_set_cell_owners(dhsa_sketch_t *s, const void *const *bits_de
     std::lock_guard<std::mutex> lk(s->mu);
     if (int rc = refuse_if_restore_pending(s)) return rc;
     s->owners = own;
+    s->owners_seq++;
     return DHSA_OK;
 }
 
