@@ -111,6 +111,7 @@ struct dhsa_sketch {
     cudaEvent_t fc_stats_ev;
     bool fc_stats_pending;
     bool auto_fell_back;           // auto mode: this window's flows do not repeat, use the 5-access kernel
+    bool auto_cache_trusted;       // auto mode: the last counters seen (this window's or an earlier one's) showed repeats
 
     // read-out workspaces
     Readback *rb, *rb_host;  // control block + window counters + first report rows: device, and its pinned mirror
@@ -206,7 +207,8 @@ struct DeviceCache {
 static DeviceCache g_cache[64];
 static DeviceCache *cache_of(int device) { return device >= 0 && device < 64 ? &g_cache[device] : nullptr; }
 
-static const unsigned long long kPolicyMinSample = 1ull << 22;  // packets before the auto policy trusts a counter
+static const unsigned long long kPolicyMinSample = DHSA_POLICY_MIN_SAMPLE;  // packets before the auto policy trusts a counter
+static const uint64_t kGatedLaunchMin = 8 * DHSA_GATE_SAMPLE;  // one launch at least this long is sampled and gated on the device
 static void consume_policy_snapshots(dhsa_sketch *s, bool window_ends);
 static int flush_host_locked(dhsa_sketch *s);
 
@@ -554,7 +556,7 @@ static int clear_flow_cache_locked(dhsa_sketch *s, bool clear_stats)
     } else {
         s->dp.fc_epoch++;
     }
-    if (clear_stats) CU(cudaMemsetAsync(s->fc_stats, 0, 2 * sizeof(unsigned long long), s->stream));
+    if (clear_stats) CU(cudaMemsetAsync(s->fc_stats, 0, 3 * sizeof(unsigned long long), s->stream));
     s->fc_dirty = false;
     return DHSA_OK;
 }
@@ -793,9 +795,16 @@ static void consume_policy_snapshots(dhsa_sketch *s, bool window_ends)
 {
     if (s->fc_stats_pending && cudaEventQuery(s->fc_stats_ev) == cudaSuccess) {
         s->fc_stats_pending = false;
-        const unsigned long long lookups = s->fc_stats_host[0], hits = s->fc_stats_host[1];
-        // a snapshot that arrives when its window is over says nothing about the next one
-        if (lookups >= kPolicyMinSample && !window_ends && hits * 10 < lookups * 3) s->auto_fell_back = true;
+        const unsigned long long lookups = s->fc_stats_host[0], hits = s->fc_stats_host[1], verdict = s->fc_stats_host[2];
+        // what the counters say: flows do not repeat (hit rate under 0.3 after enough lookups, or the device's own
+        // projection from a gated launch's sample), they do, or nothing yet
+        const bool no_repeats = verdict == 2 || (verdict == 0 && lookups >= kPolicyMinSample && hits * 10 < lookups * 3);
+        const bool repeats = verdict == 1 || (lookups >= kPolicyMinSample && hits * 10 >= lookups * 3);
+        // a snapshot that arrives when its window is over cannot switch the next window's kernel, but it is the prior
+        // that decides whether the next long launch is worth gating on the device
+        if (no_repeats) s->auto_cache_trusted = false;
+        else if (repeats) s->auto_cache_trusted = true;
+        if (no_repeats && !window_ends) s->auto_fell_back = true;
     }
     (void)cudaGetLastError();
 }
@@ -828,11 +837,11 @@ static int after_fast_scan_locked(dhsa_sketch *s, int mode)
 {
     if (s->scan_mode == DHSA_SCAN_AUTO && mode == DHSA_SCAN_FLOW_CACHE && !s->fc_stats_pending) {
         if (!s->fc_stats_host) {
-            CU(cudaMallocHost(&s->fc_stats_host, 2 * sizeof(unsigned long long)));
+            CU(cudaMallocHost(&s->fc_stats_host, 3 * sizeof(unsigned long long)));
             CU(cudaEventCreateWithFlags(&s->fc_stats_ev, cudaEventDisableTiming));
-            memset(s->fc_stats_host, 0, 2 * sizeof(unsigned long long));
+            memset(s->fc_stats_host, 0, 3 * sizeof(unsigned long long));
         }
-        CU(cudaMemcpyAsync(s->fc_stats_host, s->fc_stats, 2 * sizeof(unsigned long long), cudaMemcpyDeviceToHost,
+        CU(cudaMemcpyAsync(s->fc_stats_host, s->fc_stats, 3 * sizeof(unsigned long long), cudaMemcpyDeviceToHost,
                            s->stream));
         CU(cudaEventRecord(s->fc_stats_ev, s->stream));
         s->fc_stats_pending = true;
@@ -861,7 +870,27 @@ static int scan_locked(dhsa_sketch *s, const uint32_t *cand, const uint32_t *opp
         src.cand4 = reinterpret_cast<const uint4 *>(cand);
         src.opp4 = reinterpret_cast<const uint4 *>(opp);
         src.nvec = n / 4;
-        launch_scan_any_r(s, mode, src);
+        if (s->scan_mode == DHSA_SCAN_AUTO && mode == DHSA_SCAN_FLOW_CACHE && !s->auto_cache_trusted && n >= kGatedLaunchMin) {
+            // one long launch and no evidence yet that flows repeat: the host cannot look at the counters in the
+            // middle of it, so the device decides (k_auto_decide): a sample through the cache, then the rest through
+            // whichever kernel the sample's projected hit rate calls for.  32 instead of 15 Gpps on an all-distinct
+            // window; three short extra launches on one that repeats, and only until a window has shown repeats.
+            const uint64_t head = DHSA_GATE_SAMPLE / 4;
+            SoaSource rest = src;
+            rest.cand4 += head, rest.opp4 += head, rest.nvec -= head;
+            src.nvec = head;
+            launch_scan_any_r(s, DHSA_SCAN_FLOW_CACHE, src);
+            k_auto_decide<<<1, 1, 0, s->stream>>>(s->fc_stats, 4 * rest.nvec);
+            s->launches++;
+            s->dp.gate = 2;
+            launch_scan_any_r(s, DHSA_SCAN_TEST_RED, rest);
+            s->dp.gate = 1;
+            launch_scan_any_r(s, DHSA_SCAN_FLOW_CACHE, rest);
+            s->dp.gate = 0;
+            src.nvec += rest.nvec;
+        } else {
+            launch_scan_any_r(s, mode, src);
+        }
         if (int rc = after_fast_scan_locked(s, mode)) return rc;
         done = src.nvec * 4;
     }

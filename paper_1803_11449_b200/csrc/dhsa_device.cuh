@@ -31,7 +31,9 @@ struct DevParams {
     int fc_shift;                  // 32 - log2(fc_sets): set = a >> fc_shift
     int fc_tag_bits;               // fc_shift + log2(g): key bits an entry stores
     uint32_t fc_epoch;             // entries of other epochs count as empty: a window reset is epoch + 1
-    unsigned long long *fc_stats;  // [0] lookups, [1] hits
+    unsigned long long *fc_stats;  // [0] lookups, [1] hits, [2] k_auto_decide's verdict (0 none, 1 cache pays, 2 it does not)
+    int gate;                      // scan kernels of a device-gated auto launch: 0 run; 1 run iff k_auto_decide found that
+                                   // the flow cache pays in this window; 2 run iff it does not (fc_stats[2], scan_gated_out)
 };
 
 // Device-resident control block of one read-out: every stage kernel reads its
@@ -463,9 +465,48 @@ __device__ __forceinline__ void flush_tally(const SRC &src, uint32_t on_time, ui
     }
 }
 
+// Scan mode `auto`, decided on the device.  A window starts behind the flow cache; whether the cache pays (flows repeat)
+// is known only from its own counters.  Between launches the host reads them (dhsa_cabi.cu: the auto policy); for ONE long
+// launch it queues four kernels: the first DHSA_GATE_SAMPLE packets through the cache, k_auto_decide, then the rest
+// through the test-first kernel with gate = 2 and through the cache kernel with gate = 1.  Exactly one of the two does
+// the work; the other returns at once (scan_gated_out).
+//
+// The verdict must not be fooled by a cold table: the first m packets of a window over F equally likely flows find only
+// ~m/2F of their keys, however often the flows will repeat later (config 2: 13% hits in the first million packets, 96%
+// over the window).  So the sample's counts are projected: with D = m - hits distinct keys among m lookups,
+// x = m / F solves (1 - e^-x) / x = D / m, and over the N = m + rest packets of this launch the same population would
+// miss (1 - e^-y) / y of its lookups, y = x N / m.  The cache pays when that projected miss rate is at most 0.7 --
+// the host policy's break-even (1 + 11 (1 - h) requests per packet with the cache, 5 + 5 (1 - h) without).
+#define DHSA_POLICY_MIN_SAMPLE (1ull << 22)
+#define DHSA_GATE_SAMPLE (1ull << 20)
+__global__ void k_auto_decide(unsigned long long *fc_stats, unsigned long long rest_packets)
+{
+    const unsigned long long m = fc_stats[0], h = fc_stats[1];
+    bool pays = true;
+    if (m > 0) {
+        const float rho = (float)(m - h) / (float)m;
+        float lo = 1e-7f, hi = 64.0f;  // (1 - e^-x) / x falls from 1 to 0
+        for (int it = 0; it < 48; it++) {
+            const float x = 0.5f * (lo + hi);
+            if (-expm1f(-x) / x > rho) lo = x; else hi = x;
+        }
+        const float y = 0.5f * (lo + hi) * ((float)m + (float)rest_packets) / (float)m;
+        pays = -expm1f(-y) / y <= 0.7f;
+    }
+    fc_stats[2] = pays ? 1ull : 2ull;
+}
+
+__device__ __forceinline__ bool scan_gated_out(const DevParams &p)
+{
+    if (p.gate == 0) return false;
+    const bool no_repeats = p.fc_stats[2] == 2ull;
+    return (p.gate == 1) == no_repeats;
+}
+
 template <int R, int MODE, typename SRC>
 __global__ void __launch_bounds__(256) k_scan_vec4(SRC src, uint32_t *__restrict__ words, DevParams p)
 {
+    if (scan_gated_out(p)) return;
     const uint32_t lane = threadIdx.x & 31u;
     const uint64_t nvec = src.vectors();
     const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
@@ -649,6 +690,7 @@ struct FcSmem {
 template <int R, typename SRC>
 __global__ void __launch_bounds__(256, DHSA_FC_CTAS_PER_SM) k_scan_flowcache(SRC src, uint32_t *__restrict__ words, DevParams p)
 {
+    if (scan_gated_out(p)) return;
     // dynamic shared memory (FcSmem<SRC>::kBytes): per-warp stage rings, mbarriers, miss queues
     extern __shared__ __align__(128) uint8_t fc_smem[];
     typedef uint8_t StageRing[SRC::kStages][SRC::kStageBytes];

@@ -4,8 +4,9 @@
     (direction "dst": every packet lands in the same 5 x 4 cells) and as opposites ("src": no
     contention), per scan mode; bits are compared with the oracle in every run.
 (2) `auto` must never lose to a fixed mode by more than 5%: on both directions of (1), on a
-    config-2 window (flows repeat ~26 times) and on an all-distinct window (no flow repeats; fed in
-    16 batches, as an engine feeds chunks, so the policy can react inside the window).  Every mode
+    config-2 window (flows repeat ~26 times) and on an all-distinct window (no flow repeats), fed in
+    16 batches, as an engine feeds chunks, so the host policy can react inside the window, and in one
+    launch, where the device decides (k_auto_decide).  Every mode
     gets one untimed window first, then three timed windows (best of three).
 Prints one JSON document; exits non-zero if a bit array differs or auto loses.
 """
@@ -106,6 +107,8 @@ def main():
     ora = O.OracleSketch()
     ora.update_batch(c_np, o_np, threads=8)
     out += run("all_distinct_16_batches", cand, opp, ora.bits, N, batches=16, modes=("test", "test_agg", "flow_cache", "auto"))
+    # the same window handed over in ONE launch: the host cannot react inside it, the launch is sampled and gated on the device
+    out += run("all_distinct_one_launch", cand, opp, ora.bits, N, batches=1, modes=("test", "flow_cache", "auto"))
     verdict = {}
     for trace in dict.fromkeys(r["trace"] for r in out):
         rows = [r for r in out if r["trace"] == trace]

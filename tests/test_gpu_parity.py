@@ -271,6 +271,44 @@ def test_auto_mode_falls_back_when_flows_do_not_repeat():
     assert sk.flow_cache_stats()[0] == 1_000_000 and sk.scan_mode_used == "flow_cache"
 
 
+def test_auto_mode_decides_on_the_device_inside_one_long_launch():
+    """One 24M-packet launch of all-distinct pairs: the host cannot read the counters mid-launch, so the
+    launch is sampled and gated on the device -- the first 2^20 packets go through the flow cache, the hit
+    rate projected from them (~0) sends the rest to the test-first kernel.  Then a window whose flows
+    repeat (a cold table: few hits in the sample, many projected): the cache kernel takes the rest, and
+    from the next window on the launch is not split at all.  Bits exact throughout."""
+    import torch
+
+    n = 24_000_000
+    cand, opp = O.distinct_pairs(n, 91)
+    ora = O.OracleSketch()
+    ora.update_batch(cand, opp, threads=8)
+    cd, od = torch.from_numpy(cand.view(np.int32)).cuda(), torch.from_numpy(opp.view(np.int32)).cuda()
+    sk = P.Dhla(P.DhgParams())
+    before = sk.launch_count
+    sk.update_batch(cd, od)
+    assert sk.launch_count - before == 4                      # sample, verdict, gated test-first, gated cache
+    assert sha(sk.bits) == sha(ora.bits)
+    lookups, hits = sk.flow_cache_stats()
+    assert lookups == 1 << 20 and hits * 10 < lookups         # only the sample consulted the cache
+    # a window that repeats, slowly: 24M packets over 6M flows (4 packets per flow; 8% hits within the sample)
+    rng = np.random.default_rng(5)
+    pick = rng.integers(0, 6_000_000, size=n)
+    rc, ro = cand[:6_000_000][pick], opp[:6_000_000][pick]
+    ora2 = O.OracleSketch()
+    ora2.update_batch(rc, ro, threads=8)
+    cd, od = torch.from_numpy(rc.view(np.int32)).cuda(), torch.from_numpy(ro.view(np.int32)).cuda()
+    for window, want_launches in ((0, 4), (1, 1), (2, 1)):   # gated once more, then the counters have shown repeats
+        sk.reset()
+        before = sk.launch_count
+        sk.update_batch(cd, od)
+        sk.seal()
+        assert sk.launch_count - before == want_launches, window
+        assert sha(sk.bits) == sha(ora2.bits)
+        lookups, hits = sk.flow_cache_stats()
+        assert lookups == n and hits > 0.65 * n
+
+
 def test_estimator_returns_one_cell():
     # pkg/src/dhsa/dhla.py:107-109
     sk = P.Dhla(P.DhgParams(**PARAM_SETS["small"]))
