@@ -57,6 +57,9 @@ static int cuda_fail(cudaError_t e, const char *what)
 
 // ------------------------------------------------------------------ handle --
 
+#ifndef DHSA_COPY_NT_DEFAULT
+#define DHSA_COPY_NT_DEFAULT true
+#endif
 #ifndef DHSA_READOUT_CTAS_PER_SM
 #define DHSA_READOUT_CTAS_PER_SM 4   // grid of the stage / verify / re-estimate kernels (grid-stride loops)
 #endif
@@ -1010,6 +1013,48 @@ extern "C" int dhsa_record_tally_at_restore(dhsa_sketch_t *s, uint64_t *records_
 // there.  The reference engine hands over 65,536-pair batches (512 KB), so a job lasts tens of
 // microseconds: helpers poll for about 100 us after their last job before they go to sleep, and
 // a caller that finds the pool busy with another caller's job simply copies alone.
+// Copy into a pinned slot.  The destination is read next by the DMA engine, never by this CPU, so on x86-64 the
+// stores can bypass the cache (no read-for-ownership of the destination lines, no eviction of the caller's data):
+// 16-byte streaming stores once the destination is aligned.  DHSA_COPY_NT=0 selects plain memcpy.
+#if defined(__x86_64__)
+#include <emmintrin.h>
+static bool copy_nt_enabled()
+{
+    static const bool on = [] {
+        const char *env = getenv("DHSA_COPY_NT");
+        return env ? env[0] != '0' : DHSA_COPY_NT_DEFAULT;
+    }();
+    return on;
+}
+static void copy_to_pinned(void *dst, const void *src, size_t n)
+{
+    if (!copy_nt_enabled() || n < 4096) {
+        memcpy(dst, src, n);
+        return;
+    }
+    char *d = (char *)dst;
+    const char *s = (const char *)src;
+    const size_t lead = (16 - ((uintptr_t)d & 15)) & 15;
+    if (lead) {
+        memcpy(d, s, lead);
+        d += lead, s += lead, n -= lead;
+    }
+    size_t blocks = n / 64;
+    for (; blocks; blocks--, d += 64, s += 64) {
+        const __m128i a = _mm_loadu_si128((const __m128i *)(s + 0)), b = _mm_loadu_si128((const __m128i *)(s + 16));
+        const __m128i c = _mm_loadu_si128((const __m128i *)(s + 32)), e = _mm_loadu_si128((const __m128i *)(s + 48));
+        _mm_stream_si128((__m128i *)(d + 0), a);
+        _mm_stream_si128((__m128i *)(d + 16), b);
+        _mm_stream_si128((__m128i *)(d + 32), c);
+        _mm_stream_si128((__m128i *)(d + 48), e);
+    }
+    _mm_sfence();
+    if (n & 63) memcpy(d, s, n & 63);
+}
+#else
+static void copy_to_pinned(void *dst, const void *src, size_t n) { memcpy(dst, src, n); }
+#endif
+
 class CopyPool {
 public:
     static CopyPool &get()
@@ -1023,8 +1068,8 @@ public:
     {
         const size_t total = 2 * bytes_each;
         if (n_helpers_ == 0 || total < (128u << 10) || !job_mu_.try_lock()) {
-            memcpy(d0, s0, bytes_each);
-            memcpy(d1, s1, bytes_each);
+            copy_to_pinned(d0, s0, bytes_each);
+            copy_to_pinned(d1, s1, bytes_each);
             return;
         }
         uint32_t shares = n_helpers_ + 1;
@@ -1092,10 +1137,10 @@ private:
             size_t lo = (size_t)i * j.per, hi = lo + j.per < 2 * j.bytes_each ? lo + j.per : 2 * j.bytes_each;
             if (lo < j.bytes_each) {
                 const size_t end = hi < j.bytes_each ? hi : j.bytes_each;
-                memcpy(j.d0 + lo, j.s0 + lo, end - lo);
+                copy_to_pinned(j.d0 + lo, j.s0 + lo, end - lo);
                 lo = end;
             }
-            if (hi > lo) memcpy(j.d1 + (lo - j.bytes_each), j.s1 + (lo - j.bytes_each), hi - lo);
+            if (hi > lo) copy_to_pinned(j.d1 + (lo - j.bytes_each), j.s1 + (lo - j.bytes_each), hi - lo);
             done_.fetch_add(1, std::memory_order_acq_rel);
         }
     }
