@@ -786,13 +786,31 @@ static void launch_scan_any_r(dhsa_sketch *s, int mode, const SRC &src)
 // ---- the auto policy ------------------------------------------------------------------------
 // Decided per launch from counters the scan kernels leave behind the bit array, read through
 // asynchronous pinned snapshots (never a synchronisation):
-//   * flows that do not repeat (cache hit rate under 0.3 after >= 4M lookups): the rest of the
-//     WINDOW goes to the 5-access test-first kernel.  Break-even is a hit rate of about 1/3: 1 + 11 (1 - h)
-//     requests per packet with the cache against 5 + 5 (1 - h) without.
+//   * flows that do not repeat (after >= 4M lookups, the hit rate PROJECTED for the next stretch of the window is
+//     under 0.3, projected_no_repeats): the rest of the WINDOW goes to the 5-access test-first kernel.  Break-even is
+//     a hit rate of about 1/3: 1 + 11 (1 - h) requests per packet with the cache against 5 + 5 (1 - h) without.
 // (A second rule of an earlier round -- the plain test-first kernel for windows whose candidates are a
 // handful of hosts, BASELINE config 4 with the victims as candidates -- was measured again after the
 // lookup loop lost its per-slot miss handling: the cache path now scans that window at 205 Gpps
 // against 183 for the test-first kernel, so the rule is gone; profiles/r02_config4_ddos_contention.json.)
+
+// Would the flow cache pay over the NEXT stretch of the window, judged from the m lookups and h hits so far?  A cold
+// table hides repeats: the first m packets over F equally likely flows find only ~m/2F of their keys.  So the counts
+// are projected the way k_auto_decide does it: x = m / F solves (1 - e^-x) / x = (m - h) / m, and the next m packets of
+// the same population miss (e^-x - e^-2x) / x of their lookups.  "No repeats" = that projected miss rate above 0.7
+// (the break-even of 1 + 11 (1 - hit) requests per packet against 5 + 5 (1 - hit)).
+static bool projected_no_repeats(unsigned long long m, unsigned long long h)
+{
+    if (m == 0) return false;
+    const double rho = (double)(m - h) / (double)m;
+    double lo = 1e-9, hi = 64.0;
+    for (int it = 0; it < 60; it++) {
+        const double x = 0.5 * (lo + hi);
+        if (-expm1(-x) / x > rho) lo = x; else hi = x;
+    }
+    const double x = 0.5 * (lo + hi);
+    return (exp(-x) - exp(-2.0 * x)) / x > 0.7;
+}
 
 static void consume_policy_snapshots(dhsa_sketch *s, bool window_ends)
 {
@@ -801,8 +819,9 @@ static void consume_policy_snapshots(dhsa_sketch *s, bool window_ends)
         const unsigned long long lookups = s->fc_stats_host[0], hits = s->fc_stats_host[1], verdict = s->fc_stats_host[2];
         // what the counters say: flows do not repeat (hit rate under 0.3 after enough lookups, or the device's own
         // projection from a gated launch's sample), they do, or nothing yet
-        const bool no_repeats = verdict == 2 || (verdict == 0 && lookups >= kPolicyMinSample && hits * 10 < lookups * 3);
-        const bool repeats = verdict == 1 || (lookups >= kPolicyMinSample && hits * 10 >= lookups * 3);
+        const bool enough = lookups >= kPolicyMinSample;
+        const bool no_repeats = verdict == 2 || (verdict == 0 && enough && projected_no_repeats(lookups, hits));
+        const bool repeats = verdict == 1 || (enough && !projected_no_repeats(lookups, hits));
         // a snapshot that arrives when its window is over cannot switch the next window's kernel, but it is the prior
         // that decides whether the next long launch is worth gating on the device
         if (no_repeats) s->auto_cache_trusted = false;

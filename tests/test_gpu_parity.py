@@ -309,6 +309,26 @@ def test_auto_mode_decides_on_the_device_inside_one_long_launch():
         assert lookups == n and hits > 0.65 * n
 
 
+def test_auto_mode_is_not_fooled_by_a_cold_table():
+    """6M flows, 4 packets each, fed in six 4M-packet batches: after the first batch only a quarter of the
+    lookups hit (the table was empty), though three quarters will over the window.  The policy projects the
+    counts (projected_no_repeats) and stays behind the cache; on all-distinct pairs it still leaves it."""
+    n = 24_000_000
+    cand, opp = O.distinct_pairs(6_000_000, 92)
+    pick = np.random.default_rng(6).integers(0, 6_000_000, size=n)
+    rc, ro = cand[pick], opp[pick]
+    ora = O.OracleSketch()
+    ora.update_batch(rc, ro, threads=8)
+    sk = P.Dhla(P.DhgParams())
+    for lo in range(0, n, 4_000_000):
+        sk.update_batch(rc[lo:lo + 4_000_000], ro[lo:lo + 4_000_000])
+        lookups, hits = sk.flow_cache_stats()                # an engine's per-chunk bookkeeping: the snapshot lands
+        if lo == 0:
+            assert hits * 10 < lookups * 3                   # what the plain hit-rate rule would have fallen for
+    assert sk.scan_mode_used == "flow_cache" and lookups == n and hits > 0.65 * n
+    assert sha(sk.bits) == sha(ora.bits)
+
+
 def test_estimator_returns_one_cell():
     # pkg/src/dhsa/dhla.py:107-109
     sk = P.Dhla(P.DhgParams(**PARAM_SETS["small"]))
