@@ -103,6 +103,7 @@ struct dhsa_sketch {
     cudaEvent_t bridge_ev;  // orders a foreign producer stream with the launch stream (dhsa_update_device_from)
     int occ[5][2];          // resident CTAs per SM of the scan kernel of [mode][packet source] (0 = not asked yet)
     bool fc_opted_in[2];    // the flow-cache kernel's >48 KB dynamic shared memory was granted on this device
+    bool fc_gated_opted_in; // ... and its gated instantiation's (device-gated auto launches)
     uint64_t mutation_seq;  // bumped by every call that can change the bits
 
     // flow cache of scan mode 3
@@ -747,6 +748,27 @@ static void launch_scan_src(dhsa_sketch *s, int mode, const SRC &src)
         const int occ = resident_ctas(s, mode, kind, KERNEL, 0, FALLBACK_OCC);                             \
         KERNEL<<<grid_for(s, nvec, 256, occ), 256, 0, s->stream>>>(src, w, s->dp);                         \
     } while (0)
+    if (s->dp.gate != 0) {
+        // the two kernels behind k_auto_decide in a device-gated auto launch (pair form only): instantiations that
+        // first read the verdict, same grids as their plain twins
+        if constexpr (SrcKind<SRC>::value == 0) {
+            if (mode == DHSA_SCAN_TEST_RED) {
+                const int occ = resident_ctas(s, mode, kind, k_scan_vec4<R, 1, SRC>, 0, 3);
+                k_scan_vec4<R, 1, SRC, true><<<grid_for(s, nvec, 256, occ), 256, 0, s->stream>>>(src, w, s->dp);
+            } else {
+                auto kernel = k_scan_flowcache<R, SRC, true>;
+                const int smem = FcSmem<SRC>::kBytes;
+                if (!s->fc_gated_opted_in) {
+                    cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+                    s->fc_gated_opted_in = true;
+                }
+                const int occ = resident_ctas(s, DHSA_SCAN_FLOW_CACHE, kind, k_scan_flowcache<R, SRC>, smem, 3);
+                kernel<<<grid_for(s, nvec, 256, occ), 256, smem, s->stream>>>(src, w, s->dp);
+            }
+        }
+        s->launches++;
+        return;
+    }
     switch (mode) {
     case DHSA_SCAN_RED_ONLY: LAUNCH((k_scan_vec4<R, 0, SRC>), 8); break;
     case DHSA_SCAN_TEST_RED: LAUNCH((k_scan_vec4<R, 1, SRC>), 3); break;

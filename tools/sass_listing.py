@@ -8,7 +8,7 @@ import sys
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 LIB = os.path.join(ROOT, "paper_1803_11449_b200", "libdhsa_b200.so")
-FUN = "_ZN4dhsa16k_scan_flowcacheILi5ENS_9SoaSourceEEEvT0_PjNS_9DevParamsE"
+FUN = "_ZN4dhsa16k_scan_flowcacheILi5ENS_9SoaSourceELb0EEEvT0_PjNS_9DevParamsE"
 NOTABLE = [("UBLKCP", "cp.async.bulk global->shared: the packet stream is staged by the TMA engine"),
            ("SYNCS", "mbarrier arrive/expect_tx and try_wait: completion of the bulk copies"),
            (".256", "256-bit global load: one flow-cache set (8 ways x 4 B = one 32-byte sector) per lane"),
