@@ -57,6 +57,25 @@ assert np.array_equal(P.read_snapshot(buf).bits, ora.bits)
 del sk
 sk = P.Dhla(P.DhgParams())          # the parked one
 assert not sk.bits.any()
+# round 2, later: one long launch in auto mode is sampled and gated on the device (k_auto_decide + the gated instantiations
+# of the test-first and the cache kernel), once with flows that repeat and once with all-distinct pairs; the counter
+# snapshot travels on its side stream and the reset waits for it
+import torch
+big = np.random.default_rng(1).integers(0, len(cand), size=8_600_000)
+bc, bo = torch.from_numpy(cand[big].view(np.int32)).cuda(), torch.from_numpy(opp[big].view(np.int32)).cuda()
+sk = P.Dhla(P.DhgParams())
+n0 = sk.launch_count
+sk.update_batch(bc, bo)
+assert sk.launch_count - n0 == 4 and np.array_equal(sk.bits, ora.bits)
+sk.reset()                                      # waits (stream-ordered) for the snapshot on the side stream
+sk.update_batch(bc, bo)                         # the counters have shown repeats: one plain launch now
+assert sk.launch_count - n0 == 5 and np.array_equal(sk.bits, ora.bits)
+sk = P.Dhla(P.DhgParams(k=15, alpha=6))         # a sketch without that prior
+dc, do = O.distinct_pairs(8_600_000, 77)
+ora2 = O.OracleSketch(k=15, alpha=6)
+ora2.update_batch(dc, do, threads=8)
+sk.update_batch(torch.from_numpy(dc.view(np.int32)).cuda(), torch.from_numpy(do.view(np.int32)).cuda())
+assert np.array_equal(sk.bits, ora2.bits) and sk.flow_cache_stats()[0] == 1 << 20
 print("sanitizer run ok:", [len(r.reports) for r in res], n_pairs, n_hosts)
 PY
 for tool in memcheck racecheck synccheck; do
