@@ -49,7 +49,9 @@ extern "C" {
 #define DHSA_SCAN_TEST_AGG_RED 2  /* as 1, and lanes of a warp hitting one word merge first    */
 #define DHSA_SCAN_FLOW_CACHE 3    /* as 2 behind an exact L2-resident cache of scanned pairs   */
 #define DHSA_SCAN_AUTO 4          /* default: 3, falling back to 1 for the rest of a window whose
-                                     flows do not repeat (cache hit rate below ~1/3)            */
+                                     flows do not repeat (hit rate projected from the cache's own
+                                     counters below ~1/3): decided by the host between launches and
+                                     on the device inside one launch of >= 8M packets             */
 
 typedef struct dhsa_sketch dhsa_sketch_t; /* opaque; replaces dhsa.dhla.Dhla, pkg/src/dhsa/dhla.py:57-68 */
 
