@@ -947,7 +947,7 @@ static int scan_locked(dhsa_sketch *s, const uint32_t *cand, const uint32_t *opp
         if (s->scan_mode == DHSA_SCAN_AUTO && mode == DHSA_SCAN_FLOW_CACHE && !s->auto_cache_trusted && n >= kGatedLaunchMin) {
             // one long launch and no evidence yet that flows repeat: the host cannot look at the counters in the
             // middle of it, so the device decides (k_auto_decide): a sample through the cache, then the rest through
-            // whichever kernel the sample's projected hit rate calls for.  32 instead of 15 Gpps on an all-distinct
+            // whichever kernel the sample's projected hit rate calls for.  38 instead of 15 Gpps on an all-distinct
             // window; three short extra launches on one that repeats, and only until a window has shown repeats.
             const uint64_t head = DHSA_GATE_SAMPLE / 4;
             SoaSource rest = src;
