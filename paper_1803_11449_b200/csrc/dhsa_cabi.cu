@@ -2373,6 +2373,10 @@ static int restore_end_locked(dhsa_sketch *s, dhsa_report_t *reports_host, uint6
 {
     if (!s->restore_pending) return fail(DHSA_ECONFIG, "dhsa_restore_end without dhsa_restore_begin");
     CU(cudaEventSynchronize(s->restore_ev));
+    // the window's flow-cache counters came back with the control block: the auto policy's prior for the next long
+    // launch (a pipelined caller resets before the side-stream snapshot has landed, and reset drops it)
+    if (s->scan_mode == DHSA_SCAN_AUTO && s->ctl_host->counters[2] >= kPolicyMinSample)
+        s->auto_cache_trusted = !projected_no_repeats(s->ctl_host->counters[2], s->ctl_host->counters[3]);
     const uint64_t max_candidates = s->restore_max_candidates;
     const double theta = s->restore_theta;
     // a stage needed more room than the workspaces had (and max_candidates allows it): grow, run again

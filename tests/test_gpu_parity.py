@@ -309,6 +309,34 @@ def test_auto_mode_decides_on_the_device_inside_one_long_launch():
         assert lookups == n and hits > 0.65 * n
 
 
+def test_auto_mode_learns_from_the_read_out_when_windows_are_pipelined():
+    """reset() right behind restore_begin(): the host is a window ahead of the device, the side-stream snapshot of
+    window k has not landed when window k + 1 is reset -- the prior comes from the counters in the read-out instead,
+    so only the first two windows are sampled and gated."""
+    import torch
+
+    n = 16_000_000
+    cand, opp = O.distinct_pairs(500_000, 93)
+    pick = np.random.default_rng(7).integers(0, 500_000, size=n)
+    cd = torch.from_numpy(cand[pick].view(np.int32)).cuda()
+    od = torch.from_numpy(opp[pick].view(np.int32)).cuda()
+    ora = O.OracleSketch()
+    ora.update_batch(cand, opp)
+    sk = P.Dhla(P.DhgParams())
+    launches = []
+    for w in range(5):
+        sk.reset()
+        before = sk.launch_count
+        sk.update_batch(cd, od)
+        launches.append(sk.launch_count - before)
+        if w:
+            sk.restore_superpoints_end()                 # window w - 1
+        sk.restore_superpoints_begin(1024)
+    sk.restore_superpoints_end()
+    assert launches[0] == 4 and launches[-1] == 1 and launches[-2] == 1, launches
+    assert sha(sk.bits) == sha(ora.bits)
+
+
 def test_auto_mode_is_not_fooled_by_a_cold_table():
     """6M flows, 4 packets each, fed in six 4M-packet batches: after the first batch only a quarter of the
     lookups hit (the table was empty), though three quarters will over the window.  The policy projects the
