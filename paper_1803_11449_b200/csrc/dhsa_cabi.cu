@@ -103,7 +103,7 @@ struct dhsa_sketch {
     cudaEvent_t bridge_ev;  // orders a foreign producer stream with the launch stream (dhsa_update_device_from)
     int occ[5][2];          // resident CTAs per SM of the scan kernel of [mode][packet source] (0 = not asked yet)
     bool fc_opted_in[2];    // the flow-cache kernel's >48 KB dynamic shared memory was granted on this device
-    bool fc_gated_opted_in; // ... and its gated instantiation's (device-gated auto launches)
+    bool fc_gated_opted_in[2];  // ... and its gated instantiation's (device-gated auto launches)
     uint64_t mutation_seq;  // bumped by every call that can change the bits
 
     // flow cache of scan mode 3
@@ -770,22 +770,20 @@ static void launch_scan_src(dhsa_sketch *s, int mode, const SRC &src)
         KERNEL<<<grid_for(s, nvec, 256, occ), 256, 0, s->stream>>>(src, w, s->dp);                         \
     } while (0)
     if (s->dp.gate != 0) {
-        // the two kernels behind k_auto_decide in a device-gated auto launch (pair form only): instantiations that
-        // first read the verdict, same grids as their plain twins
-        if constexpr (SrcKind<SRC>::value == 0) {
-            if (mode == DHSA_SCAN_TEST_RED) {
-                const int occ = resident_ctas(s, mode, kind, k_scan_vec4<R, 1, SRC>, 0, 3);
-                k_scan_vec4<R, 1, SRC, true><<<grid_for(s, nvec, 256, occ), 256, 0, s->stream>>>(src, w, s->dp);
-            } else {
-                auto kernel = k_scan_flowcache<R, SRC, true>;
-                const int smem = FcSmem<SRC>::kBytes;
-                if (!s->fc_gated_opted_in) {
-                    cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-                    s->fc_gated_opted_in = true;
-                }
-                const int occ = resident_ctas(s, DHSA_SCAN_FLOW_CACHE, kind, k_scan_flowcache<R, SRC>, smem, 3);
-                kernel<<<grid_for(s, nvec, 256, occ), 256, smem, s->stream>>>(src, w, s->dp);
+        // the two kernels behind k_auto_decide in a device-gated auto launch: instantiations that first read the
+        // verdict, same grids as their plain twins
+        if (mode == DHSA_SCAN_TEST_RED) {
+            const int occ = resident_ctas(s, mode, kind, k_scan_vec4<R, 1, SRC>, 0, 3);
+            k_scan_vec4<R, 1, SRC, true><<<grid_for(s, nvec, 256, occ), 256, 0, s->stream>>>(src, w, s->dp);
+        } else {
+            auto kernel = k_scan_flowcache<R, SRC, true>;
+            const int smem = FcSmem<SRC>::kBytes;
+            if (!s->fc_gated_opted_in[kind]) {
+                cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+                s->fc_gated_opted_in[kind] = true;
             }
+            const int occ = resident_ctas(s, DHSA_SCAN_FLOW_CACHE, kind, k_scan_flowcache<R, SRC>, smem, 3);
+            kernel<<<grid_for(s, nvec, 256, occ), 256, smem, s->stream>>>(src, w, s->dp);
         }
         s->launches++;
         return;
@@ -930,6 +928,29 @@ static bool fast_params(const dhsa_sketch *s)
     return p.r >= 3 && p.r <= 6 && s->dp.log2g >= 5 && s->dp.nwords <= 0xFFFFFFFFull;
 }
 
+// One long launch in auto mode with no evidence yet that flows repeat: the host cannot look at the counters in the
+// middle of it, so the device decides (k_auto_decide) -- a sample of DHSA_GATE_SAMPLE packets through the cache, then
+// the rest through whichever kernel the sample's projected hit rate calls for.  38 instead of 15 Gpps on an all-distinct
+// window; three short extra launches on one that repeats, and only until a window has shown repeats.
+static bool wants_gated_launch(const dhsa_sketch *s, int mode, uint64_t packets)
+{
+    return s->scan_mode == DHSA_SCAN_AUTO && mode == DHSA_SCAN_FLOW_CACHE && !s->auto_cache_trusted &&
+           packets >= kGatedLaunchMin;
+}
+
+template <typename SRC>
+static void launch_scan_gated(dhsa_sketch *s, const SRC &head, const SRC &rest)
+{
+    launch_scan_any_r(s, DHSA_SCAN_FLOW_CACHE, head);
+    k_auto_decide<<<1, 1, 0, s->stream>>>(s->fc_stats, 4 * rest.vectors());
+    s->launches++;
+    s->dp.gate = 2;
+    launch_scan_any_r(s, DHSA_SCAN_TEST_RED, rest);
+    s->dp.gate = 1;
+    launch_scan_any_r(s, DHSA_SCAN_FLOW_CACHE, rest);
+    s->dp.gate = 0;
+}
+
 // Launches the scan of n device-resident packets on s->stream (lock held).
 static int scan_locked(dhsa_sketch *s, const uint32_t *cand, const uint32_t *opp, uint64_t n)
 {
@@ -944,23 +965,12 @@ static int scan_locked(dhsa_sketch *s, const uint32_t *cand, const uint32_t *opp
         src.cand4 = reinterpret_cast<const uint4 *>(cand);
         src.opp4 = reinterpret_cast<const uint4 *>(opp);
         src.nvec = n / 4;
-        if (s->scan_mode == DHSA_SCAN_AUTO && mode == DHSA_SCAN_FLOW_CACHE && !s->auto_cache_trusted && n >= kGatedLaunchMin) {
-            // one long launch and no evidence yet that flows repeat: the host cannot look at the counters in the
-            // middle of it, so the device decides (k_auto_decide): a sample through the cache, then the rest through
-            // whichever kernel the sample's projected hit rate calls for.  38 instead of 15 Gpps on an all-distinct
-            // window; three short extra launches on one that repeats, and only until a window has shown repeats.
+        if (wants_gated_launch(s, mode, n)) {
             const uint64_t head = DHSA_GATE_SAMPLE / 4;
             SoaSource rest = src;
             rest.cand4 += head, rest.opp4 += head, rest.nvec -= head;
             src.nvec = head;
-            launch_scan_any_r(s, DHSA_SCAN_FLOW_CACHE, src);
-            k_auto_decide<<<1, 1, 0, s->stream>>>(s->fc_stats, 4 * rest.nvec);
-            s->launches++;
-            s->dp.gate = 2;
-            launch_scan_any_r(s, DHSA_SCAN_TEST_RED, rest);
-            s->dp.gate = 1;
-            launch_scan_any_r(s, DHSA_SCAN_FLOW_CACHE, rest);
-            s->dp.gate = 0;
+            launch_scan_gated(s, src, rest);
             src.nvec += rest.nvec;
         } else {
             launch_scan_any_r(s, mode, src);
@@ -1006,7 +1016,15 @@ static int scan_records_locked(dhsa_sketch *s, const uint8_t *records, uint64_t 
             src.cand_is_dst = cand_is_dst;
             src.tally = s->tally;
             src.tally_late = tally_late;
-            launch_scan_any_r(s, mode, src);
+            if (wants_gated_launch(s, mode, 4 * src.nquads)) {
+                const uint64_t head = DHSA_GATE_SAMPLE / 4;
+                RecordSource rest = src;
+                rest.rec4 += 3 * head, rest.nquads -= head, rest.first_rec += 4 * head;
+                src.nquads = head;
+                launch_scan_gated(s, src, rest);
+            } else {
+                launch_scan_any_r(s, mode, src);
+            }
             if (int rc = after_fast_scan_locked(s, mode)) return rc;
             covered_hi = 4 * q_end < rec_hi ? 4 * q_end : rec_hi;
         }

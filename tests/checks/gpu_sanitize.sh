@@ -76,6 +76,17 @@ ora2 = O.OracleSketch(k=15, alpha=6)
 ora2.update_batch(dc, do, threads=8)
 sk.update_batch(torch.from_numpy(dc.view(np.int32)).cuda(), torch.from_numpy(do.view(np.int32)).cuda())
 assert np.array_equal(sk.bits, ora2.bits) and sk.flow_cache_stats()[0] == 1 << 20
+# ... and the same through the record form (gated RecordSource instantiations): one window of 8.6M all-distinct records
+rec = np.empty(len(dc), dtype=P.TRACE_DTYPE)
+rec["ts"], rec["src"], rec["dst"] = 900 + (np.arange(len(dc)) % 300), dc, do
+seen = []
+try:
+    P.DetectionEngine(P.WindowConfig(theta=1024, dhg=P.DhgParams(k=15, alpha=6)), chunk_records=1 << 24).run(
+        torch.from_numpy(rec.view(np.uint8).reshape(-1).copy()).cuda(),
+        on_sealed=lambda q: seen.append((q.flow_cache_stats()[0], bool(np.array_equal(q.bits, ora2.bits)))))
+except P.CapacityError:
+    pass
+assert seen == [(1 << 20, True)], seen
 print("sanitizer run ok:", [len(r.reports) for r in res], n_pairs, n_hosts)
 PY
 for tool in memcheck racecheck synccheck; do

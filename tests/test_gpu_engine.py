@@ -129,3 +129,32 @@ def test_records_scan_bits_equal_pair_scan_for_unaligned_segments():
         if direction in (1, 2):
             ora.update_batch(dst, src)
         assert np.array_equal(sk.bits, ora.bits), (direction, lo, hi)
+
+
+def test_auto_mode_decides_on_the_device_for_a_long_record_segment():
+    """One window of 9M all-distinct records handed over in one device buffer: the segment's scan is sampled and gated
+    on the device like a long pair launch (k_auto_decide + the gated RecordSource instantiations) -- only the sample
+    consults the flow cache -- and the sealed sketch equals the oracle's."""
+    import torch
+
+    n = 9_000_000
+    cand, opp = O.distinct_pairs(n, 95)
+    rec = np.empty(n, dtype=P.TRACE_DTYPE)
+    rec["ts"] = 3 * 300 + (np.arange(n) % 300)
+    rec["src"], rec["dst"] = cand, opp
+    ora = O.OracleSketch()
+    ora.update_batch(cand, opp, threads=8)
+    dev = torch.from_numpy(rec.view(np.uint8).reshape(-1).copy()).cuda()
+    seen = []
+
+    def sealed(sk):
+        seen.append((sk.window_id, sk.flow_cache_stats(), bool(np.array_equal(sk.bits, ora.bits))))
+
+    try:
+        res = P.DetectionEngine(P.WindowConfig(theta=1024), chunk_records=1 << 24).run(dev, on_sealed=sealed)
+    except P.CapacityError:
+        res = None                                   # 9M distinct flows make every cell hot, as in the reference
+    assert len(seen) == 1
+    window_id, (lookups, hits), same = seen[0]
+    assert window_id == 3 and same
+    assert lookups == 1 << 20 and hits * 10 < lookups
