@@ -81,19 +81,21 @@ class DeviceBits(np.ndarray):
     """
 
     _sketch = None  # the Dhla a write goes back to
-    _root = None    # the whole (r, 2^k, g/8) mirror this array is (a view of)
+    _root = None    # a view: the whole (r, 2^k, g/8) mirror it is a view of; the mirror itself: None (a reference to
+                    # itself would be a cycle: 10 MiB per `sketch.bits`, and the sketch behind it, kept until the
+                    # cyclic collector runs)
 
     def __array_finalize__(self, obj):
         if isinstance(obj, DeviceBits) and obj._sketch is not None and self.base is not None \
                 and np.shares_memory(self, obj):
-            self._sketch, self._root = obj._sketch, obj._root
+            self._sketch, self._root = obj._sketch, (obj if obj._root is None else obj._root)
         else:
             self._sketch = self._root = None
 
     def __setitem__(self, key, value):
         super().__setitem__(key, value)
         if self._sketch is not None:
-            self._sketch.load_bits(np.asarray(self._root))
+            self._sketch.load_bits(np.asarray(self if self._root is None else self._root))
 
     def __reduce__(self):  # pickles as a plain array: a handle to a device sketch does not travel
         return np.asarray(self).__reduce__()
@@ -206,7 +208,7 @@ class Dhla:
         out = np.empty((p.r, p.index_count, p.g // 8), dtype=np.uint8)
         _cabi.check(self._lib.dhsa_download_bits(self._h, out.ctypes.data, out.nbytes))
         mirror = out.view(DeviceBits)
-        mirror._sketch, mirror._root = self, mirror
+        mirror._sketch = self          # _root stays None: this IS the root
         return mirror
 
     def estimator(self, i: int, j: int) -> np.ndarray:

@@ -223,7 +223,7 @@ def test_bits_mirror_writes_through_and_copies_detach():
         @property
         def bits(self):
             m = self.dev.copy().view(DeviceBits)
-            m._sketch, m._root = self, m
+            m._sketch = self                 # as Dhla.bits builds it: the root carries no reference to itself
             return m
 
     s = Sketch()
@@ -243,6 +243,25 @@ def test_bits_mirror_writes_through_and_copies_detach():
     import pickle
 
     assert type(pickle.loads(pickle.dumps(s.bits))) is np.ndarray
+    # a mirror (and the sketch it points to) goes away with its last reference, not with the next cyclic collection:
+    # `sketch.bits` per window must not pile up 10 MiB arrays and device sketches
+    import gc
+    import weakref
+
+    gc.disable()
+    try:
+        t = Sketch()
+        mirror = t.bits
+        row = mirror[1]
+        probe_m, probe_s = weakref.ref(mirror), weakref.ref(t)
+        del mirror
+        assert probe_m() is not None                 # the view keeps its root alive (it uploads the whole mirror)
+        row[0, 0] = 3
+        assert t.dev[1, 0, 0] == 3
+        del row, t
+        assert probe_m() is None and probe_s() is None
+    finally:
+        gc.enable()
 
 
 def test_exceptions_derive_from_the_reference_classes_when_it_is_importable():
