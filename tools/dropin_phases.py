@@ -27,4 +27,9 @@ for w in range(int(sys.argv[1]) if len(sys.argv) > 1 else 6):
     got = s.restore(); t.append(time.perf_counter())
     del s; t.append(time.perf_counter())
     ms = [round((b - a) * 1e3, 2) for a, b in zip(t[:-1], t[1:])]
-    print(dict(zip(("create", "feed", "seal", "restore", "destroy"), ms)), "Gpps", round(n / (t[4] - t[0]) / 1e9, 2), len(got), flush=True)
+    if w < 8 or w % 50 == 0:
+        import psutil
+        import torch
+        free, total = torch.cuda.mem_get_info()
+        print(dict(zip(("create", "feed", "seal", "restore", "destroy"), ms)), "Gpps", round(n / (t[4] - t[0]) / 1e9, 2), len(got),
+              "RSS MiB", psutil.Process().memory_info().rss >> 20, "device MiB", (total - free) >> 20, flush=True)
