@@ -357,6 +357,33 @@ def test_auto_mode_is_not_fooled_by_a_cold_table():
     assert sha(sk.bits) == sha(ora.bits)
 
 
+def test_reading_bits_does_not_keep_sketches_alive():
+    """A sketch per window whose `bits` are read (what `dhsa bench` does, pkg/src/dhsa/cli.py:383): mirror and sketch
+    must go with their last reference, without the cyclic collector -- 60 windows may not pile up 60 sketches."""
+    import gc
+
+    import torch
+
+    def used():
+        free, total = torch.cuda.mem_get_info()
+        return (total - free) >> 20
+
+    cand, opp = O.distinct_pairs(50_000, 3)
+    gc.collect()
+    gc.disable()
+    try:
+        for w in range(60):
+            sk = P.Dhla(P.DhgParams(), window_id=w)
+            sk.update_batch(cand, opp)
+            assert sk.bits.any() and sk.bits[0].shape == (1 << 14, 128)
+            if w == 5:
+                base = used()                    # the parked sketches and their caches exist by now
+            del sk
+        assert used() - base < 256, (base, used())   # MiB; 54 leaked sketches would hold > 2 GiB
+    finally:
+        gc.enable()
+
+
 def test_estimator_returns_one_cell():
     # pkg/src/dhsa/dhla.py:107-109
     sk = P.Dhla(P.DhgParams(**PARAM_SETS["small"]))
